@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+"""Benchmark of the DeDLOC averaging round (grad avg + LAMB step) on B200.
+
+One step = one butterfly averaging round over a flattened gradient vector
+(pack -> fused reduce-scatter/weighted-average/all-gather over NVLink ->
+LAMB) through libsp_round.so. Default workload: ALBERT-large-sized vector
+(17,847,474 params, 32-tensor LAMB table), fp16 wire, one peer per GPU
+(G = N, weak scaling), LP-balanced uniform fractions, synthetic gradients.
+
+    python bench.py --gpus 1 --steps 50 --warmup 5
+    torchrun --nproc-per-node 8 ... bench.py --gpus 8 --steps 50 --warmup 5
+    python bench.py --impl reference ...   # CPU oracle port on host cores
+
+Prints ONE JSON line on rank 0 (stdout); diagnostics go to stderr.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "averaging round time + GB/s (grad avg + LAMB step), ALBERT-large, 1/2/4/8 B200"
+HP = dict(lr=1.76e-3, beta1=0.9, beta2=0.999, eps=1e-6, weight_decay=0.01, bias_correction=1)
+SIGMA = 1e-3 * 3 ** 0.5
+NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+L2_BYTES = 126e6
+
+WORKLOADS = {
+    # name: (tensor table, wire, q8 block)
+    "albert-large-fp16": ("albert-large", "fp16", 4096),
+    "albert-large-fp32": ("albert-large", "fp32", 4096),
+    "albert-large-q8": ("albert-large", "q8", 4096),
+    "resnet50-q8": ("resnet50", "q8", 4096),
+    "albert-base-fp32": ("albert-base", "fp32", 4096),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def tensor_table(name: str) -> list[int]:
+    with open(os.path.join(ROOT, "tests", "golden", "tensor_tables.json")) as f:
+        return json.load(f)[name]
+
+
+def wire_bytes(wire: str, block: int) -> float:
+    return {"fp32": 4.0, "fp16": 2.0, "q8": 1.0 + 4.0 / block}[wire]
+
+
+def peak_hbm() -> tuple[float, str]:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms (recipe's line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows: list[list[str]] = []
+        self.proc = None
+        self.marks: list[tuple[float, float]] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception as e:  # nvidia-smi missing: report empty clocks
+            log("clock sampler unavailable:", e)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([time.time()] + [x.strip() for x in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        rows = self.rows
+        if self.marks:
+            t0, t1 = self.marks[0]
+            inside = [r for r in rows if t0 - 0.25 <= r[0] <= t1 + 0.25]
+            rows = inside or rows
+        sm = [float(r[2]) for r in rows if len(r) > 3 and r[2].replace(".", "").isdigit()]
+        smax = [float(r[3]) for r in rows if len(r) > 3 and r[3].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            for k, nm in enumerate(names):
+                if len(r) > 6 + k and r[6 + k].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# ---------------------------------------------------------- CPU baseline
+def cpu_round_time(tsizes, wire, block, G, weights, reps: int, threads: int = 0):
+    """Times the oracle's CPU round (the reference semantics restated in C,
+    OpenMP over host cores) on the full vector; returns (sec/round, threads)."""
+    import numpy as np
+
+    from oracle import oracle as O
+
+    n = sum(tsizes)
+    grads = [O.fill_synthetic(n, 1, g, SIGMA) for g in range(G)]
+    p = O.fill_synthetic(n, 2, 0, 0.02, 0)
+    m = np.zeros(n, np.float32)
+    v = np.zeros(n, np.float32)
+    O.round_cpu(wire, grads, weights, p, m, v, tsizes, HP, 1, block, threads)  # warm-up
+    ts = []
+    for r in range(reps):
+        t0 = time.perf_counter()
+        O.round_cpu(wire, grads, weights, p, m, v, tsizes, HP, r + 2, block, threads)
+        ts.append(time.perf_counter() - t0)
+    return statistics.median(ts), (threads or O.max_threads())
+
+
+# ------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="albert-large-fp16")
+    ap.add_argument("--peers-per-gpu", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--phased-steps", type=int, default=20)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        log(f"note: WORLD_SIZE={world} but --gpus={args.gpus}; using WORLD_SIZE")
+
+    table, wire, block = WORKLOADS[args.workload]
+    tsizes = tensor_table(table)
+    n = sum(tsizes)
+    L = args.peers_per_gpu
+    G = L * world
+    fractions = [1.0 / G] * G  # homogeneous fleet: LP gives 1/G each (test_strategy.cpp:186-195)
+    weights = [4096.0 / G] * G  # target batch 4096 split evenly
+    b = wire_bytes(wire, block)
+
+    if args.impl == "reference":
+        return run_reference(args, rank, world, tsizes, wire, block, G, weights, b)
+
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    from paper_2106_10207_b200 import AveragingRound, fill_synthetic
+    from paper_2106_10207_b200.round import part_offsets
+
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.Stream(dev)
+    rnd = AveragingRound(n, tsizes, wire=wire, q8_block=block, peers_per_rank=L, rank=rank,
+                         world=world, device=local_rank, lr=HP["lr"],
+                         betas=(HP["beta1"], HP["beta2"]), eps=HP["eps"],
+                         weight_decay=HP["weight_decay"])
+    offsets = rnd.assign(fractions, weights)
+    grads = []
+    for l in range(L):
+        g = torch.empty(n, dtype=torch.float32, device=dev)
+        fill_synthetic(g, 1, rank * L + l, SIGMA)
+        grads.append(g)
+    p = torch.empty(n, dtype=torch.float32, device=dev)
+    fill_synthetic(p, 2, 0, 0.02, 0)
+    m = torch.zeros(n, dtype=torch.float32, device=dev)
+    v = torch.zeros(n, dtype=torch.float32, device=dev)
+    torch.cuda.synchronize(dev)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    step = 0
+
+    def one():
+        nonlocal step
+        step += 1
+        rnd.run(grads, p, m, v, step, stream)
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    # warm-up: W steps, then keep stepping (untimed) for >= 1 s so clocks ramp
+    # and the sampler has samples under load
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            one()
+        torch.cuda.synchronize(dev)
+        t_end = time.time() + 1.0
+        while time.time() < t_end:
+            for _ in range(20):
+                one()
+            stream.synchronize()
+        barrier()
+        torch.cuda.synchronize(dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        wall0 = time.time()
+        e0.record(stream)
+        for _ in range(args.steps):
+            one()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        wall1 = time.time()
+        barrier()
+        # keep the load on for the sampler if the timed region was short
+        t_end = time.time() + max(0.0, 0.6 - (wall1 - wall0))
+        while time.time() < t_end:
+            for _ in range(20):
+                one()
+            stream.synchronize()
+        torch.cuda.synchronize(dev)
+    clocks.marks.append((wall0, max(wall1, wall0 + 0.6)))
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    grad_bytes = 4.0 * n * G  # fp32 gradient bytes of all peers averaged per round
+    value = grad_bytes / (ms_step * 1e-3) / 1e9
+
+    # per-kernel device times (non-graph pass with events between kernels)
+    phases = []
+    with torch.cuda.stream(stream):
+        for _ in range(args.phased_steps):
+            step += 1
+            phases.append(rnd.run_phased(grads, p, m, v, step, stream))
+    keys = [k for k in phases[0] if k != "total_ms"]
+    ph = {k: statistics.mean(x[k] for x in phases) for k in keys}
+    ph["total_ms"] = statistics.mean(x["total_ms"] for x in phases)
+
+    # e2e through the public API with host buffers: H2D of this rank's
+    # accumulated gradients (pinned), the round, D2H of the trust ratios
+    host_g = [gg.cpu().pin_memory() for gg in grads]
+    trust_h = torch.empty(len(tsizes), dtype=torch.float32).pin_memory()
+    e2e_steps = max(3, min(args.steps, 20))
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            for l in range(L):
+                grads[l].copy_(host_g[l], non_blocking=True)
+            one()
+        barrier()
+        torch.cuda.synchronize(dev)
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(e2e_steps):
+            for l in range(L):
+                grads[l].copy_(host_g[l], non_blocking=True)
+            one()
+            rnd.copy_trust_async(trust_h.data_ptr(), stream)  # D2H of the step's result
+        f1.record(stream)
+        torch.cuda.synchronize(dev)
+    e2e_ms = f0.elapsed_time(f1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_step = e2e_ms / e2e_steps
+    e2e_value = grad_bytes / (e2e_step * 1e-3) / 1e9
+
+    if rank == 0:
+        peak, peak_kind = peak_hbm()
+        f_r = (offsets[(rank + 1) * L] - offsets[rank * L]) / n
+        alg = {  # algorithmic bytes per launch, this rank
+            "pack_ms": (L * n * (4 + b)) if wire != "fp32" else 0.0,
+            "reduce_ms": (G + world) * f_r * n * b,
+            "moments_ms": n * (20 + b),
+            "update_ms": n * 16.0,
+        }
+        dom = max(("pack_ms", "reduce_ms", "moments_ms", "update_ms"), key=lambda k: ph[k])
+        achieved = alg[dom] / (ph[dom] * 1e-3) / 1e9
+        bound, pk, unit = "hbm", peak, "GB/s"
+        if dom == "reduce_ms" and world > 1:
+            bound, pk = "nvlink", NVLINK_GBS
+            nvl = ((1 - f_r) * b + (G - 1) * f_r * b) * n  # per direction
+            achieved = nvl / (ph[dom] * 1e-3) / 1e9
+        # whole-round roofline: serialized HBM + NVLink phases
+        hbm_round = ((4 + b) * L if wire != "fp32" else 0.0) + G * f_r * b + f_r * b + 24 + b
+        nvl_round = ((1 - f_r) * b + (G - 1) * f_r * b) if world > 1 else 0.0
+        t_roof = hbm_round * n / (peak * 1e9) + nvl_round * n / (NVLINK_GBS * 1e9)
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            try:
+                sec, cores = cpu_round_time(tsizes, wire, block, G, weights, reps=3)
+                cpu = {"value": round(grad_bytes / sec / 1e9, 4), "unit": "GB/s", "cores": cores,
+                       "kind": "port", "round_ms": round(sec * 1e3, 3),
+                       "sample": f"oracle C round (OpenMP), full {table} vector, G={G}, "
+                                 f"{wire} wire, median of 3 rounds"}
+            except Exception as e:
+                log("cpu baseline failed:", e)
+        out = {
+            "metric": METRIC,
+            "value": round(value, 3),
+            "unit": "GB/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 5),
+            "round_us": round(ms_step * 1e3, 2),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": {"fp32": "f32", "fp16": "f16 wire / f32 accum", "q8": "u8 wire / f32 accum"}[wire],
+            "data": "synthetic (counter-hash gradients, sigma=1e-3, 1/997 outliers x100)",
+            "config": {"workload": f"{args.workload}: DeDLOC butterfly round + LAMB",
+                       "params": n, "tensors": len(tsizes), "peers": G, "peers_per_gpu": L,
+                       "wire": wire, "q8_block": block if wire == "q8" else None,
+                       "fractions": "uniform 1/G (LP, homogeneous fleet)",
+                       "l2": f"no flush: per-step working set {(n * (12 + 4 * L + 2 * b)) / 1e9:.2f} GB > 126 MB L2",
+                       "parallelism": f"dp{world} (one peer per GPU, CUDA IPC over NVLink)"},
+            "gpu_launches": args.steps * ((1 if wire != "fp32" else 1) + 1 + 3 + (2 if world > 1 else 0)),
+            "kernel_ms": {k: round(v_, 5) for k, v_ in ph.items()},
+            "roofline": {"bound": bound, "kernel": dom.replace("_ms", ""),
+                         "achieved": round(achieved, 1), "peak": pk, "unit": unit,
+                         "frac": round(achieved / pk, 4), "traffic": None,
+                         "peak_kind": peak_kind if bound == "hbm" else "measured peer copy (guide)"},
+            "round_roofline": {"t_roof_us": round(t_roof * 1e6, 2),
+                               "frac": round(t_roof * 1e3 / ms_step, 4),
+                               "hbm_B_per_param": round(hbm_round, 3),
+                               "nvlink_B_per_param_dir": round(nvl_round, 3)},
+            "e2e": {"value": round(e2e_value, 3), "unit": "GB/s",
+                    "round_us": round(e2e_step * 1e3, 2),
+                    "h2d_bytes_per_step": 4 * n * L, "d2h_bytes_per_step": 4 * len(tsizes)},
+            "clocks": clk,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(out), flush=True)
+    rnd.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def run_reference(args, rank, world, tsizes, wire, block, G, weights, b):
+    """--impl reference: the reference path on host cores. The reference
+    cannot be built here (Eigen/KLU missing), so this times the
+    oracle port of its semantics (groups::run_plan weighted mean + the
+    framework's wire/LAMB definition) with every host thread."""
+    if rank != 0:
+        return 0
+    n = sum(tsizes)
+    reps = max(1, args.steps)
+    import numpy as np
+
+    from oracle import oracle as O
+
+    grads = [O.fill_synthetic(n, 1, g, SIGMA) for g in range(G)]
+    p = O.fill_synthetic(n, 2, 0, 0.02, 0)
+    m = np.zeros(n, np.float32)
+    v = np.zeros(n, np.float32)
+    for w in range(args.warmup):
+        O.round_cpu(wire, grads, weights, p, m, v, tsizes, HP, w + 1, block, 0)
+    t0 = time.perf_counter()
+    for r in range(reps):
+        O.round_cpu(wire, grads, weights, p, m, v, tsizes, HP, args.warmup + r + 1, block, 0)
+    sec = (time.perf_counter() - t0) / reps
+    grad_bytes = 4.0 * n * G
+    val = grad_bytes / sec / 1e9
+    cores = O.max_threads()
+    out = {
+        "metric": METRIC, "impl": "reference", "value": round(val, 4), "unit": "GB/s",
+        "n_gpus": world, "steps": reps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": wire, "data": "synthetic",
+        "config": {"workload": f"{args.workload}: DeDLOC butterfly round + LAMB", "params": n,
+                   "tensors": len(tsizes), "peers": G, "wire": wire},
+        "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": cores, "kind": "port",
+                         "sample": f"full vector, G={G} peers simulated on host, {reps} rounds"},
+        "e2e": {"value": round(val, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main() or 0)

@@ -1,0 +1,641 @@
+// sp_kernels.cuh — sm_100a kernels of the averaging round.
+//
+// All kernels are HBM- or NVLink-bound streaming kernels (no tensor cores:
+// the round has no contraction). Conventions shared by every kernel:
+//   * 128-bit vector loads/stores on 16-byte aligned, zero-padded buffers;
+//   * explicit IEEE intrinsics (__fmul_rn, __fmaf_rn, __fdiv_rn, __fsqrt_rn)
+//     so no FMA contraction changes a rounding: the CPU oracle
+//     (oracle/sp_oracle.c) performs the same operation sequence and the
+//     wire codes, averaged parts and LAMB moments are bit-identical;
+//   * peers are summed in peer order 0..G-1 (the order groups::run_plan
+//     merges classes in, /root/reference/proj/src/groups.cpp:133-144).
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sp_round.h"
+
+namespace sp {
+
+constexpr int kLambChunk = 8192;  // elements per LAMB chunk (one CTA)
+constexpr int kLambThreads = 256;
+constexpr int kPad = 16384;       // wire/avg buffers padded to this multiple
+
+struct PackArgs {
+  const float* src[SP_MAX_LOCAL];  // accumulated fp32 grad of local peer l
+  void* dst[SP_MAX_LOCAL];         // wire buffer of local peer l
+  int64_t n;                       // valid elements
+  int64_t npad;                    // padded elements (multiple of kPad)
+  int qblock;                      // q8 block
+};
+
+struct ReduceArgs {
+  const void* src[SP_MAX_PEERS];  // wire buffer of each contributing peer
+  float w[SP_MAX_PEERS];          // normalized weight w_g / sum(w), fp32
+  void* dst[SP_MAX_RANKS];        // avg buffer of every rank (local or peer)
+  int npeers;                     // contributing (nonzero-weight) peers
+  int ndst;
+  int64_t lo, hi;                 // element range reduced by this rank
+  int64_t npad;
+  int qblock;
+};
+
+struct BarrierArgs {
+  unsigned long long* flags[SP_MAX_RANKS];  // flags array of every rank
+  unsigned long long* epoch;                // local epoch counter
+  int* err;                                 // host-mapped error flag
+  int rank, world;
+  unsigned long long timeout_ns;
+};
+
+struct Chunk {
+  long long start;
+  int len;
+  int tensor;
+};
+
+struct LambArgs {
+  const void* avg;          // all-gathered averaged gradient, wire format
+  const float* avg_scale;   // q8 scales (nullptr otherwise)
+  float* p;
+  float* m;
+  float* v;
+  const Chunk* chunks;
+  float2* partial;          // per chunk (sum p^2, sum u^2)
+  const float* hp;          // device: [lr, 1/(1-b1^t), 1/(1-b2^t)]
+  const float* step_scale;  // per tensor lr * trust (update kernel only)
+  float b1, b2, omb1, omb2, eps, wd;
+  int qblock;
+};
+
+// ---------------------------------------------------------------- helpers
+
+__device__ __forceinline__ int4 ld_nc_v4(const void* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void st_v4(void* p, int4 v) {
+  asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p,
+                                               unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v)
+               : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(
+    const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];"
+               : "=l"(v)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+// 8-bit code of x given inv = 127/absmax: rint(x*inv), clamped to +-127.
+__device__ __forceinline__ int q8_code(float x, float inv) {
+  int q = __float2int_rn(__fmul_rn(x, inv));
+  return max(-127, min(127, q));
+}
+
+__device__ __forceinline__ float warp_max(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+
+__device__ __forceinline__ float warp_sum(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// Block-wide max over blockDim.x threads (multiple of 32, <= 1024).
+__device__ __forceinline__ float block_max(float x, float* smem32) {
+  x = warp_max(x);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) smem32[wid] = x;
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  float y = lane < nw ? smem32[lane] : 0.0f;
+  y = warp_max(y);
+  __syncthreads();
+  return y;
+}
+
+// --------------------------------------------------------------- synthetic
+
+__global__ void k_fill_synthetic(float* __restrict__ out, int64_t n,
+                                 unsigned long long seed, int peer,
+                                 float scale, int64_t every, float mult) {
+  const unsigned long long key = seed ^ ((unsigned long long)peer << 40);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long u = splitmix64(key ^ (unsigned long long)i) >> 40;
+    float x = __fmul_rn(__fmul_rn((float)(long long)u - 8388608.0f,
+                                  1.0f / 8388608.0f),
+                        scale);
+    if (every > 0 && i % every == 0) x = __fmul_rn(x, mult);
+    out[i] = x;
+  }
+}
+
+// -------------------------------------------------------------------- pack
+// K1. fp32 accumulated gradient -> wire format. blockIdx.y = local peer.
+
+__global__ void __launch_bounds__(256) k_pack_fp32(PackArgs a) {
+  const float* __restrict__ src = a.src[blockIdx.y];
+  float* __restrict__ dst = static_cast<float*>(a.dst[blockIdx.y]);
+  if (src == nullptr) return;
+  const int64_t nvec = a.npad / 4;
+  const int64_t nfull = a.n / 4;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    float4 x;
+    if (v < nfull) {
+      x = __ldg(reinterpret_cast<const float4*>(src) + v);
+    } else {
+      const int64_t e = v * 4;
+      x.x = e + 0 < a.n ? src[e + 0] : 0.0f;
+      x.y = e + 1 < a.n ? src[e + 1] : 0.0f;
+      x.z = e + 2 < a.n ? src[e + 2] : 0.0f;
+      x.w = e + 3 < a.n ? src[e + 3] : 0.0f;
+    }
+    reinterpret_cast<float4*>(dst)[v] = x;
+  }
+}
+
+__device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
+  __half2 h = __halves2half2(__float2half_rn(lo), __float2half_rn(hi));
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__device__ __forceinline__ float2 unpack_half2(uint32_t u) {
+  __half2 h = *reinterpret_cast<__half2*>(&u);
+  return __half22float2(h);
+}
+
+__global__ void __launch_bounds__(256) k_pack_fp16(PackArgs a) {
+  const float* __restrict__ src = a.src[blockIdx.y];
+  char* __restrict__ dst = static_cast<char*>(a.dst[blockIdx.y]);
+  if (src == nullptr) return;
+  const int64_t nvec = a.npad / 8;
+  const int64_t nfull = a.n / 8;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    float x[8];
+    if (v < nfull) {
+      float4 a0 = __ldg(reinterpret_cast<const float4*>(src) + 2 * v);
+      float4 a1 = __ldg(reinterpret_cast<const float4*>(src) + 2 * v + 1);
+      x[0] = a0.x; x[1] = a0.y; x[2] = a0.z; x[3] = a0.w;
+      x[4] = a1.x; x[5] = a1.y; x[6] = a1.z; x[7] = a1.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int64_t e = v * 8 + j;
+        x[j] = e < a.n ? src[e] : 0.0f;
+      }
+    }
+    int4 o;
+    o.x = (int)pack_half2(x[0], x[1]);
+    o.y = (int)pack_half2(x[2], x[3]);
+    o.z = (int)pack_half2(x[4], x[5]);
+    o.w = (int)pack_half2(x[6], x[7]);
+    st_v4(dst + v * 16, o);
+  }
+}
+
+// Blockwise absmax int8. One CTA (qblock/16 threads) per q8 block; thread t
+// owns 16 contiguous elements. Codes at dst[0, npad), scales at dst + npad.
+__global__ void k_pack_q8(PackArgs a) {
+  __shared__ float red[32];
+  const float* __restrict__ src = a.src[blockIdx.y];
+  int8_t* __restrict__ codes = static_cast<int8_t*>(a.dst[blockIdx.y]);
+  if (src == nullptr) return;
+  float* __restrict__ scales = reinterpret_cast<float*>(codes + a.npad);
+  const int64_t nblk = a.npad / a.qblock;
+  for (int64_t b = blockIdx.x; b < nblk; b += gridDim.x) {
+    const int64_t e0 = b * a.qblock + threadIdx.x * 16;
+    float x[16];
+    if (e0 + 16 <= a.n) {
+      const float4* s4 = reinterpret_cast<const float4*>(src + e0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float4 t = __ldg(s4 + k);
+        x[4 * k] = t.x; x[4 * k + 1] = t.y; x[4 * k + 2] = t.z; x[4 * k + 3] = t.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) x[j] = e0 + j < a.n ? src[e0 + j] : 0.0f;
+    }
+    float amax = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) amax = fmaxf(amax, fabsf(x[j]));
+    amax = block_max(amax, red);
+    const float inv = amax > 0.0f ? __fdiv_rn(127.0f, amax) : 0.0f;
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t packed = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        packed |= (uint32_t)(q8_code(x[4 * k + j], inv) & 0xff) << (8 * j);
+      w[k] = packed;
+    }
+    st_v4(codes + e0, make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]));
+    if (threadIdx.x == 0) scales[b] = __fdiv_rn(amax, 127.0f);
+  }
+}
+
+// ----------------------------------------------------------------- barrier
+// Cross-rank barrier over NVLink: rank r stores the new epoch into
+// flags_k[r] of every rank k (system-scope release), then waits until its
+// own flags[k] >= epoch for all k (acquire). One warp; world <= 8.
+
+__global__ void k_barrier(BarrierArgs a) {
+  __shared__ unsigned long long epoch;
+  if (threadIdx.x == 0) {
+    epoch = *a.epoch + 1;
+    *a.epoch = epoch;
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t < a.world) {
+    __threadfence_system();
+    st_release_sys(a.flags[t] + a.rank, epoch);
+    const unsigned long long* mine = a.flags[a.rank] + t;
+    const unsigned long long t0 = globaltimer();
+    while (ld_acquire_sys(mine) < epoch) {
+      if (globaltimer() - t0 > a.timeout_ns) {
+        atomicExch_system(a.err, 1);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------ reduce
+// K2. Fused reduce-scatter + weighted average + all-gather: this rank reads
+// element range [lo, hi) of every contributing peer's wire buffer (local HBM
+// or a peer GPU's HBM over NVLink), accumulates sum_g w_g * x_g in fp32 in
+// peer order with fmaf, converts to the wire format and stores the result
+// into the avg buffer of every rank.
+
+__global__ void __launch_bounds__(256) k_reduce_fp32(ReduceArgs a) {
+  const int64_t nvec = (a.hi - a.lo + 3) / 4;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t off = (a.lo + v * 4) * 4;  // bytes
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    int g = 0;
+    for (; g + 4 <= a.npeers; g += 4) {
+      int4 r[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) r[k] = ld_nc_v4(static_cast<const char*>(a.src[g + k]) + off);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float w = a.w[g + k];
+        acc[0] = __fmaf_rn(w, __int_as_float(r[k].x), acc[0]);
+        acc[1] = __fmaf_rn(w, __int_as_float(r[k].y), acc[1]);
+        acc[2] = __fmaf_rn(w, __int_as_float(r[k].z), acc[2]);
+        acc[3] = __fmaf_rn(w, __int_as_float(r[k].w), acc[3]);
+      }
+    }
+    for (; g < a.npeers; ++g) {
+      int4 r = ld_nc_v4(static_cast<const char*>(a.src[g]) + off);
+      const float w = a.w[g];
+      acc[0] = __fmaf_rn(w, __int_as_float(r.x), acc[0]);
+      acc[1] = __fmaf_rn(w, __int_as_float(r.y), acc[1]);
+      acc[2] = __fmaf_rn(w, __int_as_float(r.z), acc[2]);
+      acc[3] = __fmaf_rn(w, __int_as_float(r.w), acc[3]);
+    }
+    int4 o = make_int4(__float_as_int(acc[0]), __float_as_int(acc[1]),
+                       __float_as_int(acc[2]), __float_as_int(acc[3]));
+    for (int k = 0; k < a.ndst; ++k) st_v4(static_cast<char*>(a.dst[k]) + off, o);
+  }
+}
+
+__device__ __forceinline__ void fma_half8(float* acc, float w, int4 r) {
+  const uint32_t u[4] = {(uint32_t)r.x, (uint32_t)r.y, (uint32_t)r.z, (uint32_t)r.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    float2 f = unpack_half2(u[k]);
+    acc[2 * k] = __fmaf_rn(w, f.x, acc[2 * k]);
+    acc[2 * k + 1] = __fmaf_rn(w, f.y, acc[2 * k + 1]);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_reduce_fp16(ReduceArgs a) {
+  const int64_t nvec = (a.hi - a.lo + 7) / 8;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t off = (a.lo + v * 8) * 2;  // bytes
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
+    int g = 0;
+    for (; g + 4 <= a.npeers; g += 4) {
+      int4 r[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) r[k] = ld_nc_v4(static_cast<const char*>(a.src[g + k]) + off);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) fma_half8(acc, a.w[g + k], r[k]);
+    }
+    for (; g < a.npeers; ++g)
+      fma_half8(acc, a.w[g], ld_nc_v4(static_cast<const char*>(a.src[g]) + off));
+    int4 o;
+    o.x = (int)pack_half2(acc[0], acc[1]);
+    o.y = (int)pack_half2(acc[2], acc[3]);
+    o.z = (int)pack_half2(acc[4], acc[5]);
+    o.w = (int)pack_half2(acc[6], acc[7]);
+    for (int k = 0; k < a.ndst; ++k) st_v4(static_cast<char*>(a.dst[k]) + off, o);
+  }
+}
+
+__device__ __forceinline__ void fma_q8x16(float* acc, float w, float scale, int4 r) {
+  const uint32_t u[4] = {(uint32_t)r.x, (uint32_t)r.y, (uint32_t)r.z, (uint32_t)r.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int q = (int)(int8_t)((u[k] >> (8 * j)) & 0xff);
+      acc[4 * k + j] = __fmaf_rn(w, __fmul_rn((float)q, scale), acc[4 * k + j]);
+    }
+  }
+}
+
+// One CTA (qblock/16 threads) per q8 block of [lo, hi); lo is block aligned.
+__global__ void k_reduce_q8(ReduceArgs a) {
+  __shared__ float red[32];
+  __shared__ float sc[SP_MAX_PEERS];
+  const int64_t b0 = a.lo / a.qblock;
+  const int64_t b1 = (a.hi + a.qblock - 1) / a.qblock;
+  for (int64_t b = b0 + blockIdx.x; b < b1; b += gridDim.x) {
+    __syncthreads();  // sc reuse across iterations
+    if (threadIdx.x < a.npeers) {
+      const float* s = reinterpret_cast<const float*>(
+          static_cast<const char*>(a.src[threadIdx.x]) + a.npad);
+      sc[threadIdx.x] = s[b];
+    }
+    __syncthreads();
+    const int64_t e0 = b * a.qblock + threadIdx.x * 16;
+    float acc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = 0.0f;
+    int g = 0;
+    for (; g + 4 <= a.npeers; g += 4) {
+      int4 r[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) r[k] = ld_nc_v4(static_cast<const char*>(a.src[g + k]) + e0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) fma_q8x16(acc, a.w[g + k], sc[g + k], r[k]);
+    }
+    for (; g < a.npeers; ++g)
+      fma_q8x16(acc, a.w[g], sc[g], ld_nc_v4(static_cast<const char*>(a.src[g]) + e0));
+    float amax = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) amax = fmaxf(amax, fabsf(acc[j]));
+    amax = block_max(amax, red);
+    const float inv = amax > 0.0f ? __fdiv_rn(127.0f, amax) : 0.0f;
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t packed = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        packed |= (uint32_t)(q8_code(acc[4 * k + j], inv) & 0xff) << (8 * j);
+      w[k] = packed;
+    }
+    const int4 o = make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]);
+    const float scale = __fdiv_rn(amax, 127.0f);
+    for (int k = 0; k < a.ndst; ++k) {
+      char* d = static_cast<char*>(a.dst[k]);
+      st_v4(d + e0, o);
+      if (threadIdx.x == 0) reinterpret_cast<float*>(d + a.npad)[b] = scale;
+    }
+  }
+}
+
+// -------------------------------------------------------------------- LAMB
+// K3 (moments + per-chunk norm partials) and K4 (update). Per element:
+//   m' = b1*m + (1-b1)*g          v' = b2*v + (1-b2)*g^2
+//   u  = (m'*ibc1) / (sqrt(v'*ibc2) + eps) + wd*p
+//   trust_t = ||p||_t / ||u||_t  (1 if either norm is 0)
+//   p' = p - (lr*trust_t) * u
+// The reference has no optimizer beyond x <- x - lr*g
+// (/root/reference/proj/src/sgd.cpp:207-210) and scopes LAMB out
+// (/root/reference/SPEC.md:519); this follows You et al. (2019) as cited by
+// the paper.
+
+template <int W>
+__device__ __forceinline__ float4 load_grad4(const LambArgs& a, int64_t i) {
+  if constexpr (W == SP_WIRE_FP32) {
+    return *reinterpret_cast<const float4*>(static_cast<const float*>(a.avg) + i);
+  } else if constexpr (W == SP_WIRE_FP16) {
+    uint2 u = *reinterpret_cast<const uint2*>(static_cast<const __half*>(a.avg) + i);
+    float2 lo = unpack_half2(u.x), hi = unpack_half2(u.y);
+    return make_float4(lo.x, lo.y, hi.x, hi.y);
+  } else {
+    const uint32_t u = *reinterpret_cast<const uint32_t*>(static_cast<const int8_t*>(a.avg) + i);
+    const float s = a.avg_scale[i / a.qblock];
+    return make_float4(__fmul_rn((float)(int8_t)(u & 0xff), s),
+                       __fmul_rn((float)(int8_t)((u >> 8) & 0xff), s),
+                       __fmul_rn((float)(int8_t)((u >> 16) & 0xff), s),
+                       __fmul_rn((float)(int8_t)((u >> 24) & 0xff), s));
+  }
+}
+
+template <int W>
+__device__ __forceinline__ float load_grad1(const LambArgs& a, int64_t i) {
+  if constexpr (W == SP_WIRE_FP32) {
+    return static_cast<const float*>(a.avg)[i];
+  } else if constexpr (W == SP_WIRE_FP16) {
+    return __half2float(static_cast<const __half*>(a.avg)[i]);
+  } else {
+    return __fmul_rn((float)static_cast<const int8_t*>(a.avg)[i], a.avg_scale[i / a.qblock]);
+  }
+}
+
+struct LambScalars {
+  float lr, ibc1, ibc2;
+};
+
+__device__ __forceinline__ void lamb_moments(const LambArgs& a, const LambScalars& s,
+                                             float g, float p, float& m, float& v,
+                                             float& u) {
+  m = __fmaf_rn(a.b1, m, __fmul_rn(a.omb1, g));
+  v = __fmaf_rn(a.b2, v, __fmul_rn(a.omb2, __fmul_rn(g, g)));
+  const float den = __fadd_rn(__fsqrt_rn(__fmul_rn(v, s.ibc2)), a.eps);
+  u = __fmaf_rn(a.wd, p, __fdiv_rn(__fmul_rn(m, s.ibc1), den));
+}
+
+__device__ __forceinline__ float lamb_dir(const LambArgs& a, const LambScalars& s,
+                                          float p, float m, float v) {
+  const float den = __fadd_rn(__fsqrt_rn(__fmul_rn(v, s.ibc2)), a.eps);
+  return __fmaf_rn(a.wd, p, __fdiv_rn(__fmul_rn(m, s.ibc1), den));
+}
+
+// Splits chunk [start, start+len) into a scalar head (until 4-aligned), a
+// float4 body and a scalar tail.
+struct ChunkSplit {
+  int64_t start;
+  int head, nbody4, tail;
+};
+
+__device__ __forceinline__ ChunkSplit split_chunk(const Chunk& c) {
+  ChunkSplit s;
+  s.start = c.start;
+  int head = (int)((4 - (c.start & 3)) & 3);
+  if (head > c.len) head = c.len;
+  s.head = head;
+  s.nbody4 = (c.len - head) >> 2;
+  s.tail = c.len - head - 4 * s.nbody4;
+  return s;
+}
+
+template <int W>
+__global__ void __launch_bounds__(kLambThreads) k_lamb_moments(LambArgs a) {
+  __shared__ float red_p[kLambThreads / 32], red_u[kLambThreads / 32];
+  const Chunk c = a.chunks[blockIdx.x];
+  const LambScalars s{a.hp[0], a.hp[1], a.hp[2]};
+  const ChunkSplit sp = split_chunk(c);
+  float pp = 0.0f, uu = 0.0f;
+  const int t = threadIdx.x;
+  // scalar head and tail
+  int64_t si = -1;
+  if (t < sp.head) si = sp.start + t;
+  else if (t >= 32 && t - 32 < sp.tail) si = sp.start + sp.head + 4 * (int64_t)sp.nbody4 + (t - 32);
+  if (si >= 0) {
+    const float g = load_grad1<W>(a, si);
+    const float p = a.p[si];
+    float m = a.m[si], v = a.v[si], u;
+    lamb_moments(a, s, g, p, m, v, u);
+    a.m[si] = m;
+    a.v[si] = v;
+    pp = __fmaf_rn(p, p, pp);
+    uu = __fmaf_rn(u, u, uu);
+  }
+  const int64_t b0 = sp.start + sp.head;
+  for (int k = t; k < sp.nbody4; k += kLambThreads) {
+    const int64_t i = b0 + 4 * (int64_t)k;
+    const float4 g = load_grad4<W>(a, i);
+    const float4 p = *reinterpret_cast<const float4*>(a.p + i);
+    float4 m = *reinterpret_cast<const float4*>(a.m + i);
+    float4 v = *reinterpret_cast<const float4*>(a.v + i);
+    float4 u;
+    lamb_moments(a, s, g.x, p.x, m.x, v.x, u.x);
+    lamb_moments(a, s, g.y, p.y, m.y, v.y, u.y);
+    lamb_moments(a, s, g.z, p.z, m.z, v.z, u.z);
+    lamb_moments(a, s, g.w, p.w, m.w, v.w, u.w);
+    *reinterpret_cast<float4*>(a.m + i) = m;
+    *reinterpret_cast<float4*>(a.v + i) = v;
+    pp = __fmaf_rn(p.x, p.x, pp); pp = __fmaf_rn(p.y, p.y, pp);
+    pp = __fmaf_rn(p.z, p.z, pp); pp = __fmaf_rn(p.w, p.w, pp);
+    uu = __fmaf_rn(u.x, u.x, uu); uu = __fmaf_rn(u.y, u.y, uu);
+    uu = __fmaf_rn(u.z, u.z, uu); uu = __fmaf_rn(u.w, u.w, uu);
+  }
+  pp = warp_sum(pp);
+  uu = warp_sum(uu);
+  const int lane = t & 31, wid = t >> 5;
+  if (lane == 0) {
+    red_p[wid] = pp;
+    red_u[wid] = uu;
+  }
+  __syncthreads();
+  if (t == 0) {
+    float sp_ = 0.0f, su = 0.0f;
+#pragma unroll
+    for (int w = 0; w < kLambThreads / 32; ++w) {
+      sp_ += red_p[w];
+      su += red_u[w];
+    }
+    a.partial[blockIdx.x] = make_float2(sp_, su);
+  }
+}
+
+// One CTA per tensor: deterministic fp64 sum of its chunk partials, then
+// step_scale[t] = lr * trust_t and trust[t].
+__global__ void __launch_bounds__(256) k_lamb_trust(const float2* __restrict__ partial,
+                                                    const int2* __restrict__ tchunks,
+                                                    const float* __restrict__ hp,
+                                                    float* __restrict__ trust,
+                                                    float* __restrict__ step_scale) {
+  __shared__ double sp_[256], su[256];
+  const int2 r = tchunks[blockIdx.x];
+  double a = 0.0, b = 0.0;
+  for (int c = r.x + threadIdx.x; c < r.y; c += blockDim.x) {
+    const float2 q = partial[c];
+    a += (double)q.x;
+    b += (double)q.y;
+  }
+  sp_[threadIdx.x] = a;
+  su[threadIdx.x] = b;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      sp_[threadIdx.x] += sp_[threadIdx.x + s];
+      su[threadIdx.x] += su[threadIdx.x + s];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double r1 = sqrt(sp_[0]), r2 = sqrt(su[0]);
+    const float tr = (r1 > 0.0 && r2 > 0.0) ? (float)(r1 / r2) : 1.0f;
+    trust[blockIdx.x] = tr;
+    step_scale[blockIdx.x] = __fmul_rn(hp[0], tr);
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(kLambThreads) k_lamb_update(LambArgs a) {
+  const Chunk c = a.chunks[blockIdx.x];
+  const LambScalars s{a.hp[0], a.hp[1], a.hp[2]};
+  const float neg = -a.step_scale[c.tensor];
+  const ChunkSplit sp = split_chunk(c);
+  const int t = threadIdx.x;
+  int64_t si = -1;
+  if (t < sp.head) si = sp.start + t;
+  else if (t >= 32 && t - 32 < sp.tail) si = sp.start + sp.head + 4 * (int64_t)sp.nbody4 + (t - 32);
+  if (si >= 0) {
+    const float p = a.p[si];
+    a.p[si] = __fmaf_rn(neg, lamb_dir(a, s, p, a.m[si], a.v[si]), p);
+  }
+  const int64_t b0 = sp.start + sp.head;
+  for (int k = t; k < sp.nbody4; k += kLambThreads) {
+    const int64_t i = b0 + 4 * (int64_t)k;
+    float4 p = *reinterpret_cast<const float4*>(a.p + i);
+    const float4 m = *reinterpret_cast<const float4*>(a.m + i);
+    const float4 v = *reinterpret_cast<const float4*>(a.v + i);
+    p.x = __fmaf_rn(neg, lamb_dir(a, s, p.x, m.x, v.x), p.x);
+    p.y = __fmaf_rn(neg, lamb_dir(a, s, p.y, m.y, v.y), p.y);
+    p.z = __fmaf_rn(neg, lamb_dir(a, s, p.z, m.z, v.z), p.z);
+    p.w = __fmaf_rn(neg, lamb_dir(a, s, p.w, m.w, v.w), p.w);
+    *reinterpret_cast<float4*>(a.p + i) = p;
+  }
+}
+
+}  // namespace sp

@@ -1,0 +1,567 @@
+// sp_round.cu — C-ABI implementation of the averaging-round executor.
+//
+// Host side of libsp_round.so: buffer layout, CUDA IPC wiring between ranks,
+// assignment upload, CUDA-graph capture/replay of the round. Kernels live in
+// sp_kernels.cuh. See include/sp_round.h for the contract and the reference
+// interfaces each entry point replaces.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "sp_kernels.cuh"
+#include "sp_round.h"
+
+using namespace sp;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define SP_CUDA(call)                                                        \
+  do {                                                                       \
+    cudaError_t e_ = (call);                                                 \
+    if (e_ != cudaSuccess)                                                   \
+      return fail(SP_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+int wire_bits(int wire) { return wire == SP_WIRE_FP32 ? 32 : wire == SP_WIRE_FP16 ? 16 : 8; }
+
+}  // namespace
+
+struct sp_round {
+  sp_round_cfg cfg{};
+  std::vector<int64_t> tsizes;
+  int G = 0, L = 0;
+  int64_t n = 0, npad = 0;
+  int align = 8;
+  size_t buf_bytes = 0;     // one wire/avg buffer (codes + q8 scales)
+  size_t flags_bytes = 256;
+  // shared (IPC-exported) allocation: [flags][wire x L][avg]
+  char* shared = nullptr;
+  size_t shared_bytes = 0;
+  char* base[SP_MAX_RANKS] = {};  // every rank's shared allocation (mapped)
+  bool connected = false;
+  unsigned long long* epoch = nullptr;
+  int* h_err = nullptr;  // host-mapped
+  int* d_err = nullptr;
+  // LAMB tables
+  int nchunks = 0;
+  Chunk* d_chunks = nullptr;
+  int2* d_tchunks = nullptr;
+  float2* d_partial = nullptr;
+  float* d_trust = nullptr;
+  float* d_step_scale = nullptr;
+  float* d_hp = nullptr;
+  // assignment
+  std::vector<int64_t> offsets;
+  std::vector<double> weights;
+  bool assigned = false;
+  // graph cache
+  cudaStream_t own = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  std::vector<const void*> gkey;
+  cudaEvent_t ev[8] = {};
+  int sm_count = 148;
+
+  char* wire(int rank, int l) const { return base[rank] + flags_bytes + (size_t)l * buf_bytes; }
+  char* avg(int rank) const { return base[rank] + flags_bytes + (size_t)L * buf_bytes; }
+  unsigned long long* flags(int rank) const {
+    return reinterpret_cast<unsigned long long*>(base[rank]);
+  }
+};
+
+namespace {
+
+int validate_cfg(const sp_round_cfg* c) {
+  if (!c) return fail(SP_ERR_ARG, "cfg is null");
+  if (c->world < 1 || c->world > SP_MAX_RANKS) return fail(SP_ERR_ARG, "world must be in [1, 8]");
+  if (c->rank < 0 || c->rank >= c->world) return fail(SP_ERR_ARG, "rank out of range");
+  if (c->peers_per_rank < 1 || c->peers_per_rank > SP_MAX_LOCAL)
+    return fail(SP_ERR_ARG, "peers_per_rank must be in [1, 16]");
+  if ((int64_t)c->peers_per_rank * c->world > SP_MAX_PEERS)
+    return fail(SP_ERR_ARG, "peers_per_rank * world exceeds 64");
+  if (c->n <= 0) return fail(SP_ERR_ARG, "n must be positive");
+  if (c->wire < SP_WIRE_FP32 || c->wire > SP_WIRE_Q8) return fail(SP_ERR_ARG, "unknown wire format");
+  if (c->wire == SP_WIRE_Q8) {
+    int b = c->q8_block;
+    if (b < 512 || b > 16384 || (b & (b - 1)) != 0)
+      return fail(SP_ERR_ARG, "q8_block must be a power of two in [512, 16384]");
+  }
+  if (c->num_tensors < 1 || !c->tensor_sizes) return fail(SP_ERR_ARG, "empty tensor table");
+  int64_t s = 0;
+  for (int t = 0; t < c->num_tensors; ++t) {
+    if (c->tensor_sizes[t] <= 0) return fail(SP_ERR_ARG, "tensor sizes must be positive");
+    s += c->tensor_sizes[t];
+  }
+  if (s != c->n) return fail(SP_ERR_SHAPE, "tensor sizes do not sum to n");
+  if (!(c->beta1 >= 0 && c->beta1 < 1 && c->beta2 >= 0 && c->beta2 < 1))
+    return fail(SP_ERR_ARG, "betas must lie in [0, 1)");
+  if (!(c->eps > 0)) return fail(SP_ERR_ARG, "eps must be positive");
+  return SP_OK;
+}
+
+// LAMB chunks: tensor t covers [off_t, off_t+size_t); chunk boundaries are
+// the tensor edges plus every multiple of kLambChunk inside the tensor.
+void build_chunks(const std::vector<int64_t>& sizes, std::vector<Chunk>& chunks,
+                  std::vector<int2>& tch) {
+  int64_t off = 0;
+  for (size_t t = 0; t < sizes.size(); ++t) {
+    const int64_t end = off + sizes[t];
+    int2 r;
+    r.x = (int)chunks.size();
+    int64_t s = off;
+    while (s < end) {
+      int64_t e = std::min(end, (s / kLambChunk + 1) * kLambChunk);
+      chunks.push_back(Chunk{(long long)s, (int)(e - s), (int)t});
+      s = e;
+    }
+    r.y = (int)chunks.size();
+    tch.push_back(r);
+    off = end;
+  }
+}
+
+int grid_for(int64_t work_items, int threads, int sm_count, int per_sm) {
+  int64_t g = (work_items + threads - 1) / threads;
+  g = std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)sm_count * per_sm));
+  return (int)g;
+}
+
+// Enqueues the whole round on `st`. ev != nullptr records phase events.
+int enqueue_round(sp_round* r, const float* const* grads, float* p, float* m,
+                  float* v, cudaStream_t st, cudaEvent_t* ev) {
+  const sp_round_cfg& c = r->cfg;
+  if (ev) SP_CUDA(cudaEventRecord(ev[0], st));
+  // K1 pack
+  {
+    PackArgs a{};
+    bool any = false;
+    for (int l = 0; l < r->L; ++l) {
+      a.src[l] = grads[l];
+      a.dst[l] = r->wire(c.rank, l);
+      if (grads[l] && !(c.wire == SP_WIRE_FP32 && (const void*)grads[l] == (const void*)a.dst[l]))
+        any = true;
+      else
+        a.src[l] = nullptr;  // nothing to pack (aggregation-only or zero-copy)
+    }
+    a.n = r->n;
+    a.npad = r->npad;
+    a.qblock = c.q8_block;
+    if (any) {
+      if (c.wire == SP_WIRE_Q8) {
+        dim3 grid(std::min<int64_t>(r->npad / c.q8_block, (int64_t)r->sm_count * 16), r->L);
+        k_pack_q8<<<grid, c.q8_block / 16, 0, st>>>(a);
+      } else if (c.wire == SP_WIRE_FP16) {
+        dim3 grid(grid_for(r->npad / 8, 256, r->sm_count, 8), r->L);
+        k_pack_fp16<<<grid, 256, 0, st>>>(a);
+      } else {
+        dim3 grid(grid_for(r->npad / 4, 256, r->sm_count, 8), r->L);
+        k_pack_fp32<<<grid, 256, 0, st>>>(a);
+      }
+      SP_CUDA(cudaGetLastError());
+    }
+  }
+  if (ev) SP_CUDA(cudaEventRecord(ev[1], st));
+  BarrierArgs ba{};
+  if (c.world > 1) {
+    for (int k = 0; k < c.world; ++k) ba.flags[k] = r->flags(k);
+    ba.epoch = r->epoch;
+    ba.err = r->d_err;
+    ba.rank = c.rank;
+    ba.world = c.world;
+    double to = c.barrier_timeout_s > 0 ? c.barrier_timeout_s : 20.0;
+    ba.timeout_ns = (unsigned long long)(to * 1e9);
+    k_barrier<<<1, 32, 0, st>>>(ba);
+    SP_CUDA(cudaGetLastError());
+  }
+  if (ev) SP_CUDA(cudaEventRecord(ev[2], st));
+  // K2 fused reduce-scatter / average / all-gather
+  {
+    ReduceArgs a{};
+    double wsum = 0.0;
+    for (double w : r->weights) wsum += w;
+    int np = 0;
+    for (int g = 0; g < r->G; ++g) {
+      if (r->weights[g] == 0.0) continue;
+      a.src[np] = r->wire(g / r->L, g % r->L);
+      a.w[np] = (float)(r->weights[g] / wsum);
+      ++np;
+    }
+    a.npeers = np;
+    a.ndst = c.world;
+    for (int k = 0; k < c.world; ++k) a.dst[k] = r->avg(k);
+    a.lo = r->offsets[(size_t)c.rank * r->L];
+    a.hi = r->offsets[(size_t)(c.rank + 1) * r->L];
+    a.npad = r->npad;
+    a.qblock = c.q8_block;
+    if (a.hi > a.lo) {
+      if (c.wire == SP_WIRE_Q8) {
+        int64_t nb = (a.hi + c.q8_block - 1) / c.q8_block - a.lo / c.q8_block;
+        int grid = (int)std::min<int64_t>(nb, (int64_t)r->sm_count * 16);
+        k_reduce_q8<<<grid, c.q8_block / 16, 0, st>>>(a);
+      } else if (c.wire == SP_WIRE_FP16) {
+        k_reduce_fp16<<<grid_for((a.hi - a.lo + 7) / 8, 256, r->sm_count, 8), 256, 0, st>>>(a);
+      } else {
+        k_reduce_fp32<<<grid_for((a.hi - a.lo + 3) / 4, 256, r->sm_count, 8), 256, 0, st>>>(a);
+      }
+      SP_CUDA(cudaGetLastError());
+    }
+  }
+  if (ev) SP_CUDA(cudaEventRecord(ev[3], st));
+  if (c.world > 1) {
+    k_barrier<<<1, 32, 0, st>>>(ba);
+    SP_CUDA(cudaGetLastError());
+  }
+  if (ev) SP_CUDA(cudaEventRecord(ev[4], st));
+  // K3/K4 LAMB on this rank's replica
+  {
+    LambArgs a{};
+    a.avg = r->avg(c.rank);
+    a.avg_scale = c.wire == SP_WIRE_Q8
+                      ? reinterpret_cast<const float*>(r->avg(c.rank) + r->npad)
+                      : nullptr;
+    a.p = p;
+    a.m = m;
+    a.v = v;
+    a.chunks = r->d_chunks;
+    a.partial = r->d_partial;
+    a.hp = r->d_hp;
+    a.step_scale = r->d_step_scale;
+    a.b1 = c.beta1;
+    a.b2 = c.beta2;
+    a.omb1 = 1.0f - c.beta1;
+    a.omb2 = 1.0f - c.beta2;
+    a.eps = c.eps;
+    a.wd = c.weight_decay;
+    a.qblock = c.q8_block;
+    const int nc = r->nchunks;
+    switch (c.wire) {
+      case SP_WIRE_FP32: k_lamb_moments<SP_WIRE_FP32><<<nc, kLambThreads, 0, st>>>(a); break;
+      case SP_WIRE_FP16: k_lamb_moments<SP_WIRE_FP16><<<nc, kLambThreads, 0, st>>>(a); break;
+      default: k_lamb_moments<SP_WIRE_Q8><<<nc, kLambThreads, 0, st>>>(a); break;
+    }
+    SP_CUDA(cudaGetLastError());
+    if (ev) SP_CUDA(cudaEventRecord(ev[5], st));
+    k_lamb_trust<<<c.num_tensors, 256, 0, st>>>(r->d_partial, r->d_tchunks, r->d_hp,
+                                                r->d_trust, r->d_step_scale);
+    SP_CUDA(cudaGetLastError());
+    if (ev) SP_CUDA(cudaEventRecord(ev[6], st));
+    switch (c.wire) {
+      case SP_WIRE_FP32: k_lamb_update<SP_WIRE_FP32><<<nc, kLambThreads, 0, st>>>(a); break;
+      case SP_WIRE_FP16: k_lamb_update<SP_WIRE_FP16><<<nc, kLambThreads, 0, st>>>(a); break;
+      default: k_lamb_update<SP_WIRE_Q8><<<nc, kLambThreads, 0, st>>>(a); break;
+    }
+    SP_CUDA(cudaGetLastError());
+  }
+  if (ev) SP_CUDA(cudaEventRecord(ev[7], st));
+  return SP_OK;
+}
+
+int check_run_args(sp_round* r, const float* const* grads, float* p, float* m, float* v) {
+  if (!r) return fail(SP_ERR_ARG, "null round");
+  if (!r->assigned) return fail(SP_ERR_STATE, "sp_round_set_assignment was not called");
+  if (r->cfg.world > 1 && !r->connected) return fail(SP_ERR_STATE, "sp_round_connect was not called");
+  if (!grads || !p || !m || !v) return fail(SP_ERR_ARG, "null buffer");
+  auto aligned = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  if (!aligned(p) || !aligned(m) || !aligned(v)) return fail(SP_ERR_SHAPE, "p/m/v must be 16-byte aligned");
+  for (int l = 0; l < r->L; ++l) {
+    const int g = r->cfg.rank * r->L + l;
+    if (!grads[l] && r->weights[g] != 0.0)
+      return fail(SP_ERR_ARG, "null grad for a peer with nonzero weight");
+    if (grads[l] && !aligned(grads[l])) return fail(SP_ERR_SHAPE, "grads must be 16-byte aligned");
+  }
+  if (*r->h_err) return fail(SP_ERR_PEER, "a cross-rank barrier timed out in an earlier round");
+  return SP_OK;
+}
+
+int upload_hparams(sp_round* r, int step, cudaStream_t st) {
+  if (step < 1) return fail(SP_ERR_ARG, "step must be >= 1");
+  float hp[4];
+  hp[0] = r->cfg.lr;
+  if (r->cfg.bias_correction) {
+    hp[1] = (float)(1.0 / (1.0 - std::pow((double)r->cfg.beta1, step)));
+    hp[2] = (float)(1.0 / (1.0 - std::pow((double)r->cfg.beta2, step)));
+  } else {
+    hp[1] = hp[2] = 1.0f;
+  }
+  hp[3] = 0.0f;
+  SP_CUDA(cudaMemcpyAsync(r->d_hp, hp, sizeof(hp), cudaMemcpyHostToDevice, st));
+  return SP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sp_version(void) { return "sp_round 0.1.0 (sm_100a)"; }
+const char* sp_last_error(void) { return g_last_error.c_str(); }
+
+size_t sp_round_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
+
+int sp_round_align(const sp_round* r) { return r ? r->align : 0; }
+int64_t sp_round_padded_n(const sp_round* r) { return r ? r->npad : 0; }
+
+int sp_round_create(const sp_round_cfg* cfg, sp_round** out) {
+  if (!out) return fail(SP_ERR_ARG, "out is null");
+  *out = nullptr;
+  int rc = validate_cfg(cfg);
+  if (rc) return rc;
+  SP_CUDA(cudaSetDevice(cfg->device));
+  sp_round* r = new sp_round();
+  r->cfg = *cfg;
+  r->tsizes.assign(cfg->tensor_sizes, cfg->tensor_sizes + cfg->num_tensors);
+  r->cfg.tensor_sizes = r->tsizes.data();
+  r->L = cfg->peers_per_rank;
+  r->G = cfg->peers_per_rank * cfg->world;
+  r->n = cfg->n;
+  r->npad = round_up(cfg->n, std::max<int64_t>(kPad, cfg->wire == SP_WIRE_Q8 ? cfg->q8_block : 1));
+  r->align = cfg->wire == SP_WIRE_Q8 ? cfg->q8_block : 8;
+  r->buf_bytes = (size_t)r->npad * wire_bits(cfg->wire) / 8;
+  if (cfg->wire == SP_WIRE_Q8) r->buf_bytes += round_up(r->npad / cfg->q8_block * 4, 256);
+  r->buf_bytes = round_up(r->buf_bytes, 256);
+  r->shared_bytes = r->flags_bytes + (size_t)(r->L + 1) * r->buf_bytes;
+  int dev_sms = 0;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, cfg->device);
+  if (dev_sms > 0) r->sm_count = dev_sms;
+
+  auto cleanup = [&](int code) {
+    sp_round_destroy(r);
+    return code;
+  };
+  cudaError_t e = cudaMalloc(&r->shared, r->shared_bytes);
+  if (e != cudaSuccess) return cleanup(fail(SP_ERR_CUDA, std::string("cudaMalloc shared: ") + cudaGetErrorString(e)));
+  if ((e = cudaMemset(r->shared, 0, r->shared_bytes)) != cudaSuccess)
+    return cleanup(fail(SP_ERR_CUDA, cudaGetErrorString(e)));
+  r->base[cfg->rank] = r->shared;
+
+  std::vector<Chunk> chunks;
+  std::vector<int2> tch;
+  build_chunks(r->tsizes, chunks, tch);
+  r->nchunks = (int)chunks.size();
+  if ((e = cudaMalloc(&r->d_chunks, chunks.size() * sizeof(Chunk))) != cudaSuccess ||
+      (e = cudaMalloc(&r->d_tchunks, tch.size() * sizeof(int2))) != cudaSuccess ||
+      (e = cudaMalloc(&r->d_partial, chunks.size() * sizeof(float2))) != cudaSuccess ||
+      (e = cudaMalloc(&r->d_trust, tch.size() * sizeof(float))) != cudaSuccess ||
+      (e = cudaMalloc(&r->d_step_scale, tch.size() * sizeof(float))) != cudaSuccess ||
+      (e = cudaMalloc(&r->d_hp, 4 * sizeof(float))) != cudaSuccess ||
+      (e = cudaMalloc(&r->epoch, sizeof(unsigned long long))) != cudaSuccess)
+    return cleanup(fail(SP_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e)));
+  cudaMemcpy(r->d_chunks, chunks.data(), chunks.size() * sizeof(Chunk), cudaMemcpyHostToDevice);
+  cudaMemcpy(r->d_tchunks, tch.data(), tch.size() * sizeof(int2), cudaMemcpyHostToDevice);
+  cudaMemset(r->epoch, 0, sizeof(unsigned long long));
+  cudaMemset(r->d_trust, 0, tch.size() * sizeof(float));
+  if ((e = cudaHostAlloc(&r->h_err, sizeof(int), cudaHostAllocMapped)) != cudaSuccess)
+    return cleanup(fail(SP_ERR_CUDA, cudaGetErrorString(e)));
+  *r->h_err = 0;
+  cudaHostGetDevicePointer(reinterpret_cast<void**>(&r->d_err), r->h_err, 0);
+  if ((e = cudaStreamCreateWithFlags(&r->own, cudaStreamNonBlocking)) != cudaSuccess)
+    return cleanup(fail(SP_ERR_CUDA, cudaGetErrorString(e)));
+  for (auto& ev : r->ev)
+    if ((e = cudaEventCreate(&ev)) != cudaSuccess) return cleanup(fail(SP_ERR_CUDA, cudaGetErrorString(e)));
+  if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cleanup(fail(SP_ERR_CUDA, cudaGetErrorString(e)));
+  if (cfg->world == 1) r->connected = true;
+  *out = r;
+  return SP_OK;
+}
+
+int sp_round_destroy(sp_round* r) {
+  if (!r) return SP_OK;
+  cudaSetDevice(r->cfg.device);
+  cudaDeviceSynchronize();
+  if (r->gexec) cudaGraphExecDestroy(r->gexec);
+  for (int k = 0; k < SP_MAX_RANKS; ++k)
+    if (r->base[k] && k != r->cfg.rank) cudaIpcCloseMemHandle(r->base[k]);
+  cudaFree(r->shared);
+  cudaFree(r->d_chunks);
+  cudaFree(r->d_tchunks);
+  cudaFree(r->d_partial);
+  cudaFree(r->d_trust);
+  cudaFree(r->d_step_scale);
+  cudaFree(r->d_hp);
+  cudaFree(r->epoch);
+  if (r->h_err) cudaFreeHost(r->h_err);
+  for (auto& ev : r->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (r->own) cudaStreamDestroy(r->own);
+  delete r;
+  return SP_OK;
+}
+
+int sp_round_export(sp_round* r, void* out_handle) {
+  if (!r || !out_handle) return fail(SP_ERR_ARG, "null argument");
+  SP_CUDA(cudaSetDevice(r->cfg.device));
+  cudaIpcMemHandle_t h;
+  SP_CUDA(cudaIpcGetMemHandle(&h, r->shared));
+  std::memcpy(out_handle, &h, sizeof(h));
+  return SP_OK;
+}
+
+int sp_round_connect(sp_round* r, const void* all_handles) {
+  if (!r || !all_handles) return fail(SP_ERR_ARG, "null argument");
+  SP_CUDA(cudaSetDevice(r->cfg.device));
+  const char* hb = static_cast<const char*>(all_handles);
+  for (int k = 0; k < r->cfg.world; ++k) {
+    if (k == r->cfg.rank) continue;
+    if (r->base[k]) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, hb + (size_t)k * sizeof(h), sizeof(h));
+    void* p = nullptr;
+    SP_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    r->base[k] = static_cast<char*>(p);
+  }
+  r->connected = true;
+  if (r->gexec) {
+    cudaGraphExecDestroy(r->gexec);
+    r->gexec = nullptr;
+  }
+  return SP_OK;
+}
+
+int sp_round_set_assignment(sp_round* r, const int64_t* offsets, const double* weights) {
+  if (!r || !offsets || !weights) return fail(SP_ERR_ARG, "null argument");
+  const int G = r->G;
+  if (offsets[0] != 0 || offsets[G] != r->n)
+    return fail(SP_ERR_ARG, "offsets must start at 0 and end at n");
+  for (int g = 0; g < G; ++g) {
+    if (offsets[g + 1] < offsets[g]) return fail(SP_ERR_ARG, "offsets must be non-decreasing");
+    if (g + 1 < G && offsets[g + 1] % r->align != 0)
+      return fail(SP_ERR_ARG, "inner offsets must be multiples of sp_round_align()");
+  }
+  double wsum = 0.0;
+  for (int g = 0; g < G; ++g) {
+    if (!(weights[g] >= 0.0) || !std::isfinite(weights[g]))
+      return fail(SP_ERR_ARG, "weights must be finite and non-negative");
+    wsum += weights[g];
+  }
+  if (!(wsum > 0.0)) return fail(SP_ERR_ARG, "sum of weights must be positive");
+  r->offsets.assign(offsets, offsets + G + 1);
+  r->weights.assign(weights, weights + G);
+  r->assigned = true;
+  if (r->gexec) {
+    cudaGraphExecDestroy(r->gexec);
+    r->gexec = nullptr;
+  }
+  return SP_OK;
+}
+
+int sp_round_run(sp_round* r, const float* const* grads, float* p, float* m, float* v,
+                 int step, void* stream) {
+  int rc = check_run_args(r, grads, p, m, v);
+  if (rc) return rc;
+  SP_CUDA(cudaSetDevice(r->cfg.device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : r->own;
+  std::vector<const void*> key;
+  for (int l = 0; l < r->L; ++l) key.push_back(grads[l]);
+  key.push_back(p);
+  key.push_back(m);
+  key.push_back(v);
+  if (!r->gexec || key != r->gkey) {
+    if (r->gexec) {
+      SP_CUDA(cudaStreamSynchronize(st));
+      cudaGraphExecDestroy(r->gexec);
+      r->gexec = nullptr;
+    }
+    cudaGraph_t graph;
+    SP_CUDA(cudaStreamBeginCapture(r->own, cudaStreamCaptureModeThreadLocal));
+    int erc = enqueue_round(r, grads, p, m, v, r->own, nullptr);
+    cudaError_t e = cudaStreamEndCapture(r->own, &graph);
+    if (erc) return erc;
+    if (e != cudaSuccess) return fail(SP_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&r->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return fail(SP_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    r->gkey = key;
+  }
+  rc = upload_hparams(r, step, st);
+  if (rc) return rc;
+  SP_CUDA(cudaGraphLaunch(r->gexec, st));
+  return SP_OK;
+}
+
+int sp_round_run_phased(sp_round* r, const float* const* grads, float* p, float* m, float* v,
+                        int step, void* stream, sp_phase_times* t) {
+  int rc = check_run_args(r, grads, p, m, v);
+  if (rc) return rc;
+  SP_CUDA(cudaSetDevice(r->cfg.device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : r->own;
+  rc = upload_hparams(r, step, st);
+  if (rc) return rc;
+  rc = enqueue_round(r, grads, p, m, v, st, r->ev);
+  if (rc) return rc;
+  SP_CUDA(cudaStreamSynchronize(st));
+  if (*r->h_err) return fail(SP_ERR_PEER, "cross-rank barrier timed out");
+  if (t) {
+    float* f[7] = {&t->pack_ms, &t->barrier_a_ms, &t->reduce_ms, &t->barrier_b_ms,
+                   &t->moments_ms, &t->trust_ms, &t->update_ms};
+    for (int k = 0; k < 7; ++k) SP_CUDA(cudaEventElapsedTime(f[k], r->ev[k], r->ev[k + 1]));
+    SP_CUDA(cudaEventElapsedTime(&t->total_ms, r->ev[0], r->ev[7]));
+  }
+  return SP_OK;
+}
+
+void* sp_round_wire_ptr(sp_round* r, int local_peer) {
+  if (!r || local_peer < 0 || local_peer >= r->L) return nullptr;
+  return r->wire(r->cfg.rank, local_peer);
+}
+
+void* sp_round_avg_ptr(sp_round* r) { return r ? r->avg(r->cfg.rank) : nullptr; }
+
+const float* sp_round_trust_ptr(sp_round* r) { return r ? r->d_trust : nullptr; }
+
+int sp_round_copy_trust(sp_round* r, float* dst, void* stream) {
+  if (!r || !dst) return fail(SP_ERR_ARG, "null argument");
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : r->own;
+  SP_CUDA(cudaMemcpyAsync(dst, r->d_trust, r->tsizes.size() * sizeof(float), cudaMemcpyDefault, st));
+  return SP_OK;
+}
+
+int sp_round_read(sp_round* r, int which, int local_peer, size_t offset_bytes, void* host_dst,
+                  size_t bytes) {
+  if (!r || !host_dst) return fail(SP_ERR_ARG, "null argument");
+  const char* src = nullptr;
+  size_t cap = 0;
+  if (which == SP_BUF_WIRE) {
+    if (local_peer < 0 || local_peer >= r->L) return fail(SP_ERR_ARG, "local_peer out of range");
+    src = r->wire(r->cfg.rank, local_peer);
+    cap = r->buf_bytes;
+  } else if (which == SP_BUF_AVG) {
+    src = r->avg(r->cfg.rank);
+    cap = r->buf_bytes;
+  } else if (which == SP_BUF_TRUST) {
+    src = reinterpret_cast<const char*>(r->d_trust);
+    cap = r->tsizes.size() * sizeof(float);
+  } else {
+    return fail(SP_ERR_ARG, "unknown buffer");
+  }
+  if (offset_bytes > cap || bytes > cap - offset_bytes) return fail(SP_ERR_ARG, "read out of range");
+  SP_CUDA(cudaSetDevice(r->cfg.device));
+  SP_CUDA(cudaDeviceSynchronize());
+  SP_CUDA(cudaMemcpy(host_dst, src + offset_bytes, bytes, cudaMemcpyDeviceToHost));
+  return SP_OK;
+}
+
+int sp_fill_synthetic(float* dev, int64_t n, uint64_t seed, int peer, float scale,
+                      int64_t outlier_every, float outlier_mult, void* stream) {
+  if (!dev || n < 0) return fail(SP_ERR_ARG, "bad buffer");
+  if (n == 0) return SP_OK;
+  int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  k_fill_synthetic<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      dev, n, (unsigned long long)seed, peer, scale, outlier_every, outlier_mult);
+  SP_CUDA(cudaGetLastError());
+  return SP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,162 @@
+"""Parity of the CUDA averaging round (through the C-ABI) with the CPU oracle.
+
+Bit-exact: wire codes of every peer (fp16 / q8 codes and scales), the
+averaged vector, LAMB moments m and v, and the updated parameters given the
+device's trust ratios. Within tolerance: the trust ratios themselves (device
+norms are fp32 partial sums, the oracle's are fp64): rtol 2e-5.
+Virtual peers (peers_per_rank = G on one GPU) exercise the same kernels and
+pointer tables as G GPUs do.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2106_10207_b200 import AveragingRound, fill_synthetic  # noqa: E402
+from paper_2106_10207_b200 import _native as nat  # noqa: E402
+
+HP = dict(lr=1.76e-3, beta1=0.9, beta2=0.999, eps=1e-6, weight_decay=0.01, bias_correction=1)
+SIGMA = float(np.float32(1e-3 * np.sqrt(3.0)))
+HET8C = [1 / 20] * 6 + [0.0, 7 / 10]
+HET4B = [1 / 22] * 3 + [19 / 22]
+RAGGED = [3, 1000, 70001, 2, 4096, 131075, 5]  # n = 206182, misaligned tensor edges
+
+
+def _dev(x):
+    return torch.from_numpy(x).cuda()
+
+
+def _run_case(wire, fractions, weights, sizes, steps=1, block=4096, warm=False, seed=11):
+    G = len(fractions)
+    n = sum(sizes)
+    grads_h = [O.fill_synthetic(n, seed, g, SIGMA) for g in range(G)]
+    for g in range(G):
+        if weights[g] == 0:
+            grads_h[g] = None
+    p_h = O.fill_synthetic(n, seed + 1, 0, 0.02, 0)
+    m_h = O.fill_synthetic(n, seed + 2, 0, 1e-4, 0) if warm else np.zeros(n, np.float32)
+    v_h = np.abs(O.fill_synthetic(n, seed + 3, 0, 1e-6, 0)) if warm else np.zeros(n, np.float32)
+
+    grads_d = []
+    for g in range(G):
+        if grads_h[g] is None:
+            grads_d.append(None)
+            continue
+        t = torch.empty(n, dtype=torch.float32, device="cuda")
+        fill_synthetic(t, seed, g, SIGMA)
+        grads_d.append(t)
+    p_d, m_d, v_d = _dev(p_h.copy()), _dev(m_h.copy()), _dev(v_h.copy())
+    rnd = AveragingRound(n, sizes, wire=wire, q8_block=block, peers_per_rank=G,
+                         lr=HP["lr"], betas=(HP["beta1"], HP["beta2"]), eps=HP["eps"],
+                         weight_decay=HP["weight_decay"])
+    offs = rnd.assign(fractions, weights)
+    assert offs[0] == 0 and offs[-1] == n
+
+    # device synthetic generator == host generator, bit for bit
+    for g in range(G):
+        if grads_d[g] is not None:
+            assert np.array_equal(grads_d[g].cpu().numpy(), grads_h[g])
+
+    packed = [None if x is None else O.pack(wire, x, block) for x in grads_h]
+    for step in range(1, steps + 1):
+        rnd.run(grads_d, p_d, m_d, v_d, step)
+        torch.cuda.synchronize()
+        # pack: wire codes bit-exact
+        for g in range(G):
+            if packed[g] is None:
+                continue
+            got, gs = rnd.read_wire(nat.SP_BUF_WIRE, g)
+            np.testing.assert_array_equal(got, packed[g][0], err_msg=f"wire of peer {g}")
+            if wire == "q8":
+                np.testing.assert_array_equal(gs, packed[g][1])
+        # fused reduce-scatter / average / all-gather: bit-exact
+        wires = [np.zeros(1, np.float32) if q is None else q[0] for q in packed]
+        scales = [None if q is None else q[1] for q in packed]
+        avg, avg_s = O.reduce(wire, wires, scales, weights, 0, n, n, block)
+        got, gs = rnd.read_wire(nat.SP_BUF_AVG)
+        np.testing.assert_array_equal(got, avg, err_msg="averaged vector")
+        if wire == "q8":
+            np.testing.assert_array_equal(gs, avg_s)
+        # LAMB
+        trust_d = rnd.read_trust()
+        trust_o = O.lamb(wire, avg, avg_s, p_h, m_h, v_h, sizes, HP, step, block, trust_in=trust_d)
+        np.testing.assert_allclose(trust_d, trust_o, rtol=2e-5)
+        np.testing.assert_array_equal(m_d.cpu().numpy(), m_h, err_msg="m")
+        np.testing.assert_array_equal(v_d.cpu().numpy(), v_h, err_msg="v")
+        np.testing.assert_array_equal(p_d.cpu().numpy(), p_h, err_msg="p")
+    rnd.close()
+
+
+@pytest.mark.parametrize("wire", ["fp32", "fp16", "q8"])
+@pytest.mark.parametrize("fractions,weights", [
+    ([1.0], [32.0]),
+    ([0.5, 0.5], [16.0, 16.0]),
+    ([1 / 8] * 8, [4.0] * 8),
+    (HET8C, [1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0]),
+    (HET4B, [3.0, 1.0, 2.0, 7.0]),
+])
+def test_round_parity_ragged(wire, fractions, weights):
+    _run_case(wire, fractions, weights, RAGGED, block=4096 if wire != "q8" else 4096)
+
+
+@pytest.mark.parametrize("wire", ["fp16", "q8"])
+def test_round_parity_multi_step_warm_state(wire):
+    _run_case(wire, [0.25, 0.25, 0.25, 0.25], [5.0, 0.0, 3.0, 8.0], RAGGED, steps=3, warm=True)
+
+
+@pytest.mark.parametrize("block", [512, 16384])
+def test_round_parity_q8_block_sizes(block):
+    _run_case("q8", [0.3, 0.7], [1.0, 2.0], RAGGED, block=block)
+
+
+def test_round_parity_albert_large_fp16_g8():
+    import json
+    import os
+
+    tables = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "tensor_tables.json")))
+    _run_case("fp16", [1 / 8] * 8, [4.0] * 8, tables["albert-large"])
+
+
+def test_phased_equals_graph():
+    sizes = RAGGED
+    n = sum(sizes)
+    outs = []
+    for phased in (False, True):
+        g = torch.empty(n, device="cuda")
+        fill_synthetic(g, 5, 0, SIGMA)
+        g2 = torch.empty(n, device="cuda")
+        fill_synthetic(g2, 5, 1, SIGMA)
+        p = torch.full((n,), 0.01, device="cuda")
+        m = torch.zeros(n, device="cuda")
+        v = torch.zeros(n, device="cuda")
+        rnd = AveragingRound(n, sizes, wire="fp16", peers_per_rank=2)
+        rnd.assign([0.5, 0.5], [1.0, 3.0])
+        for step in (1, 2):
+            if phased:
+                t = rnd.run_phased([g, g2], p, m, v, step)
+                assert t["total_ms"] > 0
+            else:
+                rnd.run([g, g2], p, m, v, step)
+        torch.cuda.synchronize()
+        outs.append((p.cpu(), m.cpu(), v.cpu()))
+        rnd.close()
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+
+
+def test_bad_arguments_raise():
+    rnd = AveragingRound(1000, [1000], wire="fp16", peers_per_rank=2)
+    with pytest.raises(ValueError):
+        rnd.set_assignment([0, 3, 1000], [1.0, 1.0])  # inner offset not aligned
+    with pytest.raises(ValueError):
+        rnd.set_assignment([0, 504, 1000], [0.0, 0.0])  # sum of weights is zero
+    p = torch.zeros(1000, device="cuda")
+    with pytest.raises(RuntimeError):
+        rnd.run([p, p], p, p, p, 1)  # before set_assignment
+    rnd.close()
