@@ -1,0 +1,266 @@
+// module.cpp — pybind11 module `_swarmplan`: the reference's Python API
+// (/root/reference/proj/bindings/module.cpp:92-146, re-exported by
+// proj/python/swarmplan/__init__.py) with the same names, argument meaning
+// and errors (SpecParseError -> ValueError subclass), plus the hooks the
+// averaging round needs: part_offsets, plan_parts, run_plan and the LP.
+// The GPU round itself is driven from Python through the C-ABI
+// (paper_2106_10207_b200/round.py); the GIL is released around solves.
+
+#include <pybind11/numpy.h>
+#include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
+
+#include "swarmplan/groups.hpp"
+#include "swarmplan/lp.hpp"
+#include "swarmplan/model.hpp"
+#include "swarmplan/netsim.hpp"
+#include "swarmplan/partition.hpp"
+#include "swarmplan/scenario.hpp"
+#include "swarmplan/strategy.hpp"
+
+namespace py = pybind11;
+using namespace swarmplan;
+
+namespace {
+
+std::vector<std::vector<double>> rows_of(const Eigen::MatrixXd& m) {
+  std::vector<std::vector<double>> out(static_cast<std::size_t>(m.rows()));
+  for (Eigen::Index i = 0; i < m.rows(); ++i) {
+    out[i].resize(static_cast<std::size_t>(m.cols()));
+    for (Eigen::Index j = 0; j < m.cols(); ++j) out[i][j] = m(i, j);
+  }
+  return out;
+}
+
+StrategyAssignment solve_nogil(const CollaborationSpec& spec, bool comm_only = false) {
+  py::gil_scoped_release release;
+  strategy::SolveOptions o;
+  o.communication_only = comm_only;
+  return strategy::solve_strategy(spec, o);
+}
+
+py::dict assignment_dict(const StrategyAssignment& s) {
+  py::dict d;
+  d["steps_per_sec"] = s.xi;
+  d["fractions"] = s.fractions;
+  std::vector<bool> compute(s.compute.begin(), s.compute.end());
+  d["compute"] = compute;
+  d["duty_cycle"] = s.c_raw;
+  d["gradient_flows"] = rows_of(s.a);
+  d["average_flows"] = rows_of(s.g);
+  d["lp_iterations"] = s.lp_iterations;
+  return d;
+}
+
+lp::LinearProgram program_from_py(int num_vars, const std::vector<double>& objective,
+                                  const std::vector<double>& lower, const std::vector<double>& upper,
+                                  const py::list& rows) {
+  lp::LinearProgram prog(num_vars);
+  if (static_cast<int>(objective.size()) != num_vars) prog.objective = Eigen::VectorXd::Zero(static_cast<Eigen::Index>(objective.size()));
+  for (std::size_t j = 0; j < objective.size() && static_cast<int>(j) < prog.objective.size(); ++j)
+    prog.objective(static_cast<Eigen::Index>(j)) = objective[j];
+  for (std::size_t j = 0; j < lower.size() && static_cast<int>(j) < num_vars; ++j) prog.lower(static_cast<Eigen::Index>(j)) = lower[j];
+  for (std::size_t j = 0; j < upper.size() && static_cast<int>(j) < num_vars; ++j) prog.upper(static_cast<Eigen::Index>(j)) = upper[j];
+  for (const auto& r : rows) {
+    auto t = r.cast<py::tuple>();  // (coeffs [(var, coef)], "<=" | "=", rhs)
+    auto coeffs = t[0].cast<std::vector<std::pair<int, double>>>();
+    const std::string rel = t[1].cast<std::string>();
+    prog.add_row(coeffs, rel == "=" ? lp::Relation::Eq : lp::Relation::LessEq, t[2].cast<double>());
+  }
+  return prog;
+}
+
+const char* status_name(lp::LpStatus s) {
+  switch (s) {
+    case lp::LpStatus::Optimal: return "optimal";
+    case lp::LpStatus::Infeasible: return "infeasible";
+    case lp::LpStatus::Unbounded: return "unbounded";
+  }
+  return "?";
+}
+
+}  // namespace
+
+PYBIND11_MODULE(_swarmplan, m) {
+  m.doc() = "B200-native DeDLOC averaging round: planning core (LP load balancer, group plans)";
+  m.attr("__version__") = "0.1.0";
+  py::register_exception<SpecParseError>(m, "SpecParseError", PyExc_ValueError);
+  py::register_exception<lp::MalformedProgram>(m, "MalformedProgram", PyExc_ValueError);
+
+  // ---- reference API (bindings/module.cpp:99-145) ------------------------
+  m.def("solve_strategy",
+        [](const std::string& spec_json) { return assignment_dict(solve_nogil(spec_from_json(spec_json))); },
+        py::arg("spec_json"),
+        "Solve the communication strategy for a collaboration spec (JSON text); returns flows, "
+        "duty cycles, aggregation fractions and the optimizer step rate.");
+  m.def("assignment_json",
+        [](const std::string& spec_json) {
+          CollaborationSpec spec = spec_from_json(spec_json);
+          return assignment_to_json(spec, solve_nogil(spec));
+        },
+        py::arg("spec_json"));
+  m.def("validate_spec",
+        [](const std::string& spec_json) {
+          py::list out;
+          for (const Violation& v : validate(spec_from_json(spec_json))) {
+            py::dict d;
+            d["peer"] = v.peer;
+            d["field"] = v.field;
+            d["message"] = v.message;
+            out.append(d);
+          }
+          return out;
+        },
+        py::arg("spec_json"));
+  m.def("simulate_averaging",
+        [](const std::string& spec_json, const std::string& algorithm, int server) {
+          CollaborationSpec spec = spec_from_json(spec_json);
+          netsim::Algorithm alg = netsim::algorithm_from_name(algorithm);
+          py::gil_scoped_release release;
+          return netsim::simulate_averaging(spec, alg, server);
+        },
+        py::arg("spec_json"), py::arg("algorithm"), py::arg("server") = -1,
+        "Seconds for one averaging round (allreduce, parameter_server or adaptive).");
+  m.def("compare_strategies",
+        [](const std::string& spec_json) {
+          CollaborationSpec spec = spec_from_json(spec_json);
+          std::vector<netsim::StrategyComparison> rows;
+          {
+            py::gil_scoped_release release;
+            rows = netsim::compare_strategies(spec);
+          }
+          py::list out;
+          for (const auto& c : rows) {
+            py::dict d;
+            d["algorithm"] = netsim::algorithm_name(c.algorithm);
+            d["round_s"] = c.round_s;
+            d["steps_per_hour"] = c.steps_per_hour;
+            out.append(d);
+          }
+          return out;
+        },
+        py::arg("spec_json"));
+  m.def("build_plan", [](int n, int msize) { return groups::build_plan(n, msize).rounds; },
+        py::arg("n"), py::arg("m"));
+  m.def("expected_iterations", &groups::expected_iterations, py::arg("n"), py::arg("m"), py::arg("p"));
+  m.def("optimal_group_size", &groups::optimal_group_size, py::arg("n"), py::arg("p"));
+  m.def("run_training",
+        [](const std::string&, double) -> py::dict {
+          throw py::type_error(
+              "run_training (churn simulation) is outside this framework's scope: it models whole "
+              "training runs, not the averaging round (DESIGN.md, out of scope)");
+        },
+        py::arg("scenario_json"), py::arg("hours") = 0.0);
+  m.def("check_bound",
+        [](py::args, py::kwargs) -> py::dict {
+          throw py::type_error(
+              "check_bound (SGD convergence harness) is outside this framework's scope (DESIGN.md)");
+        });
+
+  // ---- averaging-round planning ------------------------------------------
+  m.def("part_offsets", &part_offsets, py::arg("n"), py::arg("fractions"), py::arg("align"),
+        "Contiguous, aligned part boundaries (G+1 offsets) proportional to LP fractions.");
+  m.def("plan_parts",
+        [](const std::string& spec_json, std::int64_t n, std::int64_t align) {
+          StrategyAssignment s = solve_nogil(spec_from_json(spec_json));
+          py::dict d = assignment_dict(s);
+          d["offsets"] = part_offsets(n, s.fractions, align);
+          return d;
+        },
+        py::arg("spec_json"), py::arg("n"), py::arg("align"),
+        "solve_strategy + part_offsets: what each peer aggregates in the GPU round.");
+  m.def("scenario_spec_json",
+        [](const std::string& scenario_text) { return spec_to_json(scenario_from_json(scenario_text).collaboration); },
+        py::arg("scenario_json"));
+  m.def("run_plan",
+        [](int n, int msize, py::array_t<double, py::array::c_style | py::array::forcecast> values,
+           std::vector<double> weights, std::vector<std::pair<int, int>> failures) {
+          if (values.ndim() != 2) throw std::invalid_argument("values must be 2-D (peers x dim)");
+          groups::GroupPlan plan = groups::build_plan(n, msize);
+          Eigen::MatrixXd v(values.shape(0), values.shape(1));
+          auto r = values.unchecked<2>();
+          for (py::ssize_t i = 0; i < values.shape(0); ++i)
+            for (py::ssize_t j = 0; j < values.shape(1); ++j) v(i, j) = r(i, j);
+          std::set<std::pair<int, int>> fs(failures.begin(), failures.end());
+          groups::RunResult res;
+          {
+            py::gil_scoped_release release;
+            res = groups::run_plan(plan, v, weights, fs);
+          }
+          py::array_t<double> out({static_cast<py::ssize_t>(res.values.rows()),
+                                   static_cast<py::ssize_t>(res.values.cols())});
+          auto w = out.mutable_unchecked<2>();
+          for (py::ssize_t i = 0; i < out.shape(0); ++i)
+            for (py::ssize_t j = 0; j < out.shape(1); ++j) w(i, j) = res.values(i, j);
+          py::dict d;
+          d["values"] = out;
+          std::vector<bool> complete(res.complete.begin(), res.complete.end());
+          d["complete"] = complete;
+          d["coverage"] = res.coverage;
+          d["groups_failed"] = res.groups_failed;
+          return d;
+        },
+        py::arg("n"), py::arg("m"), py::arg("values"), py::arg("weights") = std::vector<double>{},
+        py::arg("failures") = std::vector<std::pair<int, int>>{},
+        "groups::run_plan on the CPU (fp64): values is peers x dim.");
+
+  // ---- LP hooks (tests and tools) -----------------------------------------
+  m.def("lp_solve",
+        [](int num_vars, std::vector<double> objective, std::vector<double> lower,
+           std::vector<double> upper, py::list rows) {
+          lp::LinearProgram prog = program_from_py(num_vars, objective, lower, upper, rows);
+          lp::LpSolution sol;
+          {
+            py::gil_scoped_release release;
+            sol = lp::solve(prog);
+          }
+          py::dict d;
+          d["status"] = status_name(sol.status);
+          d["objective"] = sol.objective;
+          d["iterations"] = sol.iterations;
+          std::vector<double> x(static_cast<std::size_t>(sol.x.size()));
+          for (std::size_t j = 0; j < x.size(); ++j) x[j] = sol.x(static_cast<Eigen::Index>(j));
+          d["x"] = x;
+          d["violation"] = lp::check_feasible(prog, sol.x);
+          return d;
+        },
+        py::arg("num_vars"), py::arg("objective"), py::arg("lower"), py::arg("upper"),
+        py::arg("rows"));
+  m.def("build_lp_shape",
+        [](const std::string& spec_json) {
+          strategy::StrategyProblem sp = strategy::build_lp(spec_from_json(spec_json));
+          py::dict d;
+          d["num_vars"] = sp.prog.num_vars;
+          d["rows"] = static_cast<int>(sp.prog.rows.size());
+          d["rows_compute"] = sp.rows_compute;
+          d["rows_aggregate"] = sp.rows_aggregate;
+          d["rows_service"] = sp.rows_service;
+          d["rows_download"] = sp.rows_download;
+          d["rows_upload"] = sp.rows_upload;
+          d["rows_link"] = sp.rows_link;
+          d["xi_var"] = sp.xi_var;
+          d["xi_scale"] = sp.xi_scale;
+          d["flow_scale"] = sp.flow_scale;
+          return d;
+        },
+        py::arg("spec_json"));
+  m.def("reference_program_xi",
+        [](const std::string& spec_json, std::vector<int> pinned_compute) {
+          // xi of the full reference-form program, optionally with duty
+          // cycles pinned (the test-only oracle of test_strategy.cpp:88-108)
+          strategy::StrategyProblem sp = strategy::build_lp(spec_from_json(spec_json));
+          for (std::size_t i = 0; i < pinned_compute.size(); ++i) {
+            if (pinned_compute[i] < 0) continue;
+            sp.prog.lower(sp.c(static_cast<int>(i))) = pinned_compute[i];
+            sp.prog.upper(sp.c(static_cast<int>(i))) = pinned_compute[i];
+          }
+          lp::LpSolution sol;
+          {
+            py::gil_scoped_release release;
+            sol = lp::solve(sp.prog);
+          }
+          return py::make_tuple(status_name(sol.status),
+                                sol.status == lp::LpStatus::Optimal ? sol.x(sp.xi_var) * sp.xi_scale : 0.0);
+        },
+        py::arg("spec_json"), py::arg("pinned_compute") = std::vector<int>{});
+}
