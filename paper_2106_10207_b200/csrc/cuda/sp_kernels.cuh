@@ -610,6 +610,194 @@ __global__ void __launch_bounds__(256) k_lamb_trust(const float2* __restrict__ p
   }
 }
 
+// ------------------------------------------------------------ fused LAMB
+// One persistent kernel for K3 + trust + K4. Work items (chunk, pass) are
+// handed out in a host-built order through an atomic counter: all pass-1
+// chunks in tensor order, with the pass-2 chunks of tensor t inserted `lag`
+// items after t's last pass-1 chunk, so pass 2 re-reads p/m/v while they are
+// still L2-resident. The CTA finishing the last pass-1 chunk of a tensor
+// reduces its chunk partials (fixed order, fp64) into trust[t] and releases
+// a ready flag that the tensor's pass-2 CTAs acquire. Items are taken in
+// list order and a pass-2 item only waits on earlier pass-1 items, so the
+// queue cannot deadlock; the last CTA to exit resets the counters for the
+// next launch (CUDA-graph replay safe).
+
+struct FusedLamb {
+  const int* items;        // >= 0: pass-1 chunk, < 0: ~chunk for pass 2
+  int nitems;
+  int* work;               // next item
+  int* exited;             // CTAs done
+  int* done;               // per tensor: pass-1 chunks finished
+  unsigned int* ready;     // per tensor: trust available
+  const int2* tchunks;     // per tensor [first, last) chunk
+  float* trust;
+  int ntensors;
+};
+
+template <int W>
+__device__ __forceinline__ void lamb_pass1(const LambArgs& a, const LambScalars& s, const Chunk& c,
+                                           float& pp, float& uu) {
+  const ChunkSplit sp = split_chunk(c);
+  const int t = threadIdx.x;
+  int64_t si = -1;
+  if (t < sp.head) si = sp.start + t;
+  else if (t >= 32 && t - 32 < sp.tail) si = sp.start + sp.head + 4 * (int64_t)sp.nbody4 + (t - 32);
+  if (si >= 0) {
+    const float g = load_grad1<W>(a, si);
+    const float p = a.p[si];
+    float m = a.m[si], v = a.v[si], u;
+    lamb_moments(a, s, g, p, m, v, u);
+    a.m[si] = m;
+    a.v[si] = v;
+    pp = __fmaf_rn(p, p, pp);
+    uu = __fmaf_rn(u, u, uu);
+  }
+  const int64_t b0 = sp.start + sp.head;
+  for (int k = t; k < sp.nbody4; k += kLambThreads) {
+    const int64_t i = b0 + 4 * (int64_t)k;
+    const float4 g = load_grad4<W>(a, i);
+    const float4 p = *reinterpret_cast<const float4*>(a.p + i);
+    float4 m = *reinterpret_cast<const float4*>(a.m + i);
+    float4 v = *reinterpret_cast<const float4*>(a.v + i);
+    float4 u;
+    lamb_moments(a, s, g.x, p.x, m.x, v.x, u.x);
+    lamb_moments(a, s, g.y, p.y, m.y, v.y, u.y);
+    lamb_moments(a, s, g.z, p.z, m.z, v.z, u.z);
+    lamb_moments(a, s, g.w, p.w, m.w, v.w, u.w);
+    *reinterpret_cast<float4*>(a.m + i) = m;
+    *reinterpret_cast<float4*>(a.v + i) = v;
+    pp = __fmaf_rn(p.x, p.x, pp); pp = __fmaf_rn(p.y, p.y, pp);
+    pp = __fmaf_rn(p.z, p.z, pp); pp = __fmaf_rn(p.w, p.w, pp);
+    uu = __fmaf_rn(u.x, u.x, uu); uu = __fmaf_rn(u.y, u.y, uu);
+    uu = __fmaf_rn(u.z, u.z, uu); uu = __fmaf_rn(u.w, u.w, uu);
+  }
+}
+
+__device__ __forceinline__ void lamb_pass2(const LambArgs& a, const LambScalars& s, const Chunk& c,
+                                           float neg) {
+  const ChunkSplit sp = split_chunk(c);
+  const int t = threadIdx.x;
+  int64_t si = -1;
+  if (t < sp.head) si = sp.start + t;
+  else if (t >= 32 && t - 32 < sp.tail) si = sp.start + sp.head + 4 * (int64_t)sp.nbody4 + (t - 32);
+  if (si >= 0) {
+    const float p = a.p[si];
+    a.p[si] = __fmaf_rn(neg, lamb_dir(a, s, p, a.m[si], a.v[si]), p);
+  }
+  const int64_t b0 = sp.start + sp.head;
+  for (int k = t; k < sp.nbody4; k += kLambThreads) {
+    const int64_t i = b0 + 4 * (int64_t)k;
+    float4 p = *reinterpret_cast<const float4*>(a.p + i);
+    const float4 m = *reinterpret_cast<const float4*>(a.m + i);
+    const float4 v = *reinterpret_cast<const float4*>(a.v + i);
+    p.x = __fmaf_rn(neg, lamb_dir(a, s, p.x, m.x, v.x), p.x);
+    p.y = __fmaf_rn(neg, lamb_dir(a, s, p.y, m.y, v.y), p.y);
+    p.z = __fmaf_rn(neg, lamb_dir(a, s, p.z, m.z, v.z), p.z);
+    p.w = __fmaf_rn(neg, lamb_dir(a, s, p.w, m.w, v.w), p.w);
+    *reinterpret_cast<float4*>(a.p + i) = p;
+  }
+}
+
+__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_gpu(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int W>
+__global__ void __launch_bounds__(kLambThreads) k_lamb_fused(LambArgs a, FusedLamb f) {
+  __shared__ int s_item;
+  __shared__ int s_last;
+  __shared__ float s_scale;
+  __shared__ float red_p[kLambThreads / 32], red_u[kLambThreads / 32];
+  __shared__ double dred_p[kLambThreads], dred_u[kLambThreads];
+  const LambScalars s{a.hp[0], a.hp[1], a.hp[2]};
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (;;) {
+    if (tid == 0) s_item = atomicAdd(f.work, 1);
+    __syncthreads();
+    const int it = s_item;
+    __syncthreads();
+    if (it >= f.nitems) break;
+    const int code = f.items[it];
+    if (code >= 0) {
+      const Chunk c = a.chunks[code];
+      float pp = 0.0f, uu = 0.0f;
+      lamb_pass1<W>(a, s, c, pp, uu);
+      pp = warp_sum(pp);
+      uu = warp_sum(uu);
+      if (lane == 0) {
+        red_p[wid] = pp;
+        red_u[wid] = uu;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        float sp_ = 0.0f, su = 0.0f;
+#pragma unroll
+        for (int w = 0; w < kLambThreads / 32; ++w) {
+          sp_ += red_p[w];
+          su += red_u[w];
+        }
+        a.partial[code] = make_float2(sp_, su);
+        __threadfence();
+        const int2 r = f.tchunks[c.tensor];
+        s_last = atomicAdd(f.done + c.tensor, 1) == r.y - r.x - 1;
+      }
+      __syncthreads();
+      if (s_last) {  // every pass-1 chunk of this tensor has published its partial
+        __threadfence();
+        const int2 r = f.tchunks[c.tensor];
+        double dp = 0.0, du = 0.0;
+        for (int q = r.x + tid; q < r.y; q += kLambThreads) {
+          const float2 v = __ldcg(a.partial + q);
+          dp += (double)v.x;
+          du += (double)v.y;
+        }
+        dred_p[tid] = dp;
+        dred_u[tid] = du;
+        __syncthreads();
+        for (int h = kLambThreads / 2; h > 0; h >>= 1) {
+          if (tid < h) {
+            dred_p[tid] += dred_p[tid + h];
+            dred_u[tid] += dred_u[tid + h];
+          }
+          __syncthreads();
+        }
+        if (tid == 0) {
+          const double r1 = sqrt(dred_p[0]), r2 = sqrt(dred_u[0]);
+          const float tr = (r1 > 0.0 && r2 > 0.0) ? (float)(r1 / r2) : 1.0f;
+          f.trust[c.tensor] = tr;
+          const_cast<float*>(a.step_scale)[c.tensor] = __fmul_rn(s.lr, tr);
+          f.done[c.tensor] = 0;
+          __threadfence();
+          st_release_gpu(f.ready + c.tensor, 1u);
+        }
+      }
+    } else {
+      const Chunk c = a.chunks[~code];
+      if (tid == 0) {
+        while (ld_acquire_gpu(f.ready + c.tensor) == 0u) __nanosleep(64);
+        s_scale = __ldcg(a.step_scale + c.tensor);
+      }
+      __syncthreads();
+      lamb_pass2(a, s, c, -s_scale);
+    }
+  }
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(f.exited, 1) == (int)gridDim.x - 1) {  // last CTA out resets the queue
+      for (int t = 0; t < f.ntensors; ++t) f.ready[t] = 0u;
+      *f.work = 0;
+      *f.exited = 0;
+      __threadfence();
+    }
+  }
+}
+
 template <int W>
 __global__ void __launch_bounds__(kLambThreads) k_lamb_update(LambArgs a) {
   const Chunk c = a.chunks[blockIdx.x];

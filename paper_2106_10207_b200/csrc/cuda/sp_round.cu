@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -65,6 +66,13 @@ struct sp_round {
   float* d_trust = nullptr;
   float* d_step_scale = nullptr;
   float* d_hp = nullptr;
+  // fused LAMB work queue
+  bool fused_lamb = true;
+  int lamb_grid = 0;
+  int nitems = 0;
+  int* d_items = nullptr;
+  int* d_qstate = nullptr;           // [work, exited, done[T]...]
+  unsigned int* d_ready = nullptr;
   // assignment
   std::vector<int64_t> offsets;
   std::vector<double> weights;
@@ -132,6 +140,33 @@ void build_chunks(const std::vector<int64_t>& sizes, std::vector<Chunk>& chunks,
     tch.push_back(r);
     off = end;
   }
+}
+
+// Fused-LAMB dispatch order: pass-1 chunks in tensor order; the pass-2
+// chunks of tensor t follow once `lag` further items were emitted after t's
+// last pass-1 chunk (about one wave of the persistent grid), so they find
+// t's trust ratio ready and its p/m/v still in L2.
+std::vector<int> build_lamb_items(const std::vector<Chunk>& chunks, const std::vector<int2>& tch,
+                                  int lag) {
+  std::vector<int> out;
+  out.reserve(chunks.size() * 2);
+  std::vector<std::pair<int, size_t>> pending;  // (tensor, position after its last pass-1 item)
+  size_t head = 0;
+  auto flush = [&](bool all) {
+    while (head < pending.size() && (all || pending[head].second + (size_t)lag <= out.size())) {
+      const int2 r = tch[pending[head].first];
+      for (int c = r.x; c < r.y; ++c) out.push_back(~c);
+      ++head;
+    }
+  };
+  for (size_t c = 0; c < chunks.size(); ++c) {
+    out.push_back((int)c);
+    const int t = chunks[c].tensor;
+    if ((int)c == tch[t].y - 1) pending.emplace_back(t, out.size());
+    flush(false);
+  }
+  flush(true);
+  return out;
 }
 
 int grid_for(int64_t work_items, int threads, int sm_count, int per_sm) {
@@ -248,23 +283,47 @@ int enqueue_round(sp_round* r, const float* const* grads, float* p, float* m,
     a.wd = c.weight_decay;
     a.qblock = c.q8_block;
     const int nc = r->nchunks;
-    switch (c.wire) {
-      case SP_WIRE_FP32: k_lamb_moments<SP_WIRE_FP32><<<nc, kLambThreads, 0, st>>>(a); break;
-      case SP_WIRE_FP16: k_lamb_moments<SP_WIRE_FP16><<<nc, kLambThreads, 0, st>>>(a); break;
-      default: k_lamb_moments<SP_WIRE_Q8><<<nc, kLambThreads, 0, st>>>(a); break;
+    if (r->fused_lamb) {
+      FusedLamb f{};
+      f.items = r->d_items;
+      f.nitems = r->nitems;
+      f.work = r->d_qstate;
+      f.exited = r->d_qstate + 1;
+      f.done = r->d_qstate + 2;
+      f.ready = r->d_ready;
+      f.tchunks = r->d_tchunks;
+      f.trust = r->d_trust;
+      f.ntensors = c.num_tensors;
+      const int g = r->lamb_grid;
+      switch (c.wire) {
+        case SP_WIRE_FP32: k_lamb_fused<SP_WIRE_FP32><<<g, kLambThreads, 0, st>>>(a, f); break;
+        case SP_WIRE_FP16: k_lamb_fused<SP_WIRE_FP16><<<g, kLambThreads, 0, st>>>(a, f); break;
+        default: k_lamb_fused<SP_WIRE_Q8><<<g, kLambThreads, 0, st>>>(a, f); break;
+      }
+      SP_CUDA(cudaGetLastError());
+      if (ev) {
+        SP_CUDA(cudaEventRecord(ev[5], st));
+        SP_CUDA(cudaEventRecord(ev[6], st));
+      }
+    } else {
+      switch (c.wire) {
+        case SP_WIRE_FP32: k_lamb_moments<SP_WIRE_FP32><<<nc, kLambThreads, 0, st>>>(a); break;
+        case SP_WIRE_FP16: k_lamb_moments<SP_WIRE_FP16><<<nc, kLambThreads, 0, st>>>(a); break;
+        default: k_lamb_moments<SP_WIRE_Q8><<<nc, kLambThreads, 0, st>>>(a); break;
+      }
+      SP_CUDA(cudaGetLastError());
+      if (ev) SP_CUDA(cudaEventRecord(ev[5], st));
+      k_lamb_trust<<<c.num_tensors, 256, 0, st>>>(r->d_partial, r->d_tchunks, r->d_hp,
+                                                  r->d_trust, r->d_step_scale);
+      SP_CUDA(cudaGetLastError());
+      if (ev) SP_CUDA(cudaEventRecord(ev[6], st));
+      switch (c.wire) {
+        case SP_WIRE_FP32: k_lamb_update<SP_WIRE_FP32><<<nc, kLambThreads, 0, st>>>(a); break;
+        case SP_WIRE_FP16: k_lamb_update<SP_WIRE_FP16><<<nc, kLambThreads, 0, st>>>(a); break;
+        default: k_lamb_update<SP_WIRE_Q8><<<nc, kLambThreads, 0, st>>>(a); break;
+      }
+      SP_CUDA(cudaGetLastError());
     }
-    SP_CUDA(cudaGetLastError());
-    if (ev) SP_CUDA(cudaEventRecord(ev[5], st));
-    k_lamb_trust<<<c.num_tensors, 256, 0, st>>>(r->d_partial, r->d_tchunks, r->d_hp,
-                                                r->d_trust, r->d_step_scale);
-    SP_CUDA(cudaGetLastError());
-    if (ev) SP_CUDA(cudaEventRecord(ev[6], st));
-    switch (c.wire) {
-      case SP_WIRE_FP32: k_lamb_update<SP_WIRE_FP32><<<nc, kLambThreads, 0, st>>>(a); break;
-      case SP_WIRE_FP16: k_lamb_update<SP_WIRE_FP16><<<nc, kLambThreads, 0, st>>>(a); break;
-      default: k_lamb_update<SP_WIRE_Q8><<<nc, kLambThreads, 0, st>>>(a); break;
-    }
-    SP_CUDA(cudaGetLastError());
   }
   if (ev) SP_CUDA(cudaEventRecord(ev[7], st));
   return SP_OK;
@@ -360,6 +419,31 @@ int sp_round_create(const sp_round_cfg* cfg, sp_round** out) {
       (e = cudaMalloc(&r->epoch, sizeof(unsigned long long))) != cudaSuccess)
     return cleanup(fail(SP_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e)));
   cudaMemcpy(r->d_chunks, chunks.data(), chunks.size() * sizeof(Chunk), cudaMemcpyHostToDevice);
+  {
+    const char* env = std::getenv("SP_LAMB_UNFUSED");
+    r->fused_lamb = !(env && env[0] == '1');
+    int per_sm = 0;
+    cudaError_t oe;
+    switch (cfg->wire) {
+      case SP_WIRE_FP32: oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lamb_fused<SP_WIRE_FP32>, kLambThreads, 0); break;
+      case SP_WIRE_FP16: oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lamb_fused<SP_WIRE_FP16>, kLambThreads, 0); break;
+      default: oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lamb_fused<SP_WIRE_Q8>, kLambThreads, 0); break;
+    }
+    if (oe != cudaSuccess || per_sm < 1) return cleanup(fail(SP_ERR_CUDA, "occupancy query failed for the fused LAMB kernel"));
+    // persistent grid: every CTA resident (the queue relies on it)
+    r->lamb_grid = std::max(1, std::min(per_sm * r->sm_count, r->nchunks));
+    const char* lag_env = std::getenv("SP_LAMB_LAG");
+    const int lag = lag_env ? std::atoi(lag_env) : r->lamb_grid;
+    std::vector<int> items = build_lamb_items(chunks, tch, lag);
+    r->nitems = (int)items.size();
+    if ((e = cudaMalloc(&r->d_items, items.size() * sizeof(int))) != cudaSuccess ||
+        (e = cudaMalloc(&r->d_qstate, (2 + tch.size()) * sizeof(int))) != cudaSuccess ||
+        (e = cudaMalloc(&r->d_ready, tch.size() * sizeof(unsigned int))) != cudaSuccess)
+      return cleanup(fail(SP_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e)));
+    cudaMemcpy(r->d_items, items.data(), items.size() * sizeof(int), cudaMemcpyHostToDevice);
+    cudaMemset(r->d_qstate, 0, (2 + tch.size()) * sizeof(int));
+    cudaMemset(r->d_ready, 0, tch.size() * sizeof(unsigned int));
+  }
   cudaMemcpy(r->d_tchunks, tch.data(), tch.size() * sizeof(int2), cudaMemcpyHostToDevice);
   cudaMemset(r->epoch, 0, sizeof(unsigned long long));
   cudaMemset(r->d_trust, 0, tch.size() * sizeof(float));
@@ -391,6 +475,9 @@ int sp_round_destroy(sp_round* r) {
   cudaFree(r->d_trust);
   cudaFree(r->d_step_scale);
   cudaFree(r->d_hp);
+  cudaFree(r->d_items);
+  cudaFree(r->d_qstate);
+  cudaFree(r->d_ready);
   cudaFree(r->epoch);
   if (r->h_err) cudaFreeHost(r->h_err);
   for (auto& ev : r->ev)
