@@ -19,7 +19,7 @@
 
 namespace sp {
 
-constexpr int kLambChunk = 8192;  // elements per LAMB chunk (one CTA)
+constexpr int kLambChunk = 8192;  // elements per LAMB work item (one CTA)
 constexpr int kLambThreads = 256;
 constexpr int kPad = 16384;       // wire/avg buffers padded to this multiple
 
@@ -68,6 +68,7 @@ struct LambArgs {
   const float* step_scale;  // per tensor lr * trust (update kernel only)
   float b1, b2, omb1, omb2, eps, wd;
   int qblock;
+  int l2_hints;             // fused LAMB: keep p/m/v of pass 1 in L2 for pass 2
 };
 
 // ---------------------------------------------------------------- helpers
@@ -83,6 +84,30 @@ __device__ __forceinline__ int4 ld_nc_v4(const void* p) {
 __device__ __forceinline__ void st_v4(void* p, int4 v) {
   asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
                "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// L2 eviction-priority policies (createpolicy) and hinted 128-bit accesses.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float4 ld_hint_f4(const float* p, uint64_t pol) {
+  float4 r;
+  asm volatile("ld.global.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ void st_hint_f4(float* p, float4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
                : "memory");
 }
 
@@ -635,6 +660,29 @@ struct FusedLamb {
 };
 
 template <int W>
+__device__ __forceinline__ void lamb_p1_vec(const LambArgs& a, const LambScalars& s, int64_t i,
+                                            float4 g, float4 p, float4 m, float4 v, float& pp,
+                                            float& uu) {
+  float4 u;
+  lamb_moments(a, s, g.x, p.x, m.x, v.x, u.x);
+  lamb_moments(a, s, g.y, p.y, m.y, v.y, u.y);
+  lamb_moments(a, s, g.z, p.z, m.z, v.z, u.z);
+  lamb_moments(a, s, g.w, p.w, m.w, v.w, u.w);
+  if (a.l2_hints) {
+    const uint64_t keep = policy_evict_last();
+    st_hint_f4(a.m + i, m, keep);
+    st_hint_f4(a.v + i, v, keep);
+  } else {
+    *reinterpret_cast<float4*>(a.m + i) = m;
+    *reinterpret_cast<float4*>(a.v + i) = v;
+  }
+  pp = __fmaf_rn(p.x, p.x, pp); pp = __fmaf_rn(p.y, p.y, pp);
+  pp = __fmaf_rn(p.z, p.z, pp); pp = __fmaf_rn(p.w, p.w, pp);
+  uu = __fmaf_rn(u.x, u.x, uu); uu = __fmaf_rn(u.y, u.y, uu);
+  uu = __fmaf_rn(u.z, u.z, uu); uu = __fmaf_rn(u.w, u.w, uu);
+}
+
+template <int W>
 __device__ __forceinline__ void lamb_pass1(const LambArgs& a, const LambScalars& s, const Chunk& c,
                                            float& pp, float& uu) {
   const ChunkSplit sp = split_chunk(c);
@@ -653,24 +701,46 @@ __device__ __forceinline__ void lamb_pass1(const LambArgs& a, const LambScalars&
     uu = __fmaf_rn(u, u, uu);
   }
   const int64_t b0 = sp.start + sp.head;
-  for (int k = t; k < sp.nbody4; k += kLambThreads) {
-    const int64_t i = b0 + 4 * (int64_t)k;
-    const float4 g = load_grad4<W>(a, i);
-    const float4 p = *reinterpret_cast<const float4*>(a.p + i);
-    float4 m = *reinterpret_cast<const float4*>(a.m + i);
-    float4 v = *reinterpret_cast<const float4*>(a.v + i);
-    float4 u;
-    lamb_moments(a, s, g.x, p.x, m.x, v.x, u.x);
-    lamb_moments(a, s, g.y, p.y, m.y, v.y, u.y);
-    lamb_moments(a, s, g.z, p.z, m.z, v.z, u.z);
-    lamb_moments(a, s, g.w, p.w, m.w, v.w, u.w);
-    *reinterpret_cast<float4*>(a.m + i) = m;
-    *reinterpret_cast<float4*>(a.v + i) = v;
-    pp = __fmaf_rn(p.x, p.x, pp); pp = __fmaf_rn(p.y, p.y, pp);
-    pp = __fmaf_rn(p.z, p.z, pp); pp = __fmaf_rn(p.w, p.w, pp);
-    uu = __fmaf_rn(u.x, u.x, uu); uu = __fmaf_rn(u.y, u.y, uu);
-    uu = __fmaf_rn(u.z, u.z, uu); uu = __fmaf_rn(u.w, u.w, uu);
+  int k = t;
+  // two independent vectors per iteration: all 8 loads issued before use
+  for (; k + kLambThreads < sp.nbody4; k += 2 * kLambThreads) {
+    const int64_t i0 = b0 + 4 * (int64_t)k, i1 = i0 + 4 * (int64_t)kLambThreads;
+    const float4 g0 = load_grad4<W>(a, i0), g1 = load_grad4<W>(a, i1);
+    float4 p0, p1, m0, m1, v0, v1;
+    if (a.l2_hints) {
+      const uint64_t keep = policy_evict_last();
+      p0 = ld_hint_f4(a.p + i0, keep);
+      p1 = ld_hint_f4(a.p + i1, keep);
+      m0 = ld_hint_f4(a.m + i0, keep);
+      m1 = ld_hint_f4(a.m + i1, keep);
+      v0 = ld_hint_f4(a.v + i0, keep);
+      v1 = ld_hint_f4(a.v + i1, keep);
+    } else {
+      p0 = *reinterpret_cast<const float4*>(a.p + i0);
+      p1 = *reinterpret_cast<const float4*>(a.p + i1);
+      m0 = *reinterpret_cast<const float4*>(a.m + i0);
+      m1 = *reinterpret_cast<const float4*>(a.m + i1);
+      v0 = *reinterpret_cast<const float4*>(a.v + i0);
+      v1 = *reinterpret_cast<const float4*>(a.v + i1);
+    }
+    lamb_p1_vec<W>(a, s, i0, g0, p0, m0, v0, pp, uu);
+    lamb_p1_vec<W>(a, s, i1, g1, p1, m1, v1, pp, uu);
   }
+  if (k < sp.nbody4) {
+    const int64_t i = b0 + 4 * (int64_t)k;
+    lamb_p1_vec<W>(a, s, i, load_grad4<W>(a, i), *reinterpret_cast<const float4*>(a.p + i),
+                   *reinterpret_cast<const float4*>(a.m + i),
+                   *reinterpret_cast<const float4*>(a.v + i), pp, uu);
+  }
+}
+
+__device__ __forceinline__ float4 lamb_p2_vec(const LambArgs& a, const LambScalars& s, float neg,
+                                              float4 p, float4 m, float4 v) {
+  p.x = __fmaf_rn(neg, lamb_dir(a, s, p.x, m.x, v.x), p.x);
+  p.y = __fmaf_rn(neg, lamb_dir(a, s, p.y, m.y, v.y), p.y);
+  p.z = __fmaf_rn(neg, lamb_dir(a, s, p.z, m.z, v.z), p.z);
+  p.w = __fmaf_rn(neg, lamb_dir(a, s, p.w, m.w, v.w), p.w);
+  return p;
 }
 
 __device__ __forceinline__ void lamb_pass2(const LambArgs& a, const LambScalars& s, const Chunk& c,
@@ -685,16 +755,32 @@ __device__ __forceinline__ void lamb_pass2(const LambArgs& a, const LambScalars&
     a.p[si] = __fmaf_rn(neg, lamb_dir(a, s, p, a.m[si], a.v[si]), p);
   }
   const int64_t b0 = sp.start + sp.head;
-  for (int k = t; k < sp.nbody4; k += kLambThreads) {
+  int k = t;
+  for (; k + kLambThreads < sp.nbody4; k += 2 * kLambThreads) {
+    const int64_t i0 = b0 + 4 * (int64_t)k, i1 = i0 + 4 * (int64_t)kLambThreads;
+    if (a.l2_hints) {  // last use of m/v this step: let them go first
+      const uint64_t drop = policy_evict_first();
+      const float4 p0 = ld_hint_f4(a.p + i0, drop), p1 = ld_hint_f4(a.p + i1, drop);
+      const float4 m0 = ld_hint_f4(a.m + i0, drop), m1 = ld_hint_f4(a.m + i1, drop);
+      const float4 v0 = ld_hint_f4(a.v + i0, drop), v1 = ld_hint_f4(a.v + i1, drop);
+      st_hint_f4(a.p + i0, lamb_p2_vec(a, s, neg, p0, m0, v0), drop);
+      st_hint_f4(a.p + i1, lamb_p2_vec(a, s, neg, p1, m1, v1), drop);
+      continue;
+    }
+    const float4 p0 = *reinterpret_cast<const float4*>(a.p + i0);
+    const float4 p1 = *reinterpret_cast<const float4*>(a.p + i1);
+    const float4 m0 = *reinterpret_cast<const float4*>(a.m + i0);
+    const float4 m1 = *reinterpret_cast<const float4*>(a.m + i1);
+    const float4 v0 = *reinterpret_cast<const float4*>(a.v + i0);
+    const float4 v1 = *reinterpret_cast<const float4*>(a.v + i1);
+    *reinterpret_cast<float4*>(a.p + i0) = lamb_p2_vec(a, s, neg, p0, m0, v0);
+    *reinterpret_cast<float4*>(a.p + i1) = lamb_p2_vec(a, s, neg, p1, m1, v1);
+  }
+  if (k < sp.nbody4) {
     const int64_t i = b0 + 4 * (int64_t)k;
-    float4 p = *reinterpret_cast<const float4*>(a.p + i);
-    const float4 m = *reinterpret_cast<const float4*>(a.m + i);
-    const float4 v = *reinterpret_cast<const float4*>(a.v + i);
-    p.x = __fmaf_rn(neg, lamb_dir(a, s, p.x, m.x, v.x), p.x);
-    p.y = __fmaf_rn(neg, lamb_dir(a, s, p.y, m.y, v.y), p.y);
-    p.z = __fmaf_rn(neg, lamb_dir(a, s, p.z, m.z, v.z), p.z);
-    p.w = __fmaf_rn(neg, lamb_dir(a, s, p.w, m.w, v.w), p.w);
-    *reinterpret_cast<float4*>(a.p + i) = p;
+    *reinterpret_cast<float4*>(a.p + i) =
+        lamb_p2_vec(a, s, neg, *reinterpret_cast<const float4*>(a.p + i),
+                    *reinterpret_cast<const float4*>(a.m + i), *reinterpret_cast<const float4*>(a.v + i));
   }
 }
 
@@ -717,12 +803,15 @@ __global__ void __launch_bounds__(kLambThreads) k_lamb_fused(LambArgs a, FusedLa
   __shared__ double dred_p[kLambThreads], dred_u[kLambThreads];
   const LambScalars s{a.hp[0], a.hp[1], a.hp[2]};
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  int next = 0;
+  if (tid == 0) next = atomicAdd(f.work, 1);
   for (;;) {
-    if (tid == 0) s_item = atomicAdd(f.work, 1);
+    if (tid == 0) s_item = next;
     __syncthreads();
     const int it = s_item;
     __syncthreads();
     if (it >= f.nitems) break;
+    if (tid == 0) next = atomicAdd(f.work, 1);  // in flight while this item runs
     const int code = f.items[it];
     if (code >= 0) {
       const Chunk c = a.chunks[code];

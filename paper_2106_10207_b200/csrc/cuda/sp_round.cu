@@ -68,6 +68,7 @@ struct sp_round {
   float* d_hp = nullptr;
   // fused LAMB work queue
   bool fused_lamb = true;
+  int l2_hints = 0;
   int lamb_grid = 0;
   int nitems = 0;
   int* d_items = nullptr;
@@ -123,7 +124,7 @@ int validate_cfg(const sp_round_cfg* c) {
 
 // LAMB chunks: tensor t covers [off_t, off_t+size_t); chunk boundaries are
 // the tensor edges plus every multiple of kLambChunk inside the tensor.
-void build_chunks(const std::vector<int64_t>& sizes, std::vector<Chunk>& chunks,
+void build_chunks(const std::vector<int64_t>& sizes, int64_t chunk, std::vector<Chunk>& chunks,
                   std::vector<int2>& tch) {
   int64_t off = 0;
   for (size_t t = 0; t < sizes.size(); ++t) {
@@ -132,7 +133,7 @@ void build_chunks(const std::vector<int64_t>& sizes, std::vector<Chunk>& chunks,
     r.x = (int)chunks.size();
     int64_t s = off;
     while (s < end) {
-      int64_t e = std::min(end, (s / kLambChunk + 1) * kLambChunk);
+      int64_t e = std::min(end, (s / chunk + 1) * chunk);
       chunks.push_back(Chunk{(long long)s, (int)(e - s), (int)t});
       s = e;
     }
@@ -282,6 +283,7 @@ int enqueue_round(sp_round* r, const float* const* grads, float* p, float* m,
     a.eps = c.eps;
     a.wd = c.weight_decay;
     a.qblock = c.q8_block;
+    a.l2_hints = r->l2_hints;
     const int nc = r->nchunks;
     if (r->fused_lamb) {
       FusedLamb f{};
@@ -408,7 +410,9 @@ int sp_round_create(const sp_round_cfg* cfg, sp_round** out) {
 
   std::vector<Chunk> chunks;
   std::vector<int2> tch;
-  build_chunks(r->tsizes, chunks, tch);
+  const char* chunk_env = std::getenv("SP_LAMB_CHUNK");
+  const int64_t chunk = chunk_env ? std::max(64, std::atoi(chunk_env)) : kLambChunk;
+  build_chunks(r->tsizes, chunk, chunks, tch);
   r->nchunks = (int)chunks.size();
   if ((e = cudaMalloc(&r->d_chunks, chunks.size() * sizeof(Chunk))) != cudaSuccess ||
       (e = cudaMalloc(&r->d_tchunks, tch.size() * sizeof(int2))) != cudaSuccess ||
@@ -422,6 +426,8 @@ int sp_round_create(const sp_round_cfg* cfg, sp_round** out) {
   {
     const char* env = std::getenv("SP_LAMB_UNFUSED");
     r->fused_lamb = !(env && env[0] == '1');
+    const char* hint_env = std::getenv("SP_LAMB_L2HINTS");
+    r->l2_hints = hint_env ? std::atoi(hint_env) : 1;
     int per_sm = 0;
     cudaError_t oe;
     switch (cfg->wire) {
@@ -433,7 +439,10 @@ int sp_round_create(const sp_round_cfg* cfg, sp_round** out) {
     // persistent grid: every CTA resident (the queue relies on it)
     r->lamb_grid = std::max(1, std::min(per_sm * r->sm_count, r->nchunks));
     const char* lag_env = std::getenv("SP_LAMB_LAG");
-    const int lag = lag_env ? std::atoi(lag_env) : r->lamb_grid;
+    // Measured on B200 (profiles/r01/lamb_sweep.txt): with 8 resident CTAs
+    // per SM the in-flight window (~9.7M elements) already exceeds L2, so a
+    // short lag only adds trust waits; default: all pass-1 items first.
+    const int lag = lag_env ? std::atoi(lag_env) : (1 << 30);
     std::vector<int> items = build_lamb_items(chunks, tch, lag);
     r->nitems = (int)items.size();
     if ((e = cudaMalloc(&r->d_items, items.size() * sizeof(int))) != cudaSuccess ||
