@@ -30,7 +30,7 @@ sys.path.insert(0, ROOT)
 METRIC = "averaging round time + GB/s (grad avg + LAMB step), ALBERT-large, 1/2/4/8 B200"
 HP = dict(lr=1.76e-3, beta1=0.9, beta2=0.999, eps=1e-6, weight_decay=0.01, bias_correction=1)
 SIGMA = 1e-3 * 3 ** 0.5
-NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+NVLINK_GBS = 660.0  # measured all-to-all kernel push per GPU per direction, 4x B200 (profiles/r01/p2p_bw.txt); 770 single-peer copy, 900 nominal
 L2_BYTES = 126e6
 
 WORKLOADS = {
@@ -172,6 +172,8 @@ def main():
     if args.impl == "reference":
         return run_reference(args, rank, world, tsizes, wire, block, G, weights, b)
 
+    if os.environ.get("NCCL_DEBUG", "VERSION").upper() in ("VERSION", ""):
+        os.environ["NCCL_DEBUG"] = "WARN"  # keep stdout to the one JSON line
     import torch
 
     torch.cuda.set_device(local_rank)
@@ -297,18 +299,21 @@ def main():
     if rank == 0:
         peak, peak_kind = peak_hbm()
         f_r = (offsets[(rank + 1) * L] - offsets[rank * L]) / n
+        fused = ph["update_ms"] < 0.1 * ph["moments_ms"]  # fused LAMB: one kernel
         alg = {  # algorithmic bytes per launch, this rank
-            "pack_ms": (L * n * (4 + b)) if wire != "fp32" else 0.0,
+            "pack_ms": (L * n * (4 + b)) if (wire != "fp32" or world > 1) else 0.0,
             "reduce_ms": (G + world) * f_r * n * b,
-            "moments_ms": n * (20 + b),
-            "update_ms": n * 16.0,
+            # fused kernel: pass 1 reads g,p,m,v writes m,v; pass 2 reads p,m,v writes p
+            "moments_ms": n * (20 + b) + (n * 16.0 if fused else 0.0),
+            "update_ms": 0.0 if fused else n * 16.0,
         }
         dom = max(("pack_ms", "reduce_ms", "moments_ms", "update_ms"), key=lambda k: ph[k])
         achieved = alg[dom] / (ph[dom] * 1e-3) / 1e9
         bound, pk, unit = "hbm", peak, "GB/s"
-        if dom == "reduce_ms" and world > 1:
+        if dom in ("reduce_ms", "pack_ms") and world > 1:
             bound, pk = "nvlink", NVLINK_GBS
-            nvl = ((1 - f_r) * b + (G - 1) * f_r * b) * n  # per direction
+            # per direction: pack scatters (1-f) b n, reduce pushes (G-1) f b n
+            nvl = ((1 - f_r) * b * n) if dom == "pack_ms" else ((world - 1) * f_r * b * n)
             achieved = nvl / (ph[dom] * 1e-3) / 1e9
         # whole-round roofline: serialized HBM + NVLink phases
         hbm_round = ((4 + b) * L if wire != "fp32" else 0.0) + G * f_r * b + f_r * b + 24 + b
@@ -344,12 +349,13 @@ def main():
                        "fractions": "uniform 1/G (LP, homogeneous fleet)",
                        "l2": f"no flush: per-step working set {(n * (12 + 4 * L + 2 * b)) / 1e9:.2f} GB > 126 MB L2",
                        "parallelism": f"dp{world} (one peer per GPU, CUDA IPC over NVLink)"},
-            "gpu_launches": args.steps * ((1 if wire != "fp32" else 1) + 1 + 3 + (2 if world > 1 else 0)),
+            # per round: pack + reduce + LAMB (1 fused / 3 unfused) + 2 barriers if N > 1
+            "gpu_launches": args.steps * (2 + (1 if fused else 3) + (2 if world > 1 else 0)),
             "kernel_ms": {k: round(v_, 5) for k, v_ in ph.items()},
             "roofline": {"bound": bound, "kernel": dom.replace("_ms", ""),
                          "achieved": round(achieved, 1), "peak": pk, "unit": unit,
                          "frac": round(achieved / pk, 4), "traffic": None,
-                         "peak_kind": peak_kind if bound == "hbm" else "measured peer copy (guide)"},
+                         "peak_kind": peak_kind if bound == "hbm" else "measured all-to-all push (profiles/r01/p2p_bw.txt)"},
             "round_roofline": {"t_roof_us": round(t_roof * 1e6, 2),
                                "frac": round(t_roof * 1e3 / ms_step, 4),
                                "hbm_B_per_param": round(hbm_round, 3),

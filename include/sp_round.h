@@ -21,9 +21,10 @@
  * `peers_per_rank` consecutive peers (virtual peers when > 1, e.g. all 8
  * peers of a fleet on one GPU for parity tests). Peer g owns the element
  * range [offsets[g], offsets[g+1]). Ranks exchange one CUDA IPC handle each
- * (sp_round_export / sp_round_connect); the reduce kernel then reads every
- * peer's packed part directly over NVLink and pushes the averaged part into
- * every rank's buffer (fused reduce-scatter + average + all-gather).
+ * (sp_round_export / sp_round_connect). The pack kernel scatters every
+ * peer's packed part straight into the owning rank's inbox over NVLink
+ * (reduce-scatter as posted writes); the owner averages its range from local
+ * HBM and pushes the result into every rank's buffer (all-gather).
  *
  * Status codes: every function returns SP_OK (0) or an SP_ERR_* code; the
  * message of the last failure on the calling thread is sp_last_error().
@@ -130,10 +131,12 @@ int sp_round_run_phased(sp_round* r, const float* const* grads, float* p,
                         float* m, float* v, int step, void* stream,
                         sp_phase_times* t);
 
-/* Buffers owned by the executor (device pointers). wire(l) is local peer l's
- * packed part buffer; when grads[l] == wire(l) with SP_WIRE_FP32 the pack is
- * skipped (zero-copy). avg is this rank's all-gathered averaged vector in the
- * wire format; q8 scales follow the codes at avg + padded_n. */
+/* Buffers owned by the executor (device pointers). wire(l) is this rank's
+ * inbox slot of local peer l (holding the part of l's packed gradient this
+ * rank owns; with world == 1 the whole vector). With world == 1 and
+ * SP_WIRE_FP32, grads[l] == wire(l) skips the pack (zero-copy). avg is this
+ * rank's all-gathered averaged vector in the wire format; q8 scales follow
+ * the codes at avg + padded_n. */
 void* sp_round_wire_ptr(sp_round* r, int local_peer);
 void* sp_round_avg_ptr(sp_round* r);
 int64_t sp_round_padded_n(const sp_round* r);

@@ -50,7 +50,8 @@ struct sp_round {
   int align = 8;
   size_t buf_bytes = 0;     // one wire/avg buffer (codes + q8 scales)
   size_t flags_bytes = 256;
-  // shared (IPC-exported) allocation: [flags][wire x L][avg]
+  // shared (IPC-exported) allocation: [flags][inbox: one slot per peer, G][avg]
+  // slot g of rank k holds peer g's packed gradient for the range k owns
   char* shared = nullptr;
   size_t shared_bytes = 0;
   char* base[SP_MAX_RANKS] = {};  // every rank's shared allocation (mapped)
@@ -85,8 +86,8 @@ struct sp_round {
   cudaEvent_t ev[8] = {};
   int sm_count = 148;
 
-  char* wire(int rank, int l) const { return base[rank] + flags_bytes + (size_t)l * buf_bytes; }
-  char* avg(int rank) const { return base[rank] + flags_bytes + (size_t)L * buf_bytes; }
+  char* wire(int rank, int g) const { return base[rank] + flags_bytes + (size_t)g * buf_bytes; }
+  char* avg(int rank) const { return base[rank] + flags_bytes + (size_t)G * buf_bytes; }
   unsigned long long* flags(int rank) const {
     return reinterpret_cast<unsigned long long*>(base[rank]);
   }
@@ -185,10 +186,16 @@ int enqueue_round(sp_round* r, const float* const* grads, float* p, float* m,
   {
     PackArgs a{};
     bool any = false;
+    a.world = c.world;
+    for (int k = 0; k <= c.world; ++k) a.rank_lo[k] = r->offsets[(size_t)k * r->L];
+    a.rot = c.world > 1 ? a.rank_lo[(c.rank + 1) % c.world] : 0;  // multiple of align
     for (int l = 0; l < r->L; ++l) {
+      const int g = c.rank * r->L + l;
       a.src[l] = grads[l];
-      a.dst[l] = r->wire(c.rank, l);
-      if (grads[l] && !(c.wire == SP_WIRE_FP32 && (const void*)grads[l] == (const void*)a.dst[l]))
+      for (int k = 0; k < c.world; ++k) a.dst[l][k] = r->wire(k, g);
+      const bool zero_copy = c.world == 1 && c.wire == SP_WIRE_FP32 &&
+                             (const void*)grads[l] == (const void*)r->wire(c.rank, g);
+      if (grads[l] && !zero_copy)
         any = true;
       else
         a.src[l] = nullptr;  // nothing to pack (aggregation-only or zero-copy)
@@ -232,13 +239,14 @@ int enqueue_round(sp_round* r, const float* const* grads, float* p, float* m,
     int np = 0;
     for (int g = 0; g < r->G; ++g) {
       if (r->weights[g] == 0.0) continue;
-      a.src[np] = r->wire(g / r->L, g % r->L);
+      a.src[np] = r->wire(c.rank, g);  // this rank's inbox: local HBM only
       a.w[np] = (float)(r->weights[g] / wsum);
       ++np;
     }
     a.npeers = np;
     a.ndst = c.world;
-    for (int k = 0; k < c.world; ++k) a.dst[k] = r->avg(k);
+    // push order rotated per rank (next rank first, self last): no incast
+    for (int k = 0; k < c.world; ++k) a.dst[k] = r->avg((c.rank + 1 + k) % c.world);
     a.lo = r->offsets[(size_t)c.rank * r->L];
     a.hi = r->offsets[(size_t)(c.rank + 1) * r->L];
     a.npad = r->npad;
@@ -393,7 +401,7 @@ int sp_round_create(const sp_round_cfg* cfg, sp_round** out) {
   r->buf_bytes = (size_t)r->npad * wire_bits(cfg->wire) / 8;
   if (cfg->wire == SP_WIRE_Q8) r->buf_bytes += round_up(r->npad / cfg->q8_block * 4, 256);
   r->buf_bytes = round_up(r->buf_bytes, 256);
-  r->shared_bytes = r->flags_bytes + (size_t)(r->L + 1) * r->buf_bytes;
+  r->shared_bytes = r->flags_bytes + (size_t)(r->G + 1) * r->buf_bytes;
   int dev_sms = 0;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, cfg->device);
   if (dev_sms > 0) r->sm_count = dev_sms;
@@ -610,7 +618,7 @@ int sp_round_run_phased(sp_round* r, const float* const* grads, float* p, float*
 
 void* sp_round_wire_ptr(sp_round* r, int local_peer) {
   if (!r || local_peer < 0 || local_peer >= r->L) return nullptr;
-  return r->wire(r->cfg.rank, local_peer);
+  return r->wire(r->cfg.rank, r->cfg.rank * r->L + local_peer);
 }
 
 void* sp_round_avg_ptr(sp_round* r) { return r ? r->avg(r->cfg.rank) : nullptr; }
@@ -631,7 +639,7 @@ int sp_round_read(sp_round* r, int which, int local_peer, size_t offset_bytes, v
   size_t cap = 0;
   if (which == SP_BUF_WIRE) {
     if (local_peer < 0 || local_peer >= r->L) return fail(SP_ERR_ARG, "local_peer out of range");
-    src = r->wire(r->cfg.rank, local_peer);
+    src = r->wire(r->cfg.rank, r->cfg.rank * r->L + local_peer);
     cap = r->buf_bytes;
   } else if (which == SP_BUF_AVG) {
     src = r->avg(r->cfg.rank);
