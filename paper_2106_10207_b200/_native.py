@@ -13,7 +13,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libsp_round.so")
+LIB_PATH = os.environ.get("SP_ROUND_LIB") or os.path.join(_HERE, "lib", "libsp_round.so")
 
 SP_OK, SP_ERR_ARG, SP_ERR_CUDA, SP_ERR_STATE, SP_ERR_PEER, SP_ERR_SHAPE = range(6)
 SP_WIRE_FP32, SP_WIRE_FP16, SP_WIRE_Q8 = range(3)

@@ -23,6 +23,14 @@ constexpr int kLambChunk = 8192;  // elements per LAMB work item (one CTA)
 constexpr int kLambThreads = 256;
 constexpr int kPad = 16384;       // wire/avg buffers padded to this multiple
 
+struct BarrierArgs {
+  unsigned long long* flags[SP_MAX_RANKS];  // flags array of every rank
+  unsigned long long* epoch;                // local epoch counter
+  int* err;                                 // host-mapped error flag
+  int rank, world;
+  unsigned long long timeout_ns;
+};
+
 // K1 scatters each local peer's packed gradient straight into the inbox of
 // the rank that owns each element range (local HBM or a peer GPU over
 // NVLink): posted writes only, no pull reads in the exchange.
@@ -62,14 +70,6 @@ struct ReduceArgs {
   int64_t lo, hi;                 // element range reduced by this rank
   int64_t npad;
   int qblock;
-};
-
-struct BarrierArgs {
-  unsigned long long* flags[SP_MAX_RANKS];  // flags array of every rank
-  unsigned long long* epoch;                // local epoch counter
-  int* err;                                 // host-mapped error flag
-  int rank, world;
-  unsigned long long timeout_ns;
 };
 
 struct Chunk {
@@ -210,13 +210,42 @@ __global__ void k_fill_synthetic(float* __restrict__ out, int64_t n,
   }
 }
 
+// ----------------------------------------------------------------- barrier
+// Cross-rank barrier over NVLink between the exchange kernels: rank r stores
+// the new epoch into flags_k[r] of every rank k (system-scope release), then
+// waits until its own flags[k] >= epoch for all k (acquire). One warp.
+// (Folding this wait/signal into the producer/consumer kernels was measured
+// slower at N=4: every CTA polls the flags and pays a fence.)
+
+__global__ void k_barrier(BarrierArgs a) {
+  __shared__ unsigned long long epoch;
+  if (threadIdx.x == 0) {
+    epoch = *a.epoch + 1;
+    *a.epoch = epoch;
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t < a.world) {
+    __threadfence_system();
+    st_release_sys(a.flags[t] + a.rank, epoch);
+    const unsigned long long* mine = a.flags[a.rank] + t;
+    const unsigned long long t0 = globaltimer();
+    while (ld_acquire_sys(mine) < epoch) {
+      if (globaltimer() - t0 > a.timeout_ns) {
+        atomicExch_system(a.err, 1);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+}
+
 // -------------------------------------------------------------------- pack
 // K1. fp32 accumulated gradient -> wire format. blockIdx.y = local peer.
 
 __global__ void __launch_bounds__(256) k_pack_fp32(PackArgs a) {
   const float* __restrict__ src = a.src[blockIdx.y];
-  if (src == nullptr) return;
-  const int64_t nvec = a.npad / 4;
+  const int64_t nvec = src ? a.npad / 4 : 0;
   const int64_t nfull = a.n / 4;
   for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nvec;
        w += (int64_t)gridDim.x * blockDim.x) {
@@ -248,8 +277,7 @@ __device__ __forceinline__ float2 unpack_half2(uint32_t u) {
 
 __global__ void __launch_bounds__(256) k_pack_fp16(PackArgs a) {
   const float* __restrict__ src = a.src[blockIdx.y];
-  if (src == nullptr) return;
-  const int64_t nvec = a.npad / 8;
+  const int64_t nvec = src ? a.npad / 8 : 0;
   const int64_t nfull = a.n / 8;
   for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nvec;
        w += (int64_t)gridDim.x * blockDim.x) {
@@ -282,8 +310,7 @@ __global__ void __launch_bounds__(256) k_pack_fp16(PackArgs a) {
 __global__ void k_pack_q8(PackArgs a) {
   __shared__ float red[32];
   const float* __restrict__ src = a.src[blockIdx.y];
-  if (src == nullptr) return;
-  const int64_t nblk = a.npad / a.qblock;
+  const int64_t nblk = src ? a.npad / a.qblock : 0;
   for (int64_t bb = blockIdx.x; bb < nblk; bb += gridDim.x) {
     const int64_t b = rotated(bb, a.rot / a.qblock, nblk);
     int8_t* __restrict__ codes = static_cast<int8_t*>(a.dst[blockIdx.y][owner_of(a, b * a.qblock)]);
@@ -318,34 +345,6 @@ __global__ void k_pack_q8(PackArgs a) {
     st_v4(codes + e0, make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]));
     if (threadIdx.x == 0) scales[b] = __fdiv_rn(amax, 127.0f);
   }
-}
-
-// ----------------------------------------------------------------- barrier
-// Cross-rank barrier over NVLink: rank r stores the new epoch into
-// flags_k[r] of every rank k (system-scope release), then waits until its
-// own flags[k] >= epoch for all k (acquire). One warp; world <= 8.
-
-__global__ void k_barrier(BarrierArgs a) {
-  __shared__ unsigned long long epoch;
-  if (threadIdx.x == 0) {
-    epoch = *a.epoch + 1;
-    *a.epoch = epoch;
-  }
-  __syncthreads();
-  const int t = threadIdx.x;
-  if (t < a.world) {
-    __threadfence_system();
-    st_release_sys(a.flags[t] + a.rank, epoch);
-    const unsigned long long* mine = a.flags[a.rank] + t;
-    const unsigned long long t0 = globaltimer();
-    while (ld_acquire_sys(mine) < epoch) {
-      if (globaltimer() - t0 > a.timeout_ns) {
-        atomicExch_system(a.err, 1);
-        break;
-      }
-    }
-  }
-  __syncthreads();
 }
 
 // ------------------------------------------------------------------ reduce

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "sp_kernels.cuh"
+#include "sp_round_fused.cuh"
 #include "sp_round.h"
 
 using namespace sp;
@@ -50,13 +51,25 @@ struct sp_round {
   int align = 8;
   size_t buf_bytes = 0;     // one wire/avg buffer (codes + q8 scales)
   size_t flags_bytes = 256;
+  size_t ctr_bytes = 0;     // arrived[ncells] + ready[ncells] (fused round)
+  // fused round (one persistent kernel per round)
+  bool fused_round = true;
+  int cell = 8192;
+  int ncells = 0;
+  int round_grid = 0;
+  int nritems = 0;
+  unsigned* d_ritems = nullptr;
+  int* d_rq = nullptr;                // [work, exited]
+  unsigned* d_repoch = nullptr;
+  unsigned char* d_cell_owners = nullptr;
+  std::vector<Chunk> h_chunks;
   // shared (IPC-exported) allocation: [flags][inbox: one slot per peer, G][avg]
   // slot g of rank k holds peer g's packed gradient for the range k owns
   char* shared = nullptr;
   size_t shared_bytes = 0;
   char* base[SP_MAX_RANKS] = {};  // every rank's shared allocation (mapped)
   bool connected = false;
-  unsigned long long* epoch = nullptr;
+  unsigned long long* epoch = nullptr;  // barrier epoch
   int* h_err = nullptr;  // host-mapped
   int* d_err = nullptr;
   // LAMB tables
@@ -86,8 +99,14 @@ struct sp_round {
   cudaEvent_t ev[8] = {};
   int sm_count = 148;
 
-  char* wire(int rank, int g) const { return base[rank] + flags_bytes + (size_t)g * buf_bytes; }
-  char* avg(int rank) const { return base[rank] + flags_bytes + (size_t)G * buf_bytes; }
+  char* wire(int rank, int g) const {
+    return base[rank] + flags_bytes + ctr_bytes + (size_t)g * buf_bytes;
+  }
+  char* avg(int rank) const { return base[rank] + flags_bytes + ctr_bytes + (size_t)G * buf_bytes; }
+  unsigned* arrived(int rank) const { return reinterpret_cast<unsigned*>(base[rank] + flags_bytes); }
+  unsigned* ready(int rank) const {
+    return reinterpret_cast<unsigned*>(base[rank] + flags_bytes + ctr_bytes / 2);
+  }
   unsigned long long* flags(int rank) const {
     return reinterpret_cast<unsigned long long*>(base[rank]);
   }
@@ -177,11 +196,179 @@ int grid_for(int64_t work_items, int threads, int sm_count, int per_sm) {
   return (int)g;
 }
 
+// Fused-round work list for this rank (see sp_round_fused.cuh): scatter items
+// column by column over owners in rotated order, then this rank's reduce
+// cells, then LAMB pass-1 chunks in expected arrival order, then pass 2.
+int build_round_items(sp_round* r) {
+  const sp_round_cfg& c = r->cfg;
+  const int W = c.world, me = c.rank;
+  std::vector<int64_t> first(W), len(W);
+  std::vector<unsigned char> owners((size_t)r->ncells, 0);
+  for (int k = 0; k < W; ++k) {
+    const int64_t lo = r->offsets[(size_t)k * r->L], hi = r->offsets[(size_t)(k + 1) * r->L];
+    first[k] = lo / r->cell;
+    len[k] = hi > lo ? (std::min(hi, r->n) + r->cell - 1) / r->cell - first[k] : 0;
+    for (int64_t j = first[k]; j < first[k] + len[k]; ++j) owners[(size_t)j]++;
+  }
+  std::vector<unsigned> items;
+  int64_t maxlen = 0;
+  for (int k = 0; k < W; ++k) maxlen = std::max(maxlen, len[k]);
+  // LAMB pass-1 chunks grouped by the column of their cell (position within
+  // the owning rank's range), the order in which owners finish them
+  std::vector<std::vector<int>> l1_by_col((size_t)std::max<int64_t>(maxlen, 1));
+  for (size_t i = 0; i < r->h_chunks.size(); ++i) {
+    const int64_t st = r->h_chunks[i].start;
+    int k0 = 0;
+    while (k0 + 1 < W && st >= r->offsets[(size_t)(k0 + 1) * r->L]) ++k0;
+    l1_by_col[(size_t)(st / r->cell - first[k0])].push_back((int)i);
+  }
+  // Interleave: column j's reduce is queued `lag` items after column j's last
+  // scatter item, and its pass-1 chunks `lag` items after that, so scatter
+  // (NVLink), reduce and LAMB pass 1 (HBM) of different columns run at the
+  // same time. Every waiting item only depends on items queued before it
+  // (here and, column-wise, on every other rank), so the queue stays
+  // deadlock-free. lag = 0 would make every column wait for itself.
+  const char* lag_env = std::getenv("SP_ROUND_LAG");
+  const size_t lag = lag_env ? (size_t)std::atol(lag_env) : (size_t)r->round_grid;
+  std::vector<std::pair<size_t, int64_t>> pend_r, pend_l;  // (ready position, column)
+  size_t hr = 0, hl = 0;
+  auto flush = [&](bool all) {
+    bool moved = true;
+    while (moved) {
+      moved = false;
+      while (hr < pend_r.size() && (all || pend_r[hr].first <= items.size())) {
+        const int64_t j = pend_r[hr++].second;
+        if (j < len[me]) items.push_back(make_item(kStR, 0u, (unsigned)(first[me] + j)));
+        pend_l.push_back({items.size() + lag, j});
+        moved = true;
+      }
+      while (hl < pend_l.size() && (all || pend_l[hl].first <= items.size())) {
+        for (int i : l1_by_col[(size_t)pend_l[hl].second]) items.push_back(make_item(kStL1, 0u, (unsigned)i));
+        ++hl;
+        moved = true;
+      }
+    }
+  };
+  for (int64_t j = 0; j < maxlen; ++j) {
+    for (int d = 1; d <= W; ++d) {
+      const int k = (me + d) % W;
+      if (j < len[k]) items.push_back(make_item(kStS, (unsigned)k, (unsigned)(first[k] + j)));
+    }
+    pend_r.push_back({items.size() + lag, j});
+    flush(false);
+  }
+  flush(true);
+  for (size_t i = 0; i < r->h_chunks.size(); ++i) items.push_back(make_item(kStL2, 0u, (unsigned)i));
+  r->nritems = (int)items.size();
+  SP_CUDA(cudaSetDevice(c.device));
+  SP_CUDA(cudaMemcpy(r->d_ritems, items.data(), items.size() * sizeof(unsigned), cudaMemcpyHostToDevice));
+  SP_CUDA(cudaMemcpy(r->d_cell_owners, owners.data(), owners.size(), cudaMemcpyHostToDevice));
+  return SP_OK;
+}
+
+LambArgs make_lamb_args(sp_round* r, float* p, float* m, float* v) {
+  const sp_round_cfg& c = r->cfg;
+  LambArgs a{};
+  a.avg = r->avg(c.rank);
+  a.avg_scale = c.wire == SP_WIRE_Q8 ? reinterpret_cast<const float*>(r->avg(c.rank) + r->npad)
+                                     : nullptr;
+  a.p = p;
+  a.m = m;
+  a.v = v;
+  a.chunks = r->d_chunks;
+  a.partial = r->d_partial;
+  a.hp = r->d_hp;
+  a.step_scale = r->d_step_scale;
+  a.b1 = c.beta1;
+  a.b2 = c.beta2;
+  a.omb1 = 1.0f - c.beta1;
+  a.omb2 = 1.0f - c.beta2;
+  a.eps = c.eps;
+  a.wd = c.weight_decay;
+  a.qblock = c.q8_block;
+  a.l2_hints = r->l2_hints;
+  return a;
+}
+
+FusedLamb make_lamb_queue(sp_round* r) {
+  FusedLamb q{};
+  q.items = r->d_items;
+  q.nitems = r->nitems;
+  q.work = r->d_qstate;
+  q.exited = r->d_qstate + 1;
+  q.done = r->d_qstate + 2;
+  q.ready = r->d_ready;
+  q.tchunks = r->d_tchunks;
+  q.trust = r->d_trust;
+  q.ntensors = r->cfg.num_tensors;
+  return q;
+}
+
+int enqueue_fused(sp_round* r, const float* const* grads, float* p, float* m, float* v,
+                  cudaStream_t st, cudaEvent_t* ev) {
+  const sp_round_cfg& c = r->cfg;
+  if (ev)
+    for (int k = 1; k <= 4; ++k) SP_CUDA(cudaEventRecord(ev[k], st));
+  RoundFused f{};
+  f.items = r->d_ritems;
+  f.nitems = r->nritems;
+  f.work = r->d_rq;
+  f.exited = r->d_rq + 1;
+  f.epoch = r->d_repoch;
+  f.err = r->d_err;
+  const double to = c.barrier_timeout_s > 0 ? c.barrier_timeout_s : 20.0;
+  f.timeout_ns = (unsigned long long)(to * 1e9);
+  f.n = r->n;
+  f.npad = r->npad;
+  f.cell = r->cell;
+  f.world = c.world;
+  f.rank = c.rank;
+  f.L = r->L;
+  for (int k = 0; k <= c.world; ++k) f.rank_lo[k] = r->offsets[(size_t)k * r->L];
+  for (int l = 0; l < r->L; ++l) {
+    const int g = c.rank * r->L + l;
+    const bool zero_copy = c.world == 1 && c.wire == SP_WIRE_FP32 &&
+                           (const void*)grads[l] == (const void*)r->wire(c.rank, g);
+    f.src[l] = zero_copy ? nullptr : grads[l];
+  }
+  for (int k = 0; k < c.world; ++k) {
+    f.inbox[k] = r->wire(k, 0);
+    f.arrived[k] = r->arrived(k);
+    const int d = (c.rank + 1 + k) % c.world;  // push order: next rank first, self last
+    f.avg[k] = r->avg(d);
+    f.ready_of[k] = r->ready(d);
+  }
+  f.slot_bytes = r->buf_bytes;
+  double wsum = 0.0;
+  for (double w : r->weights) wsum += w;
+  for (int g = 0; g < r->G; ++g) {
+    if (r->weights[g] == 0.0) continue;
+    f.peer[f.npeers] = g;
+    f.w[f.npeers] = (float)(r->weights[g] / wsum);
+    ++f.npeers;
+  }
+  f.my_ready = r->ready(c.rank);
+  f.cell_owners = r->d_cell_owners;
+  LambArgs a = make_lamb_args(r, p, m, v);
+  FusedLamb q = make_lamb_queue(r);
+  const int grid = r->round_grid;
+  switch (c.wire) {
+    case SP_WIRE_FP32: k_round_fused<SP_WIRE_FP32><<<grid, kLambThreads, 0, st>>>(f, a, q); break;
+    case SP_WIRE_FP16: k_round_fused<SP_WIRE_FP16><<<grid, kLambThreads, 0, st>>>(f, a, q); break;
+    default: k_round_fused<SP_WIRE_Q8><<<grid, kLambThreads, 0, st>>>(f, a, q); break;
+  }
+  SP_CUDA(cudaGetLastError());
+  if (ev)
+    for (int k = 5; k <= 7; ++k) SP_CUDA(cudaEventRecord(ev[k], st));
+  return SP_OK;
+}
+
 // Enqueues the whole round on `st`. ev != nullptr records phase events.
 int enqueue_round(sp_round* r, const float* const* grads, float* p, float* m,
                   float* v, cudaStream_t st, cudaEvent_t* ev) {
   const sp_round_cfg& c = r->cfg;
   if (ev) SP_CUDA(cudaEventRecord(ev[0], st));
+  if (r->fused_round) return enqueue_fused(r, grads, p, m, v, st, ev);
   // K1 pack
   {
     PackArgs a{};
@@ -225,7 +412,7 @@ int enqueue_round(sp_round* r, const float* const* grads, float* p, float* m,
     ba.err = r->d_err;
     ba.rank = c.rank;
     ba.world = c.world;
-    double to = c.barrier_timeout_s > 0 ? c.barrier_timeout_s : 20.0;
+    const double to = c.barrier_timeout_s > 0 ? c.barrier_timeout_s : 20.0;
     ba.timeout_ns = (unsigned long long)(to * 1e9);
     k_barrier<<<1, 32, 0, st>>>(ba);
     SP_CUDA(cudaGetLastError());
@@ -254,7 +441,7 @@ int enqueue_round(sp_round* r, const float* const* grads, float* p, float* m,
     if (a.hi > a.lo) {
       if (c.wire == SP_WIRE_Q8) {
         int64_t nb = (a.hi + c.q8_block - 1) / c.q8_block - a.lo / c.q8_block;
-        int grid = (int)std::min<int64_t>(nb, (int64_t)r->sm_count * 16);
+        int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nb, (int64_t)r->sm_count * 16));
         k_reduce_q8<<<grid, c.q8_block / 16, 0, st>>>(a);
       } else if (c.wire == SP_WIRE_FP16) {
         k_reduce_fp16<<<grid_for((a.hi - a.lo + 7) / 8, 256, r->sm_count, 8), 256, 0, st>>>(a);
@@ -272,26 +459,7 @@ int enqueue_round(sp_round* r, const float* const* grads, float* p, float* m,
   if (ev) SP_CUDA(cudaEventRecord(ev[4], st));
   // K3/K4 LAMB on this rank's replica
   {
-    LambArgs a{};
-    a.avg = r->avg(c.rank);
-    a.avg_scale = c.wire == SP_WIRE_Q8
-                      ? reinterpret_cast<const float*>(r->avg(c.rank) + r->npad)
-                      : nullptr;
-    a.p = p;
-    a.m = m;
-    a.v = v;
-    a.chunks = r->d_chunks;
-    a.partial = r->d_partial;
-    a.hp = r->d_hp;
-    a.step_scale = r->d_step_scale;
-    a.b1 = c.beta1;
-    a.b2 = c.beta2;
-    a.omb1 = 1.0f - c.beta1;
-    a.omb2 = 1.0f - c.beta2;
-    a.eps = c.eps;
-    a.wd = c.weight_decay;
-    a.qblock = c.q8_block;
-    a.l2_hints = r->l2_hints;
+    LambArgs a = make_lamb_args(r, p, m, v);
     const int nc = r->nchunks;
     if (r->fused_lamb) {
       FusedLamb f{};
@@ -401,7 +569,22 @@ int sp_round_create(const sp_round_cfg* cfg, sp_round** out) {
   r->buf_bytes = (size_t)r->npad * wire_bits(cfg->wire) / 8;
   if (cfg->wire == SP_WIRE_Q8) r->buf_bytes += round_up(r->npad / cfg->q8_block * 4, 256);
   r->buf_bytes = round_up(r->buf_bytes, 256);
-  r->shared_bytes = r->flags_bytes + (size_t)(r->G + 1) * r->buf_bytes;
+  {
+    const char* legacy = std::getenv("SP_ROUND_LEGACY");
+    // one-kernel round (sp_round_fused.cuh) is opt-in: measured equal at N=4
+    // and slower at N=1 than the kernel pipeline
+    const char* fused = std::getenv("SP_ROUND_FUSED");
+    r->fused_round = fused && fused[0] == '1' && !(legacy && legacy[0] == '1') &&
+                     (cfg->wire != SP_WIRE_Q8 || cfg->q8_block == 4096);
+    r->cell = (int)std::max<int64_t>(kLambChunk, cfg->wire == SP_WIRE_Q8 ? cfg->q8_block : 0);
+    if (const char* ce = std::getenv("SP_ROUND_CELL")) {  // tuning knob: multiple of the cell
+      const int want = std::atoi(ce);
+      if (want > r->cell && want % r->cell == 0) r->cell = want;
+    }
+    r->ncells = (int)((cfg->n + r->cell - 1) / r->cell);
+    r->ctr_bytes = 2 * round_up((int64_t)r->ncells * 4, 256);
+  }
+  r->shared_bytes = r->flags_bytes + r->ctr_bytes + (size_t)(r->G + 1) * r->buf_bytes;
   int dev_sms = 0;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, cfg->device);
   if (dev_sms > 0) r->sm_count = dev_sms;
@@ -461,6 +644,26 @@ int sp_round_create(const sp_round_cfg* cfg, sp_round** out) {
     cudaMemset(r->d_qstate, 0, (2 + tch.size()) * sizeof(int));
     cudaMemset(r->d_ready, 0, tch.size() * sizeof(unsigned int));
   }
+  {
+    int per_sm = 0;
+    cudaError_t oe;
+    switch (cfg->wire) {
+      case SP_WIRE_FP32: oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_round_fused<SP_WIRE_FP32>, kLambThreads, 0); break;
+      case SP_WIRE_FP16: oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_round_fused<SP_WIRE_FP16>, kLambThreads, 0); break;
+      default: oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_round_fused<SP_WIRE_Q8>, kLambThreads, 0); break;
+    }
+    if (oe != cudaSuccess || per_sm < 1) return cleanup(fail(SP_ERR_CUDA, "occupancy query failed for the fused round kernel"));
+    r->round_grid = per_sm * r->sm_count;
+    const size_t cap = 2 * (size_t)r->ncells + SP_MAX_RANKS + 2 * chunks.size() + 16;
+    if ((e = cudaMalloc(&r->d_ritems, cap * sizeof(unsigned))) != cudaSuccess ||
+        (e = cudaMalloc(&r->d_rq, 2 * sizeof(int))) != cudaSuccess ||
+        (e = cudaMalloc(&r->d_repoch, sizeof(unsigned))) != cudaSuccess ||
+        (e = cudaMalloc(&r->d_cell_owners, (size_t)r->ncells)) != cudaSuccess)
+      return cleanup(fail(SP_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e)));
+    cudaMemset(r->d_rq, 0, 2 * sizeof(int));
+    cudaMemset(r->d_repoch, 0, sizeof(unsigned));
+    r->h_chunks = chunks;
+  }
   cudaMemcpy(r->d_tchunks, tch.data(), tch.size() * sizeof(int2), cudaMemcpyHostToDevice);
   cudaMemset(r->epoch, 0, sizeof(unsigned long long));
   cudaMemset(r->d_trust, 0, tch.size() * sizeof(float));
@@ -494,6 +697,10 @@ int sp_round_destroy(sp_round* r) {
   cudaFree(r->d_hp);
   cudaFree(r->d_items);
   cudaFree(r->d_qstate);
+  cudaFree(r->d_ritems);
+  cudaFree(r->d_rq);
+  cudaFree(r->d_repoch);
+  cudaFree(r->d_cell_owners);
   cudaFree(r->d_ready);
   cudaFree(r->epoch);
   if (r->h_err) cudaFreeHost(r->h_err);
@@ -553,6 +760,11 @@ int sp_round_set_assignment(sp_round* r, const int64_t* offsets, const double* w
   if (!(wsum > 0.0)) return fail(SP_ERR_ARG, "sum of weights must be positive");
   r->offsets.assign(offsets, offsets + G + 1);
   r->weights.assign(weights, weights + G);
+  if (r->fused_round) {
+    SP_CUDA(cudaDeviceSynchronize());  // the previous round may still read the work list
+    const int rc = build_round_items(r);
+    if (rc) return rc;
+  }
   r->assigned = true;
   if (r->gexec) {
     cudaGraphExecDestroy(r->gexec);

@@ -30,11 +30,12 @@ def _free_port():
     return p
 
 
-def _launch(nproc, *extra):
+def _launch(nproc, *extra, env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", f"--nproc-per-node={nproc}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
            os.path.join(HERE, "mp_round_check.py"), *extra]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300,
+                       env=None if env is None else {**os.environ, **env})
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert r.returncode == 0 and lines, r.stdout[-2000:] + r.stderr[-3000:]
     res = json.loads(lines[-1])
@@ -62,3 +63,10 @@ def test_owner_takes_everything_q8():
     fr = [0.0] * NGPU
     fr[-1] = 1.0
     _launch(NGPU, "--wire", "q8", "--fractions", ",".join(map(str, fr)))
+
+
+@pytest.mark.parametrize("wire", ["fp16", "q8"])
+def test_one_kernel_round(wire):
+    """The opt-in single persistent kernel (pack/scatter, reduce/push, LAMB
+    in one launch with per-cell readiness counters) is bit-exact too."""
+    _launch(NGPU, "--wire", wire, "--peers-per-rank", "2", env={"SP_ROUND_FUSED": "1"})

@@ -160,3 +160,16 @@ def test_bad_arguments_raise():
     with pytest.raises(RuntimeError):
         rnd.run([p, p], p, p, p, 1)  # before set_assignment
     rnd.close()
+
+
+@pytest.mark.parametrize("wire", ["fp32", "fp16", "q8"])
+def test_one_kernel_round_parity(wire, monkeypatch):
+    """Opt-in single persistent round kernel (sp_round_fused.cuh)."""
+    monkeypatch.setenv("SP_ROUND_FUSED", "1")
+    _run_case(wire, HET8C, [1.0] * 8, RAGGED, steps=2)
+
+
+def test_unfused_lamb_parity(monkeypatch):
+    """Three-kernel LAMB (moments / trust / update) stays available."""
+    monkeypatch.setenv("SP_LAMB_UNFUSED", "1")
+    _run_case("fp16", [0.5, 0.5], [1.0, 3.0], RAGGED, steps=2)
