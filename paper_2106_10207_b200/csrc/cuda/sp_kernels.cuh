@@ -33,41 +33,38 @@ struct BarrierArgs {
 
 // K1 scatters each local peer's packed gradient straight into the inbox of
 // the rank that owns each element range (local HBM or a peer GPU over
-// NVLink): posted writes only, no pull reads in the exchange.
+// NVLink): posted writes only, no pull reads in the exchange. The kernel
+// walks a list of ranges (one per owner, possibly one segment of each
+// owner's range) in the given order. The host orders them starting with the
+// next rank's range and ending with its own, so at any moment the ranks
+// write to different owners: all-to-all without incast (4x B200: ~660
+// GB/s/dir rotated vs ~400 GB/s when every rank targets the same owner,
+// profiles/r01/p2p_bw.txt).
 struct PackArgs {
   const float* src[SP_MAX_LOCAL];          // accumulated fp32 grad of local peer l
   void* dst[SP_MAX_LOCAL][SP_MAX_RANKS];   // inbox slot of local peer l on rank k
-  int64_t rank_lo[SP_MAX_RANKS + 1];       // element range owned by rank k
-  int world;
+  int nr;                                  // ranges, in visiting order
+  int owner[SP_MAX_RANKS];                 // owner rank of range j
+  int64_t lo[SP_MAX_RANKS];                // first unit of range j (vector / q8 block)
+  int64_t pref[SP_MAX_RANKS + 1];          // prefix sums of range lengths in units
   int64_t n;                               // valid elements
   int64_t npad;                            // padded elements (multiple of kPad)
   int qblock;                              // q8 block
-  int64_t rot;                             // traversal starts at this element (see below)
 };
 
-// Every rank walks the vector starting at the range of the next rank
-// (rot = rank_lo[(rank+1) % world]) and ends with its own range, so at any
-// moment the ranks write to different owners: all-to-all without incast
-// (B200 4-GPU measurement: ~660 GB/s/dir rotated vs ~400 GB/s when every
-// rank targets the same owner, profiles/r01/p2p_bw.txt).
-__device__ __forceinline__ int64_t rotated(int64_t v, int64_t rot_units, int64_t nunits) {
-  v += rot_units;
-  return v >= nunits ? v - nunits : v;
-}
-
-__device__ __forceinline__ int owner_of(const PackArgs& a, int64_t e) {
-  int k = 0;
-  while (k + 1 < a.world && e >= a.rank_lo[k + 1]) ++k;
-  return k;
+__device__ __forceinline__ int range_of(const PackArgs& a, int64_t u) {
+  int j = 0;
+  while (j + 1 < a.nr && u >= a.pref[j + 1]) ++j;
+  return j;
 }
 
 struct ReduceArgs {
-  const void* src[SP_MAX_PEERS];  // wire buffer of each contributing peer
+  const void* src[SP_MAX_PEERS];  // inbox slot of each contributing peer (local)
   float w[SP_MAX_PEERS];          // normalized weight w_g / sum(w), fp32
-  void* dst[SP_MAX_RANKS];        // avg buffer of every rank (local or peer)
+  void* dst[SP_MAX_RANKS];        // avg buffer of every rank, push order
   int npeers;                     // contributing (nonzero-weight) peers
   int ndst;
-  int64_t lo, hi;                 // element range reduced by this rank
+  int64_t lo, hi;                 // element range reduced by this launch
   int64_t npad;
   int qblock;
 };
@@ -245,11 +242,12 @@ __global__ void k_barrier(BarrierArgs a) {
 
 __global__ void __launch_bounds__(256) k_pack_fp32(PackArgs a) {
   const float* __restrict__ src = a.src[blockIdx.y];
-  const int64_t nvec = src ? a.npad / 4 : 0;
+  const int64_t nunits = src ? a.pref[a.nr] : 0;
   const int64_t nfull = a.n / 4;
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nvec;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nunits;
        w += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = rotated(w, a.rot / 4, nvec);
+    const int j = range_of(a, w);
+    const int64_t v = a.lo[j] + (w - a.pref[j]);
     float4 x;
     if (v < nfull) {
       x = __ldg(reinterpret_cast<const float4*>(src) + v);
@@ -260,7 +258,7 @@ __global__ void __launch_bounds__(256) k_pack_fp32(PackArgs a) {
       x.z = e + 2 < a.n ? src[e + 2] : 0.0f;
       x.w = e + 3 < a.n ? src[e + 3] : 0.0f;
     }
-    float* dst = static_cast<float*>(a.dst[blockIdx.y][owner_of(a, v * 4)]);
+    float* dst = static_cast<float*>(a.dst[blockIdx.y][a.owner[j]]);
     reinterpret_cast<float4*>(dst)[v] = x;
   }
 }
@@ -277,11 +275,12 @@ __device__ __forceinline__ float2 unpack_half2(uint32_t u) {
 
 __global__ void __launch_bounds__(256) k_pack_fp16(PackArgs a) {
   const float* __restrict__ src = a.src[blockIdx.y];
-  const int64_t nvec = src ? a.npad / 8 : 0;
+  const int64_t nunits = src ? a.pref[a.nr] : 0;
   const int64_t nfull = a.n / 8;
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nvec;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nunits;
        w += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = rotated(w, a.rot / 8, nvec);
+    const int j = range_of(a, w);
+    const int64_t v = a.lo[j] + (w - a.pref[j]);
     float x[8];
     if (v < nfull) {
       float4 a0 = __ldg(reinterpret_cast<const float4*>(src) + 2 * v);
@@ -300,7 +299,7 @@ __global__ void __launch_bounds__(256) k_pack_fp16(PackArgs a) {
     o.y = (int)pack_half2(x[2], x[3]);
     o.z = (int)pack_half2(x[4], x[5]);
     o.w = (int)pack_half2(x[6], x[7]);
-    char* dst = static_cast<char*>(a.dst[blockIdx.y][owner_of(a, v * 8)]);
+    char* dst = static_cast<char*>(a.dst[blockIdx.y][a.owner[j]]);
     st_v4(dst + v * 16, o);
   }
 }
@@ -310,10 +309,11 @@ __global__ void __launch_bounds__(256) k_pack_fp16(PackArgs a) {
 __global__ void k_pack_q8(PackArgs a) {
   __shared__ float red[32];
   const float* __restrict__ src = a.src[blockIdx.y];
-  const int64_t nblk = src ? a.npad / a.qblock : 0;
+  const int64_t nblk = src ? a.pref[a.nr] : 0;
   for (int64_t bb = blockIdx.x; bb < nblk; bb += gridDim.x) {
-    const int64_t b = rotated(bb, a.rot / a.qblock, nblk);
-    int8_t* __restrict__ codes = static_cast<int8_t*>(a.dst[blockIdx.y][owner_of(a, b * a.qblock)]);
+    const int j = range_of(a, bb);
+    const int64_t b = a.lo[j] + (bb - a.pref[j]);
+    int8_t* __restrict__ codes = static_cast<int8_t*>(a.dst[blockIdx.y][a.owner[j]]);
     float* __restrict__ scales = reinterpret_cast<float*>(codes + a.npad);
     const int64_t e0 = b * a.qblock + threadIdx.x * 16;
     float x[16];
@@ -681,6 +681,7 @@ struct FusedLamb {
   const int2* tchunks;     // per tensor [first, last) chunk
   float* trust;
   int ntensors;
+  int final_launch;        // last LAMB launch of the round: clears the trust flags
 };
 
 template <int W>
@@ -903,7 +904,8 @@ __global__ void __launch_bounds__(kLambThreads) k_lamb_fused(LambArgs a, FusedLa
   if (tid == 0) {
     __threadfence();
     if (atomicAdd(f.exited, 1) == (int)gridDim.x - 1) {  // last CTA out resets the queue
-      for (int t = 0; t < f.ntensors; ++t) f.ready[t] = 0u;
+      if (f.final_launch)
+        for (int t = 0; t < f.ntensors; ++t) f.ready[t] = 0u;
       *f.work = 0;
       *f.exited = 0;
       __threadfence();

@@ -74,6 +74,17 @@ struct sp_round {
   int* d_err = nullptr;
   // LAMB tables
   int nchunks = 0;
+  int nchunks_cap = 0;
+  int64_t lamb_chunk = kLambChunk;
+  // segmented pipeline (world > 1): exchange of segment s+1 overlaps LAMB
+  // pass 1 of segment s on the aux stream
+  int segments = 1;
+  int seg_lamb_grid = 1 << 30;  // CTA cap of a segment's pass-1 launch
+  int xchg_per_sm = 8;          // CTAs per SM of the exchange kernels
+  std::vector<int> p1_off;   // K+1 offsets of the per-segment pass-1 item lists
+  int p2_off = 0;            // pass-2 items
+  cudaStream_t aux = nullptr;
+  cudaEvent_t seg_ev[9] = {};
   Chunk* d_chunks = nullptr;
   int2* d_tchunks = nullptr;
   float2* d_partial = nullptr;
@@ -142,52 +153,77 @@ int validate_cfg(const sp_round_cfg* c) {
   return SP_OK;
 }
 
-// LAMB chunks: tensor t covers [off_t, off_t+size_t); chunk boundaries are
-// the tensor edges plus every multiple of kLambChunk inside the tensor.
-void build_chunks(const std::vector<int64_t>& sizes, int64_t chunk, std::vector<Chunk>& chunks,
-                  std::vector<int2>& tch) {
+// Element boundaries where LAMB chunks must split so each chunk lies in one
+// segment of one owner's range: owner k's range [lo, hi) is cut at
+// lo + align_down((hi - lo) * s / K, align), s = 0..K.
+int64_t seg_cut(const sp_round* r, int k, int s) {
+  const int64_t lo = r->offsets[(size_t)k * r->L], hi = r->offsets[(size_t)(k + 1) * r->L];
+  if (s >= r->segments) return hi;
+  return lo + (hi - lo) * s / r->segments / r->align * r->align;
+}
+
+// Chunk table (tensor edges, every multiple of lamb_chunk, segment cuts),
+// per-tensor chunk ranges and the fused-LAMB work lists:
+//   [pass 1 of segment 0] ... [pass 1 of segment K-1] [pass 2 of all chunks].
+// With K = 1 one launch walks both lists (pass 1 first: the in-flight window
+// of the persistent grid exceeds L2, so a shorter lag only adds trust waits,
+// profiles/r01/lamb_sweep.txt).
+int build_lamb_tables(sp_round* r, bool with_cuts) {
+  std::vector<int64_t> cuts;
+  if (with_cuts && r->segments > 1)
+    for (int k = 0; k < r->cfg.world; ++k)
+      for (int s = 1; s < r->segments; ++s) cuts.push_back(seg_cut(r, k, s));
+  std::sort(cuts.begin(), cuts.end());
+  std::vector<Chunk> chunks;
+  std::vector<int2> tch;
   int64_t off = 0;
-  for (size_t t = 0; t < sizes.size(); ++t) {
-    const int64_t end = off + sizes[t];
-    int2 r;
-    r.x = (int)chunks.size();
+  size_t ci = 0;
+  for (size_t t = 0; t < r->tsizes.size(); ++t) {
+    const int64_t end = off + r->tsizes[t];
+    int2 rg;
+    rg.x = (int)chunks.size();
     int64_t s = off;
     while (s < end) {
-      int64_t e = std::min(end, (s / chunk + 1) * chunk);
+      int64_t e = std::min(end, (s / r->lamb_chunk + 1) * r->lamb_chunk);
+      while (ci < cuts.size() && cuts[ci] <= s) ++ci;
+      if (ci < cuts.size() && cuts[ci] < e) e = cuts[ci];
       chunks.push_back(Chunk{(long long)s, (int)(e - s), (int)t});
       s = e;
     }
-    r.y = (int)chunks.size();
-    tch.push_back(r);
+    rg.y = (int)chunks.size();
+    tch.push_back(rg);
     off = end;
   }
-}
-
-// Fused-LAMB dispatch order: pass-1 chunks in tensor order; the pass-2
-// chunks of tensor t follow once `lag` further items were emitted after t's
-// last pass-1 chunk (about one wave of the persistent grid), so they find
-// t's trust ratio ready and its p/m/v still in L2.
-std::vector<int> build_lamb_items(const std::vector<Chunk>& chunks, const std::vector<int2>& tch,
-                                  int lag) {
-  std::vector<int> out;
-  out.reserve(chunks.size() * 2);
-  std::vector<std::pair<int, size_t>> pending;  // (tensor, position after its last pass-1 item)
-  size_t head = 0;
-  auto flush = [&](bool all) {
-    while (head < pending.size() && (all || pending[head].second + (size_t)lag <= out.size())) {
-      const int2 r = tch[pending[head].first];
-      for (int c = r.x; c < r.y; ++c) out.push_back(~c);
-      ++head;
-    }
-  };
+  if ((int)chunks.size() > r->nchunks_cap) return fail(SP_ERR_STATE, "LAMB chunk table overflow");
+  const int K = with_cuts ? r->segments : 1;
+  std::vector<std::vector<int>> p1((size_t)K);
   for (size_t c = 0; c < chunks.size(); ++c) {
-    out.push_back((int)c);
-    const int t = chunks[c].tensor;
-    if ((int)c == tch[t].y - 1) pending.emplace_back(t, out.size());
-    flush(false);
+    int seg = 0;
+    if (K > 1) {
+      const int64_t st = chunks[c].start;
+      int k0 = 0;
+      while (k0 + 1 < r->cfg.world && st >= r->offsets[(size_t)(k0 + 1) * r->L]) ++k0;
+      while (seg + 1 < K && st >= seg_cut(r, k0, seg + 1)) ++seg;
+    }
+    p1[(size_t)seg].push_back((int)c);
   }
-  flush(true);
-  return out;
+  std::vector<int> items;
+  r->p1_off.assign((size_t)K + 1, 0);
+  for (int q = 0; q < K; ++q) {
+    r->p1_off[(size_t)q] = (int)items.size();
+    items.insert(items.end(), p1[(size_t)q].begin(), p1[(size_t)q].end());
+  }
+  r->p1_off[(size_t)K] = (int)items.size();
+  r->p2_off = (int)items.size();
+  for (size_t c = 0; c < chunks.size(); ++c) items.push_back(~(int)c);
+  r->nchunks = (int)chunks.size();
+  r->nitems = (int)items.size();
+  r->h_chunks = chunks;
+  SP_CUDA(cudaSetDevice(r->cfg.device));
+  SP_CUDA(cudaMemcpy(r->d_chunks, chunks.data(), chunks.size() * sizeof(Chunk), cudaMemcpyHostToDevice));
+  SP_CUDA(cudaMemcpy(r->d_tchunks, tch.data(), tch.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  SP_CUDA(cudaMemcpy(r->d_items, items.data(), items.size() * sizeof(int), cudaMemcpyHostToDevice));
+  return SP_OK;
 }
 
 int grid_for(int64_t work_items, int threads, int sm_count, int per_sm) {
@@ -364,18 +400,60 @@ int enqueue_fused(sp_round* r, const float* const* grads, float* p, float* m, fl
 }
 
 // Enqueues the whole round on `st`. ev != nullptr records phase events.
-int enqueue_round(sp_round* r, const float* const* grads, float* p, float* m,
-                  float* v, cudaStream_t st, cudaEvent_t* ev) {
+int launch_lamb(sp_round* r, LambArgs a, int first_item, int nitems, bool final_launch,
+                cudaStream_t st) {
+  const sp_round_cfg& c = r->cfg;
+  FusedLamb f = make_lamb_queue(r);
+  f.items = r->d_items + first_item;
+  f.nitems = nitems;
+  f.final_launch = final_launch ? 1 : 0;
+  if (nitems <= 0 && !final_launch) return SP_OK;
+  // a segment's pass 1 shares the GPU with the next segment's exchange
+  const int cap = final_launch ? r->lamb_grid : std::min(r->lamb_grid, r->seg_lamb_grid);
+  const int g = std::max(1, std::min(cap, nitems));
+  switch (c.wire) {
+    case SP_WIRE_FP32: k_lamb_fused<SP_WIRE_FP32><<<g, kLambThreads, 0, st>>>(a, f); break;
+    case SP_WIRE_FP16: k_lamb_fused<SP_WIRE_FP16><<<g, kLambThreads, 0, st>>>(a, f); break;
+    default: k_lamb_fused<SP_WIRE_Q8><<<g, kLambThreads, 0, st>>>(a, f); break;
+  }
+  SP_CUDA(cudaGetLastError());
+  return SP_OK;
+}
+
+// Enqueues the whole round on `st`. ev != nullptr records phase events.
+//
+// Kernel pipeline per segment s = 0..K-1 (K = 1 with one rank):
+//   K1 pack+scatter(s) -> barrier -> K2 reduce+push(s) -> barrier
+// and, with K > 1, LAMB pass 1 of segment s on the aux stream as soon as its
+// second barrier passed, overlapping the exchange of segment s+1; then
+// LAMB pass 2 (all chunks) on `st` after joining the aux stream.
+// Phase events (diagnostic): pack / barrier / reduce of segment 0, the
+// remaining exchange, then LAMB.
+int enqueue_round(sp_round* r, const float* const* grads, float* p, float* m, float* v,
+                  cudaStream_t st, cudaEvent_t* ev) {
   const sp_round_cfg& c = r->cfg;
   if (ev) SP_CUDA(cudaEventRecord(ev[0], st));
   if (r->fused_round) return enqueue_fused(r, grads, p, m, v, st, ev);
-  // K1 pack
-  {
+  const int K = r->segments;
+  BarrierArgs ba{};
+  if (c.world > 1) {
+    for (int k = 0; k < c.world; ++k) ba.flags[k] = r->flags(k);
+    ba.epoch = r->epoch;
+    ba.err = r->d_err;
+    ba.rank = c.rank;
+    ba.world = c.world;
+    const double to = c.barrier_timeout_s > 0 ? c.barrier_timeout_s : 20.0;
+    ba.timeout_ns = (unsigned long long)(to * 1e9);
+  }
+  const LambArgs la = make_lamb_args(r, p, m, v);
+  if (K > 1) {  // fork the aux stream off `st` (graph-capture safe)
+    SP_CUDA(cudaEventRecord(r->seg_ev[8], st));
+    SP_CUDA(cudaStreamWaitEvent(r->aux, r->seg_ev[8], 0));
+  }
+  for (int s = 0; s < K; ++s) {
+    // K1: pack this segment of every owner's range, next rank's first
     PackArgs a{};
     bool any = false;
-    a.world = c.world;
-    for (int k = 0; k <= c.world; ++k) a.rank_lo[k] = r->offsets[(size_t)k * r->L];
-    a.rot = c.world > 1 ? a.rank_lo[(c.rank + 1) % c.world] : 0;  // multiple of align
     for (int l = 0; l < r->L; ++l) {
       const int g = c.rank * r->L + l;
       a.src[l] = grads[l];
@@ -387,121 +465,125 @@ int enqueue_round(sp_round* r, const float* const* grads, float* p, float* m,
       else
         a.src[l] = nullptr;  // nothing to pack (aggregation-only or zero-copy)
     }
+    const int64_t unit = c.wire == SP_WIRE_Q8 ? c.q8_block : (c.wire == SP_WIRE_FP16 ? 8 : 4);
+    a.nr = 0;
+    a.pref[0] = 0;
+    for (int d = 1; d <= c.world; ++d) {
+      const int k = (c.rank + d) % c.world;
+      const int64_t lo = seg_cut(r, k, s), hi = seg_cut(r, k, s + 1);
+      if (hi <= lo) continue;
+      a.owner[a.nr] = k;
+      a.lo[a.nr] = lo / unit;
+      a.pref[a.nr + 1] = a.pref[a.nr] + (hi + unit - 1) / unit - lo / unit;
+      ++a.nr;
+    }
     a.n = r->n;
     a.npad = r->npad;
     a.qblock = c.q8_block;
-    if (any) {
+    const int64_t units = a.pref[a.nr];
+    if (any && units > 0) {
       if (c.wire == SP_WIRE_Q8) {
-        dim3 grid(std::min<int64_t>(r->npad / c.q8_block, (int64_t)r->sm_count * 16), r->L);
+        dim3 grid((unsigned)std::min<int64_t>(units, (int64_t)r->sm_count * 16), r->L);
         k_pack_q8<<<grid, c.q8_block / 16, 0, st>>>(a);
       } else if (c.wire == SP_WIRE_FP16) {
-        dim3 grid(grid_for(r->npad / 8, 256, r->sm_count, 8), r->L);
+        dim3 grid(grid_for(units, 256, r->sm_count, r->xchg_per_sm), r->L);
         k_pack_fp16<<<grid, 256, 0, st>>>(a);
       } else {
-        dim3 grid(grid_for(r->npad / 4, 256, r->sm_count, 8), r->L);
+        dim3 grid(grid_for(units, 256, r->sm_count, r->xchg_per_sm), r->L);
         k_pack_fp32<<<grid, 256, 0, st>>>(a);
       }
       SP_CUDA(cudaGetLastError());
     }
-  }
-  if (ev) SP_CUDA(cudaEventRecord(ev[1], st));
-  BarrierArgs ba{};
-  if (c.world > 1) {
-    for (int k = 0; k < c.world; ++k) ba.flags[k] = r->flags(k);
-    ba.epoch = r->epoch;
-    ba.err = r->d_err;
-    ba.rank = c.rank;
-    ba.world = c.world;
-    const double to = c.barrier_timeout_s > 0 ? c.barrier_timeout_s : 20.0;
-    ba.timeout_ns = (unsigned long long)(to * 1e9);
-    k_barrier<<<1, 32, 0, st>>>(ba);
-    SP_CUDA(cudaGetLastError());
-  }
-  if (ev) SP_CUDA(cudaEventRecord(ev[2], st));
-  // K2 fused reduce-scatter / average / all-gather
-  {
-    ReduceArgs a{};
-    double wsum = 0.0;
-    for (double w : r->weights) wsum += w;
-    int np = 0;
-    for (int g = 0; g < r->G; ++g) {
-      if (r->weights[g] == 0.0) continue;
-      a.src[np] = r->wire(c.rank, g);  // this rank's inbox: local HBM only
-      a.w[np] = (float)(r->weights[g] / wsum);
-      ++np;
-    }
-    a.npeers = np;
-    a.ndst = c.world;
-    // push order rotated per rank (next rank first, self last): no incast
-    for (int k = 0; k < c.world; ++k) a.dst[k] = r->avg((c.rank + 1 + k) % c.world);
-    a.lo = r->offsets[(size_t)c.rank * r->L];
-    a.hi = r->offsets[(size_t)(c.rank + 1) * r->L];
-    a.npad = r->npad;
-    a.qblock = c.q8_block;
-    if (a.hi > a.lo) {
-      if (c.wire == SP_WIRE_Q8) {
-        int64_t nb = (a.hi + c.q8_block - 1) / c.q8_block - a.lo / c.q8_block;
-        int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nb, (int64_t)r->sm_count * 16));
-        k_reduce_q8<<<grid, c.q8_block / 16, 0, st>>>(a);
-      } else if (c.wire == SP_WIRE_FP16) {
-        k_reduce_fp16<<<grid_for((a.hi - a.lo + 7) / 8, 256, r->sm_count, 8), 256, 0, st>>>(a);
-      } else {
-        k_reduce_fp32<<<grid_for((a.hi - a.lo + 3) / 4, 256, r->sm_count, 8), 256, 0, st>>>(a);
-      }
+    if (ev && s == 0) SP_CUDA(cudaEventRecord(ev[1], st));
+    if (c.world > 1) {
+      k_barrier<<<1, 32, 0, st>>>(ba);
       SP_CUDA(cudaGetLastError());
     }
-  }
-  if (ev) SP_CUDA(cudaEventRecord(ev[3], st));
-  if (c.world > 1) {
-    k_barrier<<<1, 32, 0, st>>>(ba);
-    SP_CUDA(cudaGetLastError());
+    if (ev && s == 0) SP_CUDA(cudaEventRecord(ev[2], st));
+    // K2: average this rank's segment, push it to every rank (self last)
+    {
+      ReduceArgs ra{};
+      double wsum = 0.0;
+      for (double w : r->weights) wsum += w;
+      int np = 0;
+      for (int g = 0; g < r->G; ++g) {
+        if (r->weights[g] == 0.0) continue;
+        ra.src[np] = r->wire(c.rank, g);  // this rank's inbox: local HBM only
+        ra.w[np] = (float)(r->weights[g] / wsum);
+        ++np;
+      }
+      ra.npeers = np;
+      ra.ndst = c.world;
+      for (int k = 0; k < c.world; ++k) ra.dst[k] = r->avg((c.rank + 1 + k) % c.world);
+      ra.lo = seg_cut(r, c.rank, s);
+      ra.hi = seg_cut(r, c.rank, s + 1);
+      ra.npad = r->npad;
+      ra.qblock = c.q8_block;
+      if (ra.hi > ra.lo) {
+        if (c.wire == SP_WIRE_Q8) {
+          const int64_t nb = (ra.hi + c.q8_block - 1) / c.q8_block - ra.lo / c.q8_block;
+          const int grid = (int)std::min<int64_t>(nb, (int64_t)r->sm_count * 16);
+          k_reduce_q8<<<grid, c.q8_block / 16, 0, st>>>(ra);
+        } else if (c.wire == SP_WIRE_FP16) {
+          k_reduce_fp16<<<grid_for((ra.hi - ra.lo + 7) / 8, 256, r->sm_count, r->xchg_per_sm), 256, 0, st>>>(ra);
+        } else {
+          k_reduce_fp32<<<grid_for((ra.hi - ra.lo + 3) / 4, 256, r->sm_count, r->xchg_per_sm), 256, 0, st>>>(ra);
+        }
+        SP_CUDA(cudaGetLastError());
+      }
+    }
+    if (ev && s == 0) SP_CUDA(cudaEventRecord(ev[3], st));
+    if (c.world > 1) {
+      k_barrier<<<1, 32, 0, st>>>(ba);
+      SP_CUDA(cudaGetLastError());
+    }
+    if (K > 1) {  // LAMB pass 1 of this segment overlaps the next exchange
+      SP_CUDA(cudaEventRecord(r->seg_ev[s], st));
+      SP_CUDA(cudaStreamWaitEvent(r->aux, r->seg_ev[s], 0));
+      const int rc = launch_lamb(r, la, r->p1_off[(size_t)s], r->p1_off[(size_t)s + 1] - r->p1_off[(size_t)s],
+                                 false, r->aux);
+      if (rc) return rc;
+    }
   }
   if (ev) SP_CUDA(cudaEventRecord(ev[4], st));
   // K3/K4 LAMB on this rank's replica
-  {
-    LambArgs a = make_lamb_args(r, p, m, v);
-    const int nc = r->nchunks;
-    if (r->fused_lamb) {
-      FusedLamb f{};
-      f.items = r->d_items;
-      f.nitems = r->nitems;
-      f.work = r->d_qstate;
-      f.exited = r->d_qstate + 1;
-      f.done = r->d_qstate + 2;
-      f.ready = r->d_ready;
-      f.tchunks = r->d_tchunks;
-      f.trust = r->d_trust;
-      f.ntensors = c.num_tensors;
-      const int g = r->lamb_grid;
-      switch (c.wire) {
-        case SP_WIRE_FP32: k_lamb_fused<SP_WIRE_FP32><<<g, kLambThreads, 0, st>>>(a, f); break;
-        case SP_WIRE_FP16: k_lamb_fused<SP_WIRE_FP16><<<g, kLambThreads, 0, st>>>(a, f); break;
-        default: k_lamb_fused<SP_WIRE_Q8><<<g, kLambThreads, 0, st>>>(a, f); break;
-      }
-      SP_CUDA(cudaGetLastError());
+  if (r->fused_lamb) {
+    if (K > 1) {
+      SP_CUDA(cudaEventRecord(r->seg_ev[8], r->aux));
+      SP_CUDA(cudaStreamWaitEvent(st, r->seg_ev[8], 0));  // join
       if (ev) {
         SP_CUDA(cudaEventRecord(ev[5], st));
         SP_CUDA(cudaEventRecord(ev[6], st));
       }
+      const int rc = launch_lamb(r, la, r->p2_off, r->nchunks, true, st);
+      if (rc) return rc;
     } else {
-      switch (c.wire) {
-        case SP_WIRE_FP32: k_lamb_moments<SP_WIRE_FP32><<<nc, kLambThreads, 0, st>>>(a); break;
-        case SP_WIRE_FP16: k_lamb_moments<SP_WIRE_FP16><<<nc, kLambThreads, 0, st>>>(a); break;
-        default: k_lamb_moments<SP_WIRE_Q8><<<nc, kLambThreads, 0, st>>>(a); break;
+      const int rc = launch_lamb(r, la, 0, r->nitems, true, st);
+      if (rc) return rc;
+      if (ev) {
+        SP_CUDA(cudaEventRecord(ev[5], st));
+        SP_CUDA(cudaEventRecord(ev[6], st));
       }
-      SP_CUDA(cudaGetLastError());
-      if (ev) SP_CUDA(cudaEventRecord(ev[5], st));
-      k_lamb_trust<<<c.num_tensors, 256, 0, st>>>(r->d_partial, r->d_tchunks, r->d_hp,
-                                                  r->d_trust, r->d_step_scale);
-      SP_CUDA(cudaGetLastError());
-      if (ev) SP_CUDA(cudaEventRecord(ev[6], st));
-      switch (c.wire) {
-        case SP_WIRE_FP32: k_lamb_update<SP_WIRE_FP32><<<nc, kLambThreads, 0, st>>>(a); break;
-        case SP_WIRE_FP16: k_lamb_update<SP_WIRE_FP16><<<nc, kLambThreads, 0, st>>>(a); break;
-        default: k_lamb_update<SP_WIRE_Q8><<<nc, kLambThreads, 0, st>>>(a); break;
-      }
-      SP_CUDA(cudaGetLastError());
     }
+  } else {
+    const int nc = r->nchunks;
+    switch (c.wire) {
+      case SP_WIRE_FP32: k_lamb_moments<SP_WIRE_FP32><<<nc, kLambThreads, 0, st>>>(la); break;
+      case SP_WIRE_FP16: k_lamb_moments<SP_WIRE_FP16><<<nc, kLambThreads, 0, st>>>(la); break;
+      default: k_lamb_moments<SP_WIRE_Q8><<<nc, kLambThreads, 0, st>>>(la); break;
+    }
+    SP_CUDA(cudaGetLastError());
+    if (ev) SP_CUDA(cudaEventRecord(ev[5], st));
+    k_lamb_trust<<<c.num_tensors, 256, 0, st>>>(r->d_partial, r->d_tchunks, r->d_hp, r->d_trust,
+                                                r->d_step_scale);
+    SP_CUDA(cudaGetLastError());
+    if (ev) SP_CUDA(cudaEventRecord(ev[6], st));
+    switch (c.wire) {
+      case SP_WIRE_FP32: k_lamb_update<SP_WIRE_FP32><<<nc, kLambThreads, 0, st>>>(la); break;
+      case SP_WIRE_FP16: k_lamb_update<SP_WIRE_FP16><<<nc, kLambThreads, 0, st>>>(la); break;
+      default: k_lamb_update<SP_WIRE_Q8><<<nc, kLambThreads, 0, st>>>(la); break;
+    }
+    SP_CUDA(cudaGetLastError());
   }
   if (ev) SP_CUDA(cudaEventRecord(ev[7], st));
   return SP_OK;
@@ -599,21 +681,34 @@ int sp_round_create(const sp_round_cfg* cfg, sp_round** out) {
     return cleanup(fail(SP_ERR_CUDA, cudaGetErrorString(e)));
   r->base[cfg->rank] = r->shared;
 
-  std::vector<Chunk> chunks;
-  std::vector<int2> tch;
   const char* chunk_env = std::getenv("SP_LAMB_CHUNK");
-  const int64_t chunk = chunk_env ? std::max(64, std::atoi(chunk_env)) : kLambChunk;
-  build_chunks(r->tsizes, chunk, chunks, tch);
-  r->nchunks = (int)chunks.size();
-  if ((e = cudaMalloc(&r->d_chunks, chunks.size() * sizeof(Chunk))) != cudaSuccess ||
-      (e = cudaMalloc(&r->d_tchunks, tch.size() * sizeof(int2))) != cudaSuccess ||
-      (e = cudaMalloc(&r->d_partial, chunks.size() * sizeof(float2))) != cudaSuccess ||
-      (e = cudaMalloc(&r->d_trust, tch.size() * sizeof(float))) != cudaSuccess ||
-      (e = cudaMalloc(&r->d_step_scale, tch.size() * sizeof(float))) != cudaSuccess ||
+  r->lamb_chunk = chunk_env ? std::max(64, std::atoi(chunk_env)) : kLambChunk;
+  {
+    const char* seg_env = std::getenv("SP_SEGMENTS");
+    const char* unf = std::getenv("SP_LAMB_UNFUSED");
+    const bool unfused = unf && unf[0] == '1';
+    if (const char* g = std::getenv("SP_SEG_LAMB_GRID")) r->seg_lamb_grid = std::max(1, std::atoi(g));
+    if (const char* x = std::getenv("SP_XCHG_PER_SM")) r->xchg_per_sm = std::max(1, std::atoi(x));
+    r->segments = (cfg->world > 1 && !unfused && !r->fused_round)
+                      ? std::max(1, std::min(8, seg_env ? std::atoi(seg_env) : 1))
+                      : 1;
+  }
+  {
+    int64_t base = 0;
+    for (int64_t sz : r->tsizes) base += sz / r->lamb_chunk + 2;
+    r->nchunks_cap = (int)(base + (int64_t)cfg->world * (r->segments + 1) + 8);
+  }
+  const size_t ntens = r->tsizes.size();
+  if ((e = cudaMalloc(&r->d_chunks, (size_t)r->nchunks_cap * sizeof(Chunk))) != cudaSuccess ||
+      (e = cudaMalloc(&r->d_tchunks, ntens * sizeof(int2))) != cudaSuccess ||
+      (e = cudaMalloc(&r->d_partial, (size_t)r->nchunks_cap * sizeof(float2))) != cudaSuccess ||
+      (e = cudaMalloc(&r->d_trust, ntens * sizeof(float))) != cudaSuccess ||
+      (e = cudaMalloc(&r->d_step_scale, ntens * sizeof(float))) != cudaSuccess ||
       (e = cudaMalloc(&r->d_hp, 4 * sizeof(float))) != cudaSuccess ||
+      (e = cudaMalloc(&r->d_items, 2 * (size_t)r->nchunks_cap * sizeof(int))) != cudaSuccess ||
       (e = cudaMalloc(&r->epoch, sizeof(unsigned long long))) != cudaSuccess)
     return cleanup(fail(SP_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e)));
-  cudaMemcpy(r->d_chunks, chunks.data(), chunks.size() * sizeof(Chunk), cudaMemcpyHostToDevice);
+  if (int rc2 = build_lamb_tables(r, false)) return cleanup(rc2);
   {
     const char* env = std::getenv("SP_LAMB_UNFUSED");
     r->fused_lamb = !(env && env[0] == '1');
@@ -627,22 +722,14 @@ int sp_round_create(const sp_round_cfg* cfg, sp_round** out) {
       default: oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lamb_fused<SP_WIRE_Q8>, kLambThreads, 0); break;
     }
     if (oe != cudaSuccess || per_sm < 1) return cleanup(fail(SP_ERR_CUDA, "occupancy query failed for the fused LAMB kernel"));
-    // persistent grid: every CTA resident (the queue relies on it)
-    r->lamb_grid = std::max(1, std::min(per_sm * r->sm_count, r->nchunks));
-    const char* lag_env = std::getenv("SP_LAMB_LAG");
-    // Measured on B200 (profiles/r01/lamb_sweep.txt): with 8 resident CTAs
-    // per SM the in-flight window (~9.7M elements) already exceeds L2, so a
-    // short lag only adds trust waits; default: all pass-1 items first.
-    const int lag = lag_env ? std::atoi(lag_env) : (1 << 30);
-    std::vector<int> items = build_lamb_items(chunks, tch, lag);
-    r->nitems = (int)items.size();
-    if ((e = cudaMalloc(&r->d_items, items.size() * sizeof(int))) != cudaSuccess ||
-        (e = cudaMalloc(&r->d_qstate, (2 + tch.size()) * sizeof(int))) != cudaSuccess ||
-        (e = cudaMalloc(&r->d_ready, tch.size() * sizeof(unsigned int))) != cudaSuccess)
+    // persistent grid (the work queue is safe either way: items are taken in
+    // order and only wait on earlier ones)
+    r->lamb_grid = std::max(1, per_sm * r->sm_count);
+    if ((e = cudaMalloc(&r->d_qstate, (2 + ntens) * sizeof(int))) != cudaSuccess ||
+        (e = cudaMalloc(&r->d_ready, ntens * sizeof(unsigned int))) != cudaSuccess)
       return cleanup(fail(SP_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e)));
-    cudaMemcpy(r->d_items, items.data(), items.size() * sizeof(int), cudaMemcpyHostToDevice);
-    cudaMemset(r->d_qstate, 0, (2 + tch.size()) * sizeof(int));
-    cudaMemset(r->d_ready, 0, tch.size() * sizeof(unsigned int));
+    cudaMemset(r->d_qstate, 0, (2 + ntens) * sizeof(int));
+    cudaMemset(r->d_ready, 0, ntens * sizeof(unsigned int));
   }
   {
     int per_sm = 0;
@@ -654,7 +741,7 @@ int sp_round_create(const sp_round_cfg* cfg, sp_round** out) {
     }
     if (oe != cudaSuccess || per_sm < 1) return cleanup(fail(SP_ERR_CUDA, "occupancy query failed for the fused round kernel"));
     r->round_grid = per_sm * r->sm_count;
-    const size_t cap = 2 * (size_t)r->ncells + SP_MAX_RANKS + 2 * chunks.size() + 16;
+    const size_t cap = 2 * (size_t)r->ncells + SP_MAX_RANKS + 2 * (size_t)r->nchunks_cap + 16;
     if ((e = cudaMalloc(&r->d_ritems, cap * sizeof(unsigned))) != cudaSuccess ||
         (e = cudaMalloc(&r->d_rq, 2 * sizeof(int))) != cudaSuccess ||
         (e = cudaMalloc(&r->d_repoch, sizeof(unsigned))) != cudaSuccess ||
@@ -662,17 +749,19 @@ int sp_round_create(const sp_round_cfg* cfg, sp_round** out) {
       return cleanup(fail(SP_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e)));
     cudaMemset(r->d_rq, 0, 2 * sizeof(int));
     cudaMemset(r->d_repoch, 0, sizeof(unsigned));
-    r->h_chunks = chunks;
   }
-  cudaMemcpy(r->d_tchunks, tch.data(), tch.size() * sizeof(int2), cudaMemcpyHostToDevice);
   cudaMemset(r->epoch, 0, sizeof(unsigned long long));
-  cudaMemset(r->d_trust, 0, tch.size() * sizeof(float));
+  cudaMemset(r->d_trust, 0, ntens * sizeof(float));
   if ((e = cudaHostAlloc(&r->h_err, sizeof(int), cudaHostAllocMapped)) != cudaSuccess)
     return cleanup(fail(SP_ERR_CUDA, cudaGetErrorString(e)));
   *r->h_err = 0;
   cudaHostGetDevicePointer(reinterpret_cast<void**>(&r->d_err), r->h_err, 0);
-  if ((e = cudaStreamCreateWithFlags(&r->own, cudaStreamNonBlocking)) != cudaSuccess)
+  if ((e = cudaStreamCreateWithFlags(&r->own, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaStreamCreateWithFlags(&r->aux, cudaStreamNonBlocking)) != cudaSuccess)
     return cleanup(fail(SP_ERR_CUDA, cudaGetErrorString(e)));
+  for (auto& ev : r->seg_ev)
+    if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess)
+      return cleanup(fail(SP_ERR_CUDA, cudaGetErrorString(e)));
   for (auto& ev : r->ev)
     if ((e = cudaEventCreate(&ev)) != cudaSuccess) return cleanup(fail(SP_ERR_CUDA, cudaGetErrorString(e)));
   if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cleanup(fail(SP_ERR_CUDA, cudaGetErrorString(e)));
@@ -707,6 +796,9 @@ int sp_round_destroy(sp_round* r) {
   for (auto& ev : r->ev)
     if (ev) cudaEventDestroy(ev);
   if (r->own) cudaStreamDestroy(r->own);
+  if (r->aux) cudaStreamDestroy(r->aux);
+  for (auto& ev : r->seg_ev)
+    if (ev) cudaEventDestroy(ev);
   delete r;
   return SP_OK;
 }
@@ -760,8 +852,10 @@ int sp_round_set_assignment(sp_round* r, const int64_t* offsets, const double* w
   if (!(wsum > 0.0)) return fail(SP_ERR_ARG, "sum of weights must be positive");
   r->offsets.assign(offsets, offsets + G + 1);
   r->weights.assign(weights, weights + G);
+  SP_CUDA(cudaSetDevice(r->cfg.device));
+  SP_CUDA(cudaDeviceSynchronize());  // the previous round may still read the tables
+  if (int rc = build_lamb_tables(r, true)) return rc;
   if (r->fused_round) {
-    SP_CUDA(cudaDeviceSynchronize());  // the previous round may still read the work list
     const int rc = build_round_items(r);
     if (rc) return rc;
   }
