@@ -124,6 +124,22 @@ def build_tests(force: bool = False) -> str | None:
     return out
 
 
+def build_gpu_tests(force: bool = False) -> str | None:
+    """C++ GPU check of the orchestrator (run by tests/test_cpp_gpu.py on a B200)."""
+    src = os.path.join(ROOT, "tests", "cpp_gpu", "round_check.cpp")
+    if not os.path.exists(src):
+        return None
+    out = os.path.join(ROOT, "tests", "cpp_gpu", "_build", "round_check")
+    deps = [src] + HOST_DEPS + ORACLE_DEPS + [os.path.join(LIB, "libswarmplan.so")]
+    if force or _stale(out, deps):
+        os.makedirs(os.path.dirname(out), exist_ok=True)
+        oracle_dir = os.path.join(ROOT, "oracle", "_build")
+        _run(["g++", *_host_flags(), "-o", out, src, f"-L{LIB}", "-lswarmplan", "-lsp_round",
+              f"-L{oracle_dir}", "-lsp_oracle", f"-L{os.path.join(CUDA_HOME, 'lib64')}", "-lcudart",
+              f"-Wl,-rpath,{LIB}:{oracle_dir}:{os.path.join(CUDA_HOME, 'lib64')}"])
+    return out
+
+
 def build_all(force: bool = False) -> None:
     if shutil.which(NVCC) is None and not os.path.exists(NVCC):
         raise RuntimeError(f"nvcc not found at {NVCC}")
@@ -132,6 +148,7 @@ def build_all(force: bool = False) -> None:
     build_host(force)
     build_bindings(force)
     build_tests(force)
+    build_gpu_tests(force)
 
 
 if __name__ == "__main__":

@@ -1,0 +1,63 @@
+"""Multi-rank host plumbing of the round (one process per GPU).
+
+torch.distributed is used only to move a few bytes between processes: the
+CUDA IPC handle blobs of every rank (sp_round_export / sp_round_connect) and
+the sanity check that every rank planned the same assignment. The data path
+itself never touches torch.distributed (NVLink stores from the kernels).
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+
+
+def exchange_handles(blob: bytes, group=None) -> bytes:
+    """All-gather one opaque blob per rank; returns the concatenation in rank
+    order (what sp_round_connect expects)."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    out: list = [None] * world
+    dist.all_gather_object(out, bytes(blob), group=group)
+    sizes = {len(b) for b in out}
+    if len(sizes) != 1:
+        raise RuntimeError(f"ranks exported handle blobs of different sizes: {sorted(sizes)}")
+    return b"".join(out)
+
+
+def plan_round(spec_json: str, n: int, align: int, sample_counts=None) -> dict:
+    """LP plan shared by every rank: fractions from solve_strategy, part
+    offsets, weights (sample counts; default samples_per_sec * duty cycle,
+    the accumulation the LP assumed, /root/reference/proj/src/netsim.cpp:158)."""
+    from . import _swarmplan
+
+    plan = _swarmplan.plan_parts(spec_json, n, align)
+    if sample_counts is None:
+        spec = json.loads(spec_json)
+        sample_counts = [p.get("samples_per_sec", 0.0) * c
+                         for p, c in zip(spec["peers"], plan["duty_cycle"])]
+    plan["weights"] = [float(w) for w in sample_counts]
+    return plan
+
+
+def rank_range(offsets, rank: int, peers_per_rank: int) -> tuple[int, int]:
+    """Element range rank `rank` owns: the union of its peers' parts."""
+    return int(offsets[rank * peers_per_rank]), int(offsets[(rank + 1) * peers_per_rank])
+
+
+def plan_digest(offsets, weights) -> str:
+    h = hashlib.sha256()
+    h.update(json.dumps([list(map(int, offsets)), list(map(float, weights))]).encode())
+    return h.hexdigest()
+
+
+def check_same_plan(offsets, weights, group=None) -> None:
+    """Every rank must run the round with the same offsets and weights (a
+    mismatch would make owners disagree about who reduces what)."""
+    import torch.distributed as dist
+
+    mine = plan_digest(offsets, weights)
+    out: list = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, mine, group=group)
+    if any(d != mine for d in out):
+        raise RuntimeError("ranks disagree on the round assignment (offsets/weights)")

@@ -77,18 +77,19 @@ class AveragingRound:
         self.weights: list[float] | None = None
         if self.world > 1:
             self._connect(process_group)
+        self._group = process_group
 
     # -- multi-rank wiring ------------------------------------------------
     def _connect(self, group) -> None:
         import torch
         import torch.distributed as dist
 
+        from .dist import exchange_handles
+
         nb = self._lib.sp_round_handle_bytes()
         mine = (ctypes.c_char * nb)()
         nat.check(self._lib.sp_round_export(self._h, mine))
-        gathered: list = [None] * self.world
-        dist.all_gather_object(gathered, bytes(mine), group=group)
-        blob = b"".join(gathered)
+        blob = exchange_handles(bytes(mine), group)
         buf = (ctypes.c_char * len(blob)).from_buffer_copy(blob)
         nat.check(self._lib.sp_round_connect(self._h, buf))
         dist.barrier(group=group)
@@ -106,6 +107,10 @@ class AveragingRound:
         w = (ctypes.c_double * self.G)(*[float(x) for x in weights])
         nat.check(self._lib.sp_round_set_assignment(self._h, o, w))
         self.offsets, self.weights = list(map(int, offsets)), list(map(float, weights))
+        if self.world > 1:
+            from .dist import check_same_plan
+
+            check_same_plan(self.offsets, self.weights, getattr(self, "_group", None))
 
     def assign(self, fractions: Sequence[float], weights: Sequence[float]) -> list[int]:
         offs = part_offsets(self.n, fractions, self.align)
