@@ -169,8 +169,9 @@ void sp_oracle_reduce(int wire, const void* const* wires, const float* const* sc
   if (wire != SPO_Q8) {
 #pragma omp parallel for schedule(static)
     for (int64_t i = lo; i < hi; ++i) {
-      float acc = 0.0f;
-      for (int k = 0; k < np; ++k)
+      /* first contributor by product (no +0 seed), then fmaf in peer order */
+      float acc = wn[0] * dequant(wire, wires[idx[0]], NULL, block, i);
+      for (int k = 1; k < np; ++k)
         acc = fmaf(wn[k], dequant(wire, wires[idx[k]], NULL, block, i), acc);
       if (wire == SPO_FP32)
         ((float*)out_wire)[i] = acc;
@@ -188,8 +189,8 @@ void sp_oracle_reduce(int wire, const void* const* wires, const float* const* sc
       const int64_t s = b * block;
       const int64_t e = (s + block) < hi ? (s + block) : hi;
       for (int64_t i = s; i < e; ++i) {
-        float acc = 0.0f;
-        for (int k = 0; k < np; ++k) {
+        float acc = wn[0] * ((float)((const int8_t*)wires[idx[0]])[i] * scales[idx[0]][b]);
+        for (int k = 1; k < np; ++k) {
           const int g = idx[k];
           const float x = (float)((const int8_t*)wires[g])[i] * scales[g][b];
           acc = fmaf(wn[k], x, acc);

@@ -66,8 +66,8 @@ void sp_oracle_weighted_average_f64(const double* const* values,
                                     double* out);
 
 /* The executor's fp32 reduction of elements [lo, hi): wn_g = (float)(w_g /
- * sum w) (fp64 division), acc = fmaf(wn_g, x_g, acc) over peers 0..G-1 with
- * w_g != 0, x_g the dequantized wire value (q8: (float)q * scale); result
+ * sum w) (fp64 division); over the peers with w_g != 0 in peer order,
+ * acc = wn_first * x_first, then acc = fmaf(wn_g, x_g, acc), x_g the dequantized wire value (q8: (float)q * scale); result
  * re-encoded in the wire format into out_wire (and out_scales for q8, whose
  * blocks are aligned: lo % block == 0). wire[g]/scales[g] are peer g's full
  * buffers. */

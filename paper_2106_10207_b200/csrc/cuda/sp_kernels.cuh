@@ -20,7 +20,10 @@
 namespace sp {
 
 constexpr int kLambChunk = 8192;  // elements per LAMB work item (one CTA)
-constexpr int kLambThreads = 256;
+#ifndef SP_LAMB_THREADS
+#define SP_LAMB_THREADS 256
+#endif
+constexpr int kLambThreads = SP_LAMB_THREADS;
 constexpr int kPad = 16384;       // wire/avg buffers padded to this multiple
 
 struct BarrierArgs {
@@ -359,8 +362,17 @@ __global__ void __launch_bounds__(256) k_reduce_fp32(ReduceArgs a) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec;
        v += (int64_t)gridDim.x * blockDim.x) {
     const int64_t off = (a.lo + v * 4) * 4;  // bytes
-    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-    int g = 0;
+    // the sum starts from the first contributor's product (no +0 seed), so a
+    // single contributor with weight 1 reproduces its values bit for bit
+    float acc[4];
+    {
+      const int4 r0 = ld_nc_v4(static_cast<const char*>(a.src[0]) + off);
+      acc[0] = __fmul_rn(a.w[0], __int_as_float(r0.x));
+      acc[1] = __fmul_rn(a.w[0], __int_as_float(r0.y));
+      acc[2] = __fmul_rn(a.w[0], __int_as_float(r0.z));
+      acc[3] = __fmul_rn(a.w[0], __int_as_float(r0.w));
+    }
+    int g = 1;
     for (; g + 4 <= a.npeers; g += 4) {
       int4 r[4];
 #pragma unroll
@@ -398,15 +410,24 @@ __device__ __forceinline__ void fma_half8(float* acc, float w, int4 r) {
   }
 }
 
+__device__ __forceinline__ void mul_half8(float* acc, float w, int4 r) {
+  const uint32_t u[4] = {(uint32_t)r.x, (uint32_t)r.y, (uint32_t)r.z, (uint32_t)r.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    float2 f = unpack_half2(u[k]);
+    acc[2 * k] = __fmul_rn(w, f.x);
+    acc[2 * k + 1] = __fmul_rn(w, f.y);
+  }
+}
+
 __global__ void __launch_bounds__(256) k_reduce_fp16(ReduceArgs a) {
   const int64_t nvec = (a.hi - a.lo + 7) / 8;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec;
        v += (int64_t)gridDim.x * blockDim.x) {
     const int64_t off = (a.lo + v * 8) * 2;  // bytes
     float acc[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
-    int g = 0;
+    mul_half8(acc, a.w[0], ld_nc_v4(static_cast<const char*>(a.src[0]) + off));
+    int g = 1;
     for (; g + 4 <= a.npeers; g += 4) {
       int4 r[4];
 #pragma unroll
@@ -437,6 +458,18 @@ __device__ __forceinline__ void fma_q8x16(float* acc, float w, float scale, int4
   }
 }
 
+__device__ __forceinline__ void mul_q8x16(float* acc, float w, float scale, int4 r) {
+  const uint32_t u[4] = {(uint32_t)r.x, (uint32_t)r.y, (uint32_t)r.z, (uint32_t)r.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int q = (int)(int8_t)((u[k] >> (8 * j)) & 0xff);
+      acc[4 * k + j] = __fmul_rn(w, __fmul_rn((float)q, scale));
+    }
+  }
+}
+
 // One CTA (qblock/16 threads) per q8 block of [lo, hi); lo is block aligned.
 __global__ void k_reduce_q8(ReduceArgs a) {
   __shared__ float red[32];
@@ -453,9 +486,8 @@ __global__ void k_reduce_q8(ReduceArgs a) {
     __syncthreads();
     const int64_t e0 = b * a.qblock + threadIdx.x * 16;
     float acc[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) acc[j] = 0.0f;
-    int g = 0;
+    mul_q8x16(acc, a.w[0], sc[0], ld_nc_v4(static_cast<const char*>(a.src[0]) + e0));
+    int g = 1;
     for (; g + 4 <= a.npeers; g += 4) {
       int4 r[4];
 #pragma unroll

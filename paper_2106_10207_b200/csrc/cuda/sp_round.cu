@@ -209,13 +209,36 @@ int build_lamb_tables(sp_round* r, bool with_cuts) {
   }
   std::vector<int> items;
   r->p1_off.assign((size_t)K + 1, 0);
-  for (int q = 0; q < K; ++q) {
-    r->p1_off[(size_t)q] = (int)items.size();
-    items.insert(items.end(), p1[(size_t)q].begin(), p1[(size_t)q].end());
+  const char* lag_env = std::getenv("SP_LAMB_LAG");
+  if (K == 1 && lag_env) {
+    // single launch, pass 2 of tensor t queued `lag` items after its last
+    // pass-1 chunk (tuning experiment for L2 reuse between the passes)
+    const size_t lag = (size_t)std::max(0, std::atoi(lag_env));
+    std::vector<std::pair<int, size_t>> pend;
+    size_t head = 0;
+    auto flush = [&](bool all) {
+      while (head < pend.size() && (all || pend[head].second + lag <= items.size())) {
+        const int2 rg = tch[(size_t)pend[head].first];
+        for (int c = rg.x; c < rg.y; ++c) items.push_back(~c);
+        ++head;
+      }
+    };
+    for (size_t c = 0; c < chunks.size(); ++c) {
+      items.push_back((int)c);
+      if ((int)c == tch[(size_t)chunks[c].tensor].y - 1) pend.push_back({chunks[c].tensor, items.size()});
+      flush(false);
+    }
+    flush(true);
+    r->p1_off[1] = r->p2_off = (int)items.size();
+  } else {
+    for (int q = 0; q < K; ++q) {
+      r->p1_off[(size_t)q] = (int)items.size();
+      items.insert(items.end(), p1[(size_t)q].begin(), p1[(size_t)q].end());
+    }
+    r->p1_off[(size_t)K] = (int)items.size();
+    r->p2_off = (int)items.size();
+    for (size_t c = 0; c < chunks.size(); ++c) items.push_back(~(int)c);
   }
-  r->p1_off[(size_t)K] = (int)items.size();
-  r->p2_off = (int)items.size();
-  for (size_t c = 0; c < chunks.size(); ++c) items.push_back(~(int)c);
   r->nchunks = (int)chunks.size();
   r->nitems = (int)items.size();
   r->h_chunks = chunks;
@@ -302,10 +325,32 @@ int build_round_items(sp_round* r) {
   return SP_OK;
 }
 
+// With one rank and a single contributing peer the fp32/fp16 average is the
+// identity on that peer's wire values (acc = fmaf(1.0f, x, 0) = x, and x is
+// exactly representable in the wire format): the averaged vector IS the
+// peer's inbox slot and the reduce kernel is skipped. q8 requantization is
+// not the identity, so it always reduces.
+const char* identity_avg(const sp_round* r) {
+  const sp_round_cfg& c = r->cfg;
+  if (c.world != 1 || c.wire == SP_WIRE_Q8 || !r->assigned || r->fused_round) return nullptr;
+  int np = 0, who = -1;
+  for (int g = 0; g < r->G; ++g)
+    if (r->weights[g] != 0.0) {
+      ++np;
+      who = g;
+    }
+  return np == 1 ? r->wire(c.rank, who) : nullptr;
+}
+
+const char* avg_buffer(const sp_round* r) {
+  const char* id = identity_avg(r);
+  return id ? id : r->avg(r->cfg.rank);
+}
+
 LambArgs make_lamb_args(sp_round* r, float* p, float* m, float* v) {
   const sp_round_cfg& c = r->cfg;
   LambArgs a{};
-  a.avg = r->avg(c.rank);
+  a.avg = avg_buffer(r);
   a.avg_scale = c.wire == SP_WIRE_Q8 ? reinterpret_cast<const float*>(r->avg(c.rank) + r->npad)
                                      : nullptr;
   a.p = p;
@@ -519,7 +564,7 @@ int enqueue_round(sp_round* r, const float* const* grads, float* p, float* m, fl
       ra.hi = seg_cut(r, c.rank, s + 1);
       ra.npad = r->npad;
       ra.qblock = c.q8_block;
-      if (ra.hi > ra.lo) {
+      if (ra.hi > ra.lo && !identity_avg(r)) {
         if (c.wire == SP_WIRE_Q8) {
           const int64_t nb = (ra.hi + c.q8_block - 1) / c.q8_block - ra.lo / c.q8_block;
           const int grid = (int)std::min<int64_t>(nb, (int64_t)r->sm_count * 16);
@@ -725,6 +770,7 @@ int sp_round_create(const sp_round_cfg* cfg, sp_round** out) {
     // persistent grid (the work queue is safe either way: items are taken in
     // order and only wait on earlier ones)
     r->lamb_grid = std::max(1, per_sm * r->sm_count);
+    if (const char* lg = std::getenv("SP_LAMB_GRID")) r->lamb_grid = std::max(1, std::min(r->lamb_grid, std::atoi(lg)));
     if ((e = cudaMalloc(&r->d_qstate, (2 + ntens) * sizeof(int))) != cudaSuccess ||
         (e = cudaMalloc(&r->d_ready, ntens * sizeof(unsigned int))) != cudaSuccess)
       return cleanup(fail(SP_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e)));
@@ -927,7 +973,7 @@ void* sp_round_wire_ptr(sp_round* r, int local_peer) {
   return r->wire(r->cfg.rank, r->cfg.rank * r->L + local_peer);
 }
 
-void* sp_round_avg_ptr(sp_round* r) { return r ? r->avg(r->cfg.rank) : nullptr; }
+void* sp_round_avg_ptr(sp_round* r) { return r ? const_cast<char*>(avg_buffer(r)) : nullptr; }
 
 const float* sp_round_trust_ptr(sp_round* r) { return r ? r->d_trust : nullptr; }
 
@@ -948,7 +994,7 @@ int sp_round_read(sp_round* r, int which, int local_peer, size_t offset_bytes, v
     src = r->wire(r->cfg.rank, r->cfg.rank * r->L + local_peer);
     cap = r->buf_bytes;
   } else if (which == SP_BUF_AVG) {
-    src = r->avg(r->cfg.rank);
+    src = avg_buffer(r);
     cap = r->buf_bytes;
   } else if (which == SP_BUF_TRUST) {
     src = reinterpret_cast<const char*>(r->d_trust);

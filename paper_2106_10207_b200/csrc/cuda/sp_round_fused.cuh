@@ -190,9 +190,18 @@ __device__ __forceinline__ void fused_reduce(const RoundFused& f, int64_t s, int
     for (int64_t v = v0 + tid; v < v1; v += blockDim.x) {
       const size_t off = (size_t)v * 16;
       float acc[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
-      int g = 0;
+      {
+        const int4 r0 = ld_cg_v4(base + (size_t)f.peer[0] * f.slot_bytes + off);
+        if constexpr (W == SP_WIRE_FP16) {
+          mul_half8(acc, f.w[0], r0);
+        } else {
+          acc[0] = __fmul_rn(f.w[0], __int_as_float(r0.x));
+          acc[1] = __fmul_rn(f.w[0], __int_as_float(r0.y));
+          acc[2] = __fmul_rn(f.w[0], __int_as_float(r0.z));
+          acc[3] = __fmul_rn(f.w[0], __int_as_float(r0.w));
+        }
+      }
+      int g = 1;
       for (; g + 4 <= f.npeers; g += 4) {
         int4 r[4];
 #pragma unroll
@@ -241,9 +250,8 @@ __device__ __forceinline__ void fused_reduce(const RoundFused& f, int64_t s, int
       __syncthreads();
       const size_t e0 = (size_t)b * 4096 + tid * 16;
       float acc[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) acc[j] = 0.0f;
-      int g = 0;
+      mul_q8x16(acc, f.w[0], sc[0], ld_cg_v4(base + (size_t)f.peer[0] * f.slot_bytes + e0));
+      int g = 1;
       for (; g + 4 <= f.npeers; g += 4) {
         int4 r[4];
 #pragma unroll
