@@ -527,16 +527,25 @@ int enqueue_round(sp_round* r, const float* const* grads, float* p, float* m, fl
     a.qblock = c.q8_block;
     const int64_t units = a.pref[a.nr];
     if (any && units > 0) {
-      if (c.wire == SP_WIRE_Q8) {
-        dim3 grid((unsigned)std::min<int64_t>(units, (int64_t)r->sm_count * 16), r->L);
-        k_pack_q8<<<grid, c.q8_block / 16, 0, st>>>(a);
-      } else if (c.wire == SP_WIRE_FP16) {
-        dim3 grid(grid_for(units, 256, r->sm_count, r->xchg_per_sm), r->L);
-        k_pack_fp16<<<grid, 256, 0, st>>>(a);
-      } else {
-        dim3 grid(grid_for(units, 256, r->sm_count, r->xchg_per_sm), r->L);
-        k_pack_fp32<<<grid, 256, 0, st>>>(a);
+      const int threads = c.wire == SP_WIRE_Q8 ? c.q8_block / 16 : 256;
+      const int64_t per_cta = c.wire == SP_WIRE_Q8 ? 1 : 256;  // units per CTA per pass
+      const int want = c.wire == SP_WIRE_Q8
+                           ? (int)std::min<int64_t>(units, (int64_t)r->sm_count * 16)
+                           : grid_for(units, 256, r->sm_count, r->xchg_per_sm);
+      // split the CTAs over the ranges in proportion to their lengths (>= 1 each)
+      int total = 0;
+      a.cta0[0] = 0;
+      for (int j = 0; j < a.nr; ++j) {
+        const int64_t len = a.pref[j + 1] - a.pref[j];
+        int nct = (int)std::max<int64_t>(1, (int64_t)((double)want * len / units + 0.5));
+        nct = (int)std::min<int64_t>(nct, (len + per_cta - 1) / per_cta);
+        total += std::max(1, nct);
+        a.cta0[j + 1] = total;
       }
+      dim3 grid((unsigned)total, r->L);
+      if (c.wire == SP_WIRE_Q8) k_pack_q8<<<grid, threads, 0, st>>>(a);
+      else if (c.wire == SP_WIRE_FP16) k_pack_fp16<<<grid, threads, 0, st>>>(a);
+      else k_pack_fp32<<<grid, threads, 0, st>>>(a);
       SP_CUDA(cudaGetLastError());
     }
     if (ev && s == 0) SP_CUDA(cudaEventRecord(ev[1], st));
