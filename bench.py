@@ -56,6 +56,28 @@ def wire_bytes(wire: str, block: int) -> float:
     return {"fp32": 4.0, "fp16": 2.0, "q8": 1.0 + 4.0 / block}[wire]
 
 
+def ncu_traffic(kernel_substr: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the kernel in the
+    committed `ncu --set full` capture (profiles/*/ncu_full_*.csv), bytes per
+    launch, or None when no capture of that kernel is committed."""
+    import csv
+    import glob
+
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_full_*.csv")), reverse=True):
+        try:
+            rows = list(csv.reader(open(path)))
+            h = rows[0]
+            ki, ri, wi = h.index("Kernel Name"), h.index("dram__bytes_read.sum"), h.index("dram__bytes_write.sum")
+            unit = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            ur, uw = unit.get(rows[1][ri], 1.0), unit.get(rows[1][wi], 1.0)
+            for r in rows[2:]:
+                if kernel_substr in r[ki]:
+                    return float(r[ri]) * ur + float(r[wi]) * uw
+        except Exception:
+            continue
+    return None
+
+
 def peak_hbm() -> tuple[float, str]:
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -308,6 +330,9 @@ def main():
             "update_ms": 0.0 if fused else n * 16.0,
         }
         dom = max(("pack_ms", "reduce_ms", "moments_ms", "update_ms"), key=lambda k: ph[k])
+        kname = {"pack_ms": "k_pack", "reduce_ms": "k_reduce",
+                 "moments_ms": "k_lamb_fused" if fused else "k_lamb_moments",
+                 "update_ms": "k_lamb_update"}[dom]
         achieved = alg[dom] / (ph[dom] * 1e-3) / 1e9
         bound, pk, unit = "hbm", peak, "GB/s"
         if dom in ("reduce_ms", "pack_ms") and world > 1:
@@ -354,7 +379,8 @@ def main():
             "kernel_ms": {k: round(v_, 5) for k, v_ in ph.items()},
             "roofline": {"bound": bound, "kernel": dom.replace("_ms", ""),
                          "achieved": round(achieved, 1), "peak": pk, "unit": unit,
-                         "frac": round(achieved / pk, 4), "traffic": None,
+                         "frac": round(achieved / pk, 4), "traffic": ncu_traffic(kname),
+                         "algorithmic_bytes": alg[dom],
                          "peak_kind": peak_kind if bound == "hbm" else "measured all-to-all push (profiles/r01/p2p_bw.txt)"},
             "round_roofline": {"t_roof_us": round(t_roof * 1e6, 2),
                                "frac": round(t_roof * 1e3 / ms_step, 4),

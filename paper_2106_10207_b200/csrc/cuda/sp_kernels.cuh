@@ -871,8 +871,11 @@ __device__ __forceinline__ void st_release_gpu(unsigned int* p, unsigned int v) 
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+#ifndef SP_LAMB_MIN_CTAS
+#define SP_LAMB_MIN_CTAS 1
+#endif
 template <int W>
-__global__ void __launch_bounds__(kLambThreads) k_lamb_fused(LambArgs a, FusedLamb f) {
+__global__ void __launch_bounds__(kLambThreads, SP_LAMB_MIN_CTAS) k_lamb_fused(LambArgs a, FusedLamb f) {
   __shared__ int s_item;
   __shared__ int s_last;
   __shared__ float s_scale;
