@@ -162,6 +162,29 @@ def cpu_round_time(tsizes, wire, block, G, weights, reps: int, threads: int = 0)
     return statistics.median(ts), (threads or O.max_threads())
 
 
+def lp_solve_times() -> dict:
+    """Host LP (strategy solve) time, median of 5, for the fleets the budget is
+    quoted on (< 50 ms at n = 16: PAPER.md:140)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from golden.fleets import homogeneous, spec_json
+
+    from paper_2106_10207_b200 import _swarmplan
+
+    out = {}
+    for name, sj in (("n4_homogeneous", json.dumps(homogeneous(4, 1.0, 1000.0, 4.0, 17847474))),
+                     ("n8_homogeneous8", spec_json("homogeneous8")),
+                     ("n8_het8c", spec_json("het8c")),
+                     ("n16_static16", spec_json("static16")),
+                     ("n16_table1_b", spec_json("table1_b"))):
+        ts = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            _swarmplan.solve_strategy(sj)
+            ts.append(time.perf_counter() - t0)
+        out[name] = round(statistics.median(ts) * 1e3, 2)
+    return out
+
+
 # ------------------------------------------------------------------ main
 def main():
     ap = argparse.ArgumentParser()
@@ -344,6 +367,11 @@ def main():
         hbm_round = ((4 + b) * L if wire != "fp32" else 0.0) + G * f_r * b + f_r * b + 24 + b
         nvl_round = ((1 - f_r) * b + (G - 1) * f_r * b) if world > 1 else 0.0
         t_roof = hbm_round * n / (peak * 1e9) + nvl_round * n / (NVLINK_GBS * 1e9)
+        lp_times = None
+        try:
+            lp_times = lp_solve_times()
+        except Exception as e:
+            log("lp timing failed:", e)
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             try:
@@ -391,6 +419,7 @@ def main():
                     "h2d_bytes_per_step": 4 * n * L, "d2h_bytes_per_step": 4 * len(tsizes)},
             "clocks": clk,
             "cpu_baseline": cpu,
+            "lp_solve_ms": lp_times,
         }
         print(json.dumps(out), flush=True)
     rnd.close()

@@ -85,7 +85,8 @@ def build_oracle(force: bool = False) -> str:
 
 
 def _host_flags() -> list[str]:
-    return ["-O2", "-std=c++20", "-fPIC", "-Wall", "-Wextra", f"-I{INC}",
+    # x86-64-v3 (AVX2/FMA): every B200 host CPU has it; 1.3x on the LP
+    return ["-O3", "-march=x86-64-v3", "-std=c++20", "-fPIC", "-Wall", "-Wextra", f"-I{INC}",
             f"-I{_json_include()}", f"-I{os.path.join(CUDA_HOME, 'include')}"]
 
 

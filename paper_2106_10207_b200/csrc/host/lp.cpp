@@ -5,11 +5,12 @@
 // strategy programs (<= ~1.3k rows at 24 peers):
 //
 //  * Basis representation. Slack columns are unit vectors, so a basis with
-//    S basic slacks reduces to a dense k x k "kernel" M (k = m - S): the rows
-//    not covered by a basic slack times the basic structural columns. M is
-//    LU-factored with partial pivoting; the covered rows are recovered by one
-//    sparse sweep. Between refactorizations, basis changes are applied as
-//    product-form eta columns. ftran/btran cost O(k^2 + nnz + etas*m).
+//    S basic slacks reduces to a k x k "kernel" M (k = m - S): the rows not
+//    covered by a basic slack times the basic structural columns. M gets a
+//    sparse Markowitz LU with threshold pivoting (strategy kernels have ~4
+//    nonzeros per column and little fill); the covered rows are recovered by
+//    one sparse sweep. Between refactorizations, basis changes are applied
+//    as product-form eta columns. ftran/btran cost O(nnz(L+U) + etas*m).
 //  * Pricing: devex reference weights (symmetric fleets make whole column
 //    families tie; largest-coefficient pricing stalls on them), lowest index
 //    on ties, Bland's rule after a run of degenerate pivots.
@@ -31,6 +32,7 @@
 #include <cmath>
 #include <cstdint>
 #include <limits>
+#include <cstdint>
 #include <sstream>
 
 #include "swarmplan/log.hpp"
@@ -145,9 +147,13 @@ struct SimplexSolver::Impl {
   // kernel factorization
   int k = 0;
   std::vector<int> kpos, kvar, krow, row_k, slack_pos;  // snapshot of B0 at factor time
-  std::vector<double> lu;   // k x k row-major, L unit-lower + U
-  std::vector<double> lut;  // its transpose (column access for ftran)
-  std::vector<int> perm;   // factored row i = kernel row perm[i]
+  // sparse LU of the kernel: step t pivots on (kernel row prow[t], kernel
+  // column pcol[t]); L column t holds the multipliers of the rows it
+  // eliminated, U row t the remaining entries of the pivot row
+  std::vector<int> prow, pcol;
+  std::vector<double> piv;
+  std::vector<int> lbeg, lidx, ubeg, uidx;
+  std::vector<double> lval, uval;
   std::vector<Eta> etas;
   std::vector<double> tk1, tk2;
 
@@ -279,50 +285,166 @@ struct SimplexSolver::Impl {
     if (static_cast<int>(krow.size()) != k) return false;
     kvar.resize(k);
     for (int c = 0; c < k; ++c) kvar[c] = basis[kpos[c]];
-    lu.assign(static_cast<std::size_t>(k) * k, 0.0);
+    return sparse_lu();
+  }
+
+  // Markowitz-style sparse LU with threshold pivoting: at each step the
+  // active column with the fewest entries, and in it the row with the fewest
+  // entries among those within 0.1 of the column's largest magnitude.
+  // Strategy-LP kernels have ~4 nonzeros per column and little fill.
+  bool sparse_lu() {
+    std::vector<std::vector<std::pair<int, double>>> col(k);  // active entries
+    std::vector<std::vector<int>> row(k);                     // active pattern
     for (int c = 0; c < k; ++c)
       for (const auto& [r, a] : v[kvar[c]].col)
-        if (row_k[r] >= 0) lu[static_cast<std::size_t>(row_k[r]) * k + c] = a;
-    perm.resize(k);
-    for (int i = 0; i < k; ++i) perm[i] = i;
-    for (int c = 0; c < k; ++c) {
-      int pr = c;
-      double best = std::fabs(lu[static_cast<std::size_t>(c) * k + c]);
-      for (int r = c + 1; r < k; ++r) {
-        const double a = std::fabs(lu[static_cast<std::size_t>(r) * k + c]);
-        if (a > best) {
-          best = a;
-          pr = r;
+        if (row_k[r] >= 0 && a != 0.0) {
+          col[c].emplace_back(row_k[r], a);
+          row[row_k[r]].push_back(c);
         }
-      }
-      if (best < kSingular) {
-        fail_col = c;
-        fail_row = perm[c];  // an uneliminated kernel row
+    std::vector<char> rdone(k, 0), cdone(k, 0);
+    prow.assign(k, -1);
+    pcol.assign(k, -1);
+    piv.assign(k, 0.0);
+    lbeg.assign(1, 0);
+    ubeg.assign(1, 0);
+    lidx.clear();
+    lval.clear();
+    uidx.clear();
+    uval.clear();
+    std::vector<double> urowv;
+    std::vector<int> urowc;
+    for (int t = 0; t < k; ++t) {
+      int q = -1;
+      std::size_t best = SIZE_MAX;
+      for (int c = 0; c < k; ++c)
+        if (!cdone[c] && col[c].size() < best) {
+          best = col[c].size();
+          q = c;
+          if (best <= 1) break;
+        }
+      double cmax = 0.0;
+      for (const auto& e : col[q]) cmax = std::max(cmax, std::fabs(e.second));
+      if (cmax < kSingular) {
+        fail_col = q;
+        for (int r = 0; r < k; ++r)
+          if (!rdone[r]) {
+            fail_row = r;
+            break;
+          }
         return false;
       }
-      if (pr != c) {
-        std::swap_ranges(lu.begin() + static_cast<std::ptrdiff_t>(pr) * k,
-                         lu.begin() + static_cast<std::ptrdiff_t>(pr + 1) * k,
-                         lu.begin() + static_cast<std::ptrdiff_t>(c) * k);
-        std::swap(perm[pr], perm[c]);
+      int p = -1;
+      double pv = 0.0;
+      std::size_t rbest = SIZE_MAX;
+      for (const auto& [r, a] : col[q]) {
+        if (std::fabs(a) < 0.1 * cmax) continue;
+        if (row[r].size() < rbest || (row[r].size() == rbest && std::fabs(a) > std::fabs(pv))) {
+          rbest = row[r].size();
+          p = r;
+          pv = a;
+        }
       }
-      const double* urow = &lu[static_cast<std::size_t>(c) * k];
-      const double d = urow[c];
-      for (int r = c + 1; r < k; ++r) {
-        double* lrow = &lu[static_cast<std::size_t>(r) * k];
-        if (lrow[c] == 0.0) continue;
-        const double f = lrow[c] / d;
-        lrow[c] = f;
-        for (int j = c + 1; j < k; ++j) lrow[j] -= f * urow[j];
+      prow[t] = p;
+      pcol[t] = q;
+      piv[t] = pv;
+      // U row: the pivot row's other active entries
+      urowc.clear();
+      urowv.clear();
+      for (int c : row[p]) {
+        if (c == q || cdone[c]) continue;
+        for (const auto& e : col[c])
+          if (e.first == p) {
+            urowc.push_back(c);
+            urowv.push_back(e.second);
+            break;
+          }
       }
+      for (std::size_t u = 0; u < urowc.size(); ++u) {
+        uidx.push_back(urowc[u]);
+        uval.push_back(urowv[u]);
+      }
+      ubeg.push_back(static_cast<int>(uidx.size()));
+      // eliminate column q from every other active row
+      for (const auto& [r, a] : col[q]) {
+        if (r == p) continue;
+        const double mult = a / pv;
+        lidx.push_back(r);
+        lval.push_back(mult);
+        for (std::size_t u = 0; u < urowc.size(); ++u) {
+          auto& cc = col[urowc[u]];
+          bool found = false;
+          for (auto& e : cc)
+            if (e.first == r) {
+              e.second -= mult * urowv[u];
+              found = true;
+              break;
+            }
+          if (!found) {  // fill-in
+            cc.emplace_back(r, -mult * urowv[u]);
+            row[r].push_back(urowc[u]);
+          }
+        }
+      }
+      lbeg.push_back(static_cast<int>(lidx.size()));
+      // retire row p and column q
+      rdone[p] = 1;
+      cdone[q] = 1;
+      for (int c : row[p]) {
+        if (cdone[c]) continue;
+        auto& cc = col[c];
+        for (std::size_t e = 0; e < cc.size(); ++e)
+          if (cc[e].first == p) {
+            cc[e] = cc.back();
+            cc.pop_back();
+            break;
+          }
+      }
+      for (const auto& [r, a] : col[q]) {
+        (void)a;
+        if (r == p) continue;
+        auto& rr = row[r];
+        for (std::size_t e = 0; e < rr.size(); ++e)
+          if (rr[e] == q) {
+            rr[e] = rr.back();
+            rr.pop_back();
+            break;
+          }
+      }
+      col[q].clear();
+      row[p].clear();
     }
-    lut.resize(lu.size());
-    for (int i = 0; i < k; ++i)
-      for (int j = 0; j < k; ++j)
-        lut[static_cast<std::size_t>(j) * k + i] = lu[static_cast<std::size_t>(i) * k + j];
     tk1.resize(k);
     tk2.resize(k);
     return true;
+  }
+
+  // kernel solve M z = b: b by kernel row (consumed), z by kernel column
+  void lu_solve(std::vector<double>& b, std::vector<double>& z) {
+    for (int t = 0; t < k; ++t) {
+      const double bt = b[prow[t]];
+      if (bt == 0.0) continue;
+      for (int e = lbeg[t]; e < lbeg[t + 1]; ++e) b[lidx[e]] -= lval[e] * bt;
+    }
+    for (int t = k - 1; t >= 0; --t) {
+      double s = b[prow[t]];
+      for (int e = ubeg[t]; e < ubeg[t + 1]; ++e) s -= uval[e] * z[uidx[e]];
+      z[pcol[t]] = s / piv[t];
+    }
+  }
+
+  // kernel solve M' y = c: c by kernel column (consumed), y by kernel row
+  void lu_solve_t(std::vector<double>& c, std::vector<double>& y) {
+    for (int t = 0; t < k; ++t) {
+      const double h = c[pcol[t]] / piv[t];
+      y[prow[t]] = h;  // provisional: h_t, finished by the L' pass below
+      if (h == 0.0) continue;
+      for (int e = ubeg[t]; e < ubeg[t + 1]; ++e) c[uidx[e]] -= uval[e] * h;
+    }
+    for (int t = k - 1; t >= 0; --t) {
+      double s = y[prow[t]];
+      for (int e = lbeg[t]; e < lbeg[t + 1]; ++e) s -= lval[e] * y[lidx[e]];
+      y[prow[t]] = s;
+    }
   }
 
   void refactor() {
@@ -371,22 +493,8 @@ struct SimplexSolver::Impl {
   void ftran(const std::vector<double>& a, std::vector<double>& w) {
     w.assign(m, 0.0);
     if (k > 0) {
-      for (int i = 0; i < k; ++i) tk1[i] = a[krow[perm[i]]];
-      // column-oriented solves on the transposed factors: a zero entry skips
-      // a whole column (right-hand sides here are very sparse)
-      for (int j = 0; j < k; ++j) {  // L (unit lower)
-        const double t = tk1[j];
-        if (t == 0.0) continue;
-        const double* col = &lut[static_cast<std::size_t>(j) * k];
-        for (int i = j + 1; i < k; ++i) tk1[i] -= col[i] * t;
-      }
-      for (int j = k - 1; j >= 0; --j) {  // U
-        const double* col = &lut[static_cast<std::size_t>(j) * k];
-        const double z = tk1[j] / col[j];
-        tk1[j] = z;
-        if (z == 0.0) continue;
-        for (int i = 0; i < j; ++i) tk1[i] -= col[i] * z;
-      }
+      for (int i = 0; i < k; ++i) tk2[i] = a[krow[i]];
+      lu_solve(tk2, tk1);  // tk1: kernel column order
       for (int i = 0; i < k; ++i) w[kpos[i]] = tk1[i];
     }
     for (int r = 0; r < m; ++r)
@@ -422,22 +530,8 @@ struct SimplexSolver::Impl {
         if (slack_pos[r] >= 0) s -= a * y[r];
       tk1[i] = s;
     }
-    // M' = U' L' P : solve U' s = rhs, L' t = s, y[krow[perm[i]]] = t[i];
-    // row-oriented axpy form of both transposed solves (zero entries skip)
-    for (int i = 0; i < k; ++i) {
-      const double* row = &lu[static_cast<std::size_t>(i) * k];
-      const double sv = tk1[i] / row[i];
-      tk2[i] = sv;
-      if (sv == 0.0) continue;
-      for (int j = i + 1; j < k; ++j) tk1[j] -= row[j] * sv;
-    }
-    for (int i = k - 1; i >= 0; --i) {
-      const double t = tk2[i];
-      if (t == 0.0) continue;
-      const double* row = &lu[static_cast<std::size_t>(i) * k];
-      for (int j = 0; j < i; ++j) tk2[j] -= row[j] * t;
-    }
-    for (int i = 0; i < k; ++i) y[krow[perm[i]]] = tk2[i];
+    lu_solve_t(tk1, tk2);  // tk1 by kernel column -> tk2 by kernel row
+    for (int i = 0; i < k; ++i) y[krow[i]] = tk2[i];
   }
 
   void recompute_basics() {
@@ -517,11 +611,11 @@ struct SimplexSolver::Impl {
       for (int j = 0; j < nv(); ++j) {
         const St s = st[j];
         if (s == St::Basic || v[j].lo == v[j].up) continue;
-        const double d = (phase1 ? 0.0 : v[j].cost) - col_dot(j, y);
+        const double dj = (phase1 ? 0.0 : v[j].cost) - col_dot(j, y);
         int cd = 0;
-        if ((s == St::Lower || s == St::Free) && d > dtol)
+        if ((s == St::Lower || s == St::Free) && dj > dtol)
           cd = 1;
-        else if ((s == St::Upper || s == St::Free) && d < -dtol)
+        else if ((s == St::Upper || s == St::Free) && dj < -dtol)
           cd = -1;
         if (cd == 0) continue;
         if (bland) {
@@ -529,7 +623,7 @@ struct SimplexSolver::Impl {
           dir = cd;
           break;
         }
-        const double score = d * d / ref[j];
+        const double score = dj * dj / ref[j];
         if (score > best) {
           best = score;
           q = j;
