@@ -173,3 +173,36 @@ def test_unfused_lamb_parity(monkeypatch):
     """Three-kernel LAMB (moments / trust / update) stays available."""
     monkeypatch.setenv("SP_LAMB_UNFUSED", "1")
     _run_case("fp16", [0.5, 0.5], [1.0, 3.0], RAGGED, steps=2)
+
+
+@pytest.mark.parametrize("wire", ["fp32", "fp16", "q8"])
+def test_no_writes_outside_user_buffers(wire):
+    """compute-sanitizer is closed on this pool: guard regions after p/m/v and
+    around the gradients must survive rounds untouched (out-of-bounds writes
+    into caller memory would show up here)."""
+    sizes = [3, 1000, 70001, 2, 4096, 131075, 5]
+    n, guard = sum(sizes), 4096
+    sentinel = 12345.678
+
+    def guarded(fill):
+        t = torch.full((n + 2 * guard,), sentinel, device="cuda")
+        t[guard:guard + n] = fill
+        return t
+
+    grads = []
+    for g in range(4):
+        t = torch.full((n + 2 * guard,), sentinel, device="cuda")
+        fill_synthetic(t[guard:guard + n], 5, g, SIGMA)
+        grads.append(t)
+    p, m, v = guarded(0.02), guarded(0.0), guarded(0.0)
+    rnd = AveragingRound(n, sizes, wire=wire, peers_per_rank=4)
+    rnd.assign([0.1, 0.2, 0.3, 0.4], [1.0, 2.0, 3.0, 4.0])
+    views = [g[guard:guard + n] for g in grads]
+    for step in (1, 2, 3):
+        rnd.run(views, p[guard:guard + n], m[guard:guard + n], v[guard:guard + n], step)
+    rnd.run_phased(views, p[guard:guard + n], m[guard:guard + n], v[guard:guard + n], 4)
+    torch.cuda.synchronize()
+    for t in [p, m, v] + grads:
+        assert torch.all(t[:guard] == sentinel) and torch.all(t[guard + n:] == sentinel)
+    assert torch.isfinite(p[guard:guard + n]).all()
+    rnd.close()
