@@ -158,6 +158,29 @@ int sp_round_copy_trust(sp_round* r, float* dst, void* stream);
 int sp_round_read(sp_round* r, int which, int local_peer, size_t offset_bytes,
                   void* host_dst, size_t bytes);
 
+/* Device-side accumulation to the target batch (the round's first step; the
+ * reference only models it: samples = rate * time, /root/reference/proj/src/
+ * netsim.cpp:338-339, and weights the mean by them, groups.cpp:119). Two
+ * accumulator buffers per local peer let a round consume one while the next
+ * step's micro-batches land in the other (DPU).
+ *  - sp_round_accumulate: acc[buf][l] = grad (first call of the round) or
+ *    acc + grad (fp32), and adds `samples` to the peer's count.
+ *  - sp_round_accumulator_ptr: the device fp32[n] accumulator, for writing
+ *    gradients in place (then report them with sp_round_add_samples).
+ *  - sp_round_run_accumulated: the round over acc[buf] weighted by the sample
+ *    counts, which every rank publishes to every rank over NVLink; the
+ *    `weights` of sp_round_set_assignment are not used. Resets the counts of
+ *    `buf` (its next accumulate overwrites). The accumulator may be refilled
+ *    only after this call is ordered before the refill (same stream or event).
+ */
+int sp_round_accumulate(sp_round* r, int buf, int local_peer, const float* grad,
+                        double samples, void* stream);
+float* sp_round_accumulator_ptr(sp_round* r, int buf, int local_peer);
+int sp_round_add_samples(sp_round* r, int buf, int local_peer, double samples);
+double sp_round_samples(const sp_round* r, int buf, int local_peer);
+int sp_round_run_accumulated(sp_round* r, int buf, float* p, float* m, float* v,
+                             int step, void* stream);
+
 /* Synthetic accumulated gradient, bit-identical to the CPU oracle's
  * generator (oracle/sp_oracle.c: sp_oracle_fill_synthetic):
  *   u = splitmix64(seed ^ (peer << 40) ^ i) >> 40;

@@ -59,6 +59,14 @@ class AveragingRound {
   sp_phase_times run_phased(const float* const* grads, float* p, float* m, float* v, int step,
                             void* stream = nullptr);
 
+  // Round step 1 on the device: accumulate micro-batch gradients (two
+  // buffers for delayed parameter updates) and run the round weighted by the
+  // accumulated sample counts (see include/sp_round.h).
+  void accumulate(int buf, int local_peer, const float* grad, double samples, void* stream = nullptr);
+  float* accumulator(int buf, int local_peer);
+  double samples(int buf, int local_peer) const;
+  void run_accumulated(int buf, float* p, float* m, float* v, int step, void* stream = nullptr);
+
   const std::vector<std::int64_t>& offsets() const { return offsets_; }
   sp_round* handle() const { return h_; }
   int peers() const { return cfg_.peers_per_rank * cfg_.world; }

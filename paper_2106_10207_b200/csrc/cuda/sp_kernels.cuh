@@ -88,7 +88,51 @@ struct ReduceArgs {
   int64_t lo, hi;                 // element range reduced by this launch
   int64_t npad;
   int qblock;
+  // device-side weights (accumulation mode): per-peer sample counts published
+  // by every rank; the kernel normalizes them exactly like the host would
+  const double* dev_w;            // G counts (nullptr: use src/w/npeers)
+  const void* all_src[SP_MAX_PEERS];  // inbox slot of every peer
+  int G;
+  int* err;
 };
+
+// Contributing peers of a reduce launch, in peer order. With device weights
+// thread 0 computes sum(w) in fp64 in peer order and (float)(w_g / sum), the
+// same operations the host normalization uses, so results stay bit-exact.
+struct PeerView {
+  const void* src[SP_MAX_PEERS];
+  float w[SP_MAX_PEERS];
+  int np;
+};
+
+__device__ __forceinline__ void load_peers(const ReduceArgs& a, PeerView& pv) {
+  if (threadIdx.x == 0) {
+    if (a.dev_w) {
+      double s = 0.0;
+      for (int g = 0; g < a.G; ++g) s += a.dev_w[g];
+      int np = 0;
+      if (s > 0.0) {
+        for (int g = 0; g < a.G; ++g) {
+          const double w = a.dev_w[g];
+          if (w == 0.0) continue;
+          pv.src[np] = a.all_src[g];
+          pv.w[np] = (float)(w / s);
+          ++np;
+        }
+      } else if (a.err) {
+        atomicExch_system(a.err, 2);  // no samples accumulated anywhere
+      }
+      pv.np = np;
+    } else {
+      for (int g = 0; g < a.npeers; ++g) {
+        pv.src[g] = a.src[g];
+        pv.w[g] = a.w[g];
+      }
+      pv.np = a.npeers;
+    }
+  }
+  __syncthreads();
+}
 
 struct Chunk {
   long long start;
@@ -258,6 +302,49 @@ __global__ void k_barrier(BarrierArgs a) {
   __syncthreads();
 }
 
+// -------------------------------------------------------------- accumulate
+// Peers accumulate micro-batch gradients to the target batch (the DeDLOC
+// round's first step): acc = g for the first micro-batch of a round, then
+// acc = acc + g (one fp32 rounding per add, in call order).
+
+__global__ void __launch_bounds__(256) k_accumulate(float* __restrict__ acc,
+                                                    const float* __restrict__ g, int64_t n,
+                                                    int overwrite) {
+  const int64_t nv = n / 4;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const float4 x = __ldg(reinterpret_cast<const float4*>(g) + v);
+    float4* d = reinterpret_cast<float4*>(acc) + v;
+    if (overwrite) {
+      *d = x;
+    } else {
+      float4 y = *d;
+      y.x = __fadd_rn(y.x, x.x);
+      y.y = __fadd_rn(y.y, x.y);
+      y.z = __fadd_rn(y.z, x.z);
+      y.w = __fadd_rn(y.w, x.w);
+      *d = y;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+    const int64_t i = nv * 4 + threadIdx.x;
+    acc[i] = overwrite ? g[i] : __fadd_rn(acc[i], g[i]);
+  }
+}
+
+// Copies this rank's L per-peer sample counts into the count table of every
+// rank (NVLink stores; the following barrier orders them).
+struct PublishArgs {
+  const double* staged;          // L counts (device copy of the host tallies)
+  double* table[SP_MAX_RANKS];   // every rank's count table for this buffer
+  int world, first, L;
+};
+
+__global__ void k_publish_counts(PublishArgs a) {
+  const int t = threadIdx.x;
+  if (t < a.world * a.L) a.table[t / a.L][a.first + t % a.L] = a.staged[t % a.L];
+}
+
 // -------------------------------------------------------------------- pack
 // K1. fp32 accumulated gradient -> wire format. blockIdx.y = local peer.
 
@@ -378,6 +465,9 @@ __global__ void k_pack_q8(PackArgs a) {
 // into the avg buffer of every rank.
 
 __global__ void __launch_bounds__(256) k_reduce_fp32(ReduceArgs a) {
+  __shared__ PeerView pv;
+  load_peers(a, pv);
+  if (pv.np == 0) return;
   const int64_t nvec = (a.hi - a.lo + 3) / 4;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec;
        v += (int64_t)gridDim.x * blockDim.x) {
@@ -386,29 +476,29 @@ __global__ void __launch_bounds__(256) k_reduce_fp32(ReduceArgs a) {
     // single contributor with weight 1 reproduces its values bit for bit
     float acc[4];
     {
-      const int4 r0 = ld_nc_v4(static_cast<const char*>(a.src[0]) + off);
-      acc[0] = __fmul_rn(a.w[0], __int_as_float(r0.x));
-      acc[1] = __fmul_rn(a.w[0], __int_as_float(r0.y));
-      acc[2] = __fmul_rn(a.w[0], __int_as_float(r0.z));
-      acc[3] = __fmul_rn(a.w[0], __int_as_float(r0.w));
+      const int4 r0 = ld_nc_v4(static_cast<const char*>(pv.src[0]) + off);
+      acc[0] = __fmul_rn(pv.w[0], __int_as_float(r0.x));
+      acc[1] = __fmul_rn(pv.w[0], __int_as_float(r0.y));
+      acc[2] = __fmul_rn(pv.w[0], __int_as_float(r0.z));
+      acc[3] = __fmul_rn(pv.w[0], __int_as_float(r0.w));
     }
     int g = 1;
-    for (; g + 4 <= a.npeers; g += 4) {
+    for (; g + 4 <= pv.np; g += 4) {
       int4 r[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) r[k] = ld_nc_v4(static_cast<const char*>(a.src[g + k]) + off);
+      for (int k = 0; k < 4; ++k) r[k] = ld_nc_v4(static_cast<const char*>(pv.src[g + k]) + off);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const float w = a.w[g + k];
+        const float w = pv.w[g + k];
         acc[0] = __fmaf_rn(w, __int_as_float(r[k].x), acc[0]);
         acc[1] = __fmaf_rn(w, __int_as_float(r[k].y), acc[1]);
         acc[2] = __fmaf_rn(w, __int_as_float(r[k].z), acc[2]);
         acc[3] = __fmaf_rn(w, __int_as_float(r[k].w), acc[3]);
       }
     }
-    for (; g < a.npeers; ++g) {
-      int4 r = ld_nc_v4(static_cast<const char*>(a.src[g]) + off);
-      const float w = a.w[g];
+    for (; g < pv.np; ++g) {
+      int4 r = ld_nc_v4(static_cast<const char*>(pv.src[g]) + off);
+      const float w = pv.w[g];
       acc[0] = __fmaf_rn(w, __int_as_float(r.x), acc[0]);
       acc[1] = __fmaf_rn(w, __int_as_float(r.y), acc[1]);
       acc[2] = __fmaf_rn(w, __int_as_float(r.z), acc[2]);
@@ -441,22 +531,25 @@ __device__ __forceinline__ void mul_half8(float* acc, float w, int4 r) {
 }
 
 __global__ void __launch_bounds__(256) k_reduce_fp16(ReduceArgs a) {
+  __shared__ PeerView pv;
+  load_peers(a, pv);
+  if (pv.np == 0) return;
   const int64_t nvec = (a.hi - a.lo + 7) / 8;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec;
        v += (int64_t)gridDim.x * blockDim.x) {
     const int64_t off = (a.lo + v * 8) * 2;  // bytes
     float acc[8];
-    mul_half8(acc, a.w[0], ld_nc_v4(static_cast<const char*>(a.src[0]) + off));
+    mul_half8(acc, pv.w[0], ld_nc_v4(static_cast<const char*>(pv.src[0]) + off));
     int g = 1;
-    for (; g + 4 <= a.npeers; g += 4) {
+    for (; g + 4 <= pv.np; g += 4) {
       int4 r[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) r[k] = ld_nc_v4(static_cast<const char*>(a.src[g + k]) + off);
+      for (int k = 0; k < 4; ++k) r[k] = ld_nc_v4(static_cast<const char*>(pv.src[g + k]) + off);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) fma_half8(acc, a.w[g + k], r[k]);
+      for (int k = 0; k < 4; ++k) fma_half8(acc, pv.w[g + k], r[k]);
     }
-    for (; g < a.npeers; ++g)
-      fma_half8(acc, a.w[g], ld_nc_v4(static_cast<const char*>(a.src[g]) + off));
+    for (; g < pv.np; ++g)
+      fma_half8(acc, pv.w[g], ld_nc_v4(static_cast<const char*>(pv.src[g]) + off));
     int4 o;
     o.x = (int)pack_half2(acc[0], acc[1]);
     o.y = (int)pack_half2(acc[2], acc[3]);
@@ -494,29 +587,32 @@ __device__ __forceinline__ void mul_q8x16(float* acc, float w, float scale, int4
 __global__ void k_reduce_q8(ReduceArgs a) {
   __shared__ float red[32];
   __shared__ float sc[SP_MAX_PEERS];
+  __shared__ PeerView pv;
+  load_peers(a, pv);
+  if (pv.np == 0) return;
   const int64_t b0 = a.lo / a.qblock;
   const int64_t b1 = (a.hi + a.qblock - 1) / a.qblock;
   for (int64_t b = b0 + blockIdx.x; b < b1; b += gridDim.x) {
     __syncthreads();  // sc reuse across iterations
-    if (threadIdx.x < a.npeers) {
+    if (threadIdx.x < pv.np) {
       const float* s = reinterpret_cast<const float*>(
-          static_cast<const char*>(a.src[threadIdx.x]) + a.npad);
+          static_cast<const char*>(pv.src[threadIdx.x]) + a.npad);
       sc[threadIdx.x] = s[b];
     }
     __syncthreads();
     const int64_t e0 = b * a.qblock + threadIdx.x * 16;
     float acc[16];
-    mul_q8x16(acc, a.w[0], sc[0], ld_nc_v4(static_cast<const char*>(a.src[0]) + e0));
+    mul_q8x16(acc, pv.w[0], sc[0], ld_nc_v4(static_cast<const char*>(pv.src[0]) + e0));
     int g = 1;
-    for (; g + 4 <= a.npeers; g += 4) {
+    for (; g + 4 <= pv.np; g += 4) {
       int4 r[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) r[k] = ld_nc_v4(static_cast<const char*>(a.src[g + k]) + e0);
+      for (int k = 0; k < 4; ++k) r[k] = ld_nc_v4(static_cast<const char*>(pv.src[g + k]) + e0);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) fma_q8x16(acc, a.w[g + k], sc[g + k], r[k]);
+      for (int k = 0; k < 4; ++k) fma_q8x16(acc, pv.w[g + k], sc[g + k], r[k]);
     }
-    for (; g < a.npeers; ++g)
-      fma_q8x16(acc, a.w[g], sc[g], ld_nc_v4(static_cast<const char*>(a.src[g]) + e0));
+    for (; g < pv.np; ++g)
+      fma_q8x16(acc, pv.w[g], sc[g], ld_nc_v4(static_cast<const char*>(pv.src[g]) + e0));
     float amax = 0.0f;
 #pragma unroll
     for (int j = 0; j < 16; ++j) amax = fmaxf(amax, fabsf(acc[j]));

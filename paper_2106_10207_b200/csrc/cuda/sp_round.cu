@@ -50,7 +50,7 @@ struct sp_round {
   int64_t n = 0, npad = 0;
   int align = 8;
   size_t buf_bytes = 0;     // one wire/avg buffer (codes + q8 scales)
-  size_t flags_bytes = 256;
+  size_t flags_bytes = 256;  // barrier flags + per-buffer sample-count tables
   size_t ctr_bytes = 0;     // arrived[ncells] + ready[ncells] (fused round)
   // fused round (one persistent kernel per round)
   bool fused_round = true;
@@ -85,6 +85,12 @@ struct sp_round {
   int p2_off = 0;            // pass-2 items
   cudaStream_t aux = nullptr;
   cudaEvent_t seg_ev[9] = {};
+  // device-side accumulation (two buffers, so a round can consume one while
+  // the next step's micro-batches land in the other)
+  float* acc[2][SP_MAX_LOCAL] = {};
+  double host_count[2][SP_MAX_LOCAL] = {};
+  double* d_stage = nullptr;  // [2][L] staged counts
+  int acc_buf = -1;           // >= 0 while enqueuing an accumulated round
   Chunk* d_chunks = nullptr;
   int2* d_tchunks = nullptr;
   float2* d_partial = nullptr;
@@ -114,6 +120,9 @@ struct sp_round {
     return base[rank] + flags_bytes + ctr_bytes + (size_t)g * buf_bytes;
   }
   char* avg(int rank) const { return base[rank] + flags_bytes + ctr_bytes + (size_t)G * buf_bytes; }
+  double* counts(int rank, int buf) const {
+    return reinterpret_cast<double*>(base[rank] + 256) + (size_t)buf * G;
+  }
   unsigned* arrived(int rank) const { return reinterpret_cast<unsigned*>(base[rank] + flags_bytes); }
   unsigned* ready(int rank) const {
     return reinterpret_cast<unsigned*>(base[rank] + flags_bytes + ctr_bytes / 2);
@@ -332,7 +341,8 @@ int build_round_items(sp_round* r) {
 // not the identity, so it always reduces.
 const char* identity_avg(const sp_round* r) {
   const sp_round_cfg& c = r->cfg;
-  if (c.world != 1 || c.wire == SP_WIRE_Q8 || !r->assigned || r->fused_round) return nullptr;
+  if (c.world != 1 || c.wire == SP_WIRE_Q8 || !r->assigned || r->fused_round || r->acc_buf >= 0)
+    return nullptr;
   int np = 0, who = -1;
   for (int g = 0; g < r->G; ++g)
     if (r->weights[g] != 0.0) {
@@ -491,6 +501,16 @@ int enqueue_round(sp_round* r, const float* const* grads, float* p, float* m, fl
     ba.timeout_ns = (unsigned long long)(to * 1e9);
   }
   const LambArgs la = make_lamb_args(r, p, m, v);
+  if (r->acc_buf >= 0) {  // accumulated round: every rank learns every peer's sample count
+    PublishArgs pa{};
+    pa.staged = r->d_stage + (size_t)r->acc_buf * r->L;
+    for (int k = 0; k < c.world; ++k) pa.table[k] = r->counts(k, r->acc_buf);
+    pa.world = c.world;
+    pa.first = c.rank * r->L;
+    pa.L = r->L;
+    k_publish_counts<<<1, 128, 0, st>>>(pa);
+    SP_CUDA(cudaGetLastError());
+  }
   if (K > 1) {  // fork the aux stream off `st` (graph-capture safe)
     SP_CUDA(cudaEventRecord(r->seg_ev[8], st));
     SP_CUDA(cudaStreamWaitEvent(r->aux, r->seg_ev[8], 0));
@@ -567,6 +587,12 @@ int enqueue_round(sp_round* r, const float* const* grads, float* p, float* m, fl
         ++np;
       }
       ra.npeers = np;
+      if (r->acc_buf >= 0) {
+        ra.dev_w = r->counts(c.rank, r->acc_buf);
+        for (int g = 0; g < r->G; ++g) ra.all_src[g] = r->wire(c.rank, g);
+        ra.G = r->G;
+        ra.err = r->d_err;
+      }
       ra.ndst = c.world;
       for (int k = 0; k < c.world; ++k) ra.dst[k] = r->avg((c.rank + 1 + k) % c.world);
       ra.lo = seg_cut(r, c.rank, s);
@@ -675,6 +701,33 @@ int upload_hparams(sp_round* r, int step, cudaStream_t st) {
   return SP_OK;
 }
 
+// Captures the round into a CUDA graph the first time a (pointer set, mode)
+// is seen, then replays it; per-step scalars go through d_hp.
+int launch_graph(sp_round* r, const std::vector<const void*>& key, const float* const* grads,
+                 float* p, float* m, float* v, int step, cudaStream_t st) {
+  if (!r->gexec || key != r->gkey) {
+    if (r->gexec) {
+      SP_CUDA(cudaStreamSynchronize(st));
+      cudaGraphExecDestroy(r->gexec);
+      r->gexec = nullptr;
+    }
+    cudaGraph_t graph;
+    SP_CUDA(cudaStreamBeginCapture(r->own, cudaStreamCaptureModeThreadLocal));
+    int erc = enqueue_round(r, grads, p, m, v, r->own, nullptr);
+    cudaError_t e = cudaStreamEndCapture(r->own, &graph);
+    if (erc) return erc;
+    if (e != cudaSuccess) return fail(SP_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&r->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return fail(SP_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    r->gkey = key;
+  }
+  int rc = upload_hparams(r, step, st);
+  if (rc) return rc;
+  SP_CUDA(cudaGraphLaunch(r->gexec, st));
+  return SP_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -720,6 +773,7 @@ int sp_round_create(const sp_round_cfg* cfg, sp_round** out) {
     r->ncells = (int)((cfg->n + r->cell - 1) / r->cell);
     r->ctr_bytes = 2 * round_up((int64_t)r->ncells * 4, 256);
   }
+  r->flags_bytes = 256 + round_up((int64_t)2 * r->G * 8, 256);
   r->shared_bytes = r->flags_bytes + r->ctr_bytes + (size_t)(r->G + 1) * r->buf_bytes;
   int dev_sms = 0;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, cfg->device);
@@ -841,6 +895,9 @@ int sp_round_destroy(sp_round* r) {
   cudaFree(r->d_hp);
   cudaFree(r->d_items);
   cudaFree(r->d_qstate);
+  for (int b = 0; b < 2; ++b)
+    for (int l = 0; l < SP_MAX_LOCAL; ++l) cudaFree(r->acc[b][l]);
+  cudaFree(r->d_stage);
   cudaFree(r->d_ritems);
   cudaFree(r->d_rq);
   cudaFree(r->d_repoch);
@@ -933,27 +990,8 @@ int sp_round_run(sp_round* r, const float* const* grads, float* p, float* m, flo
   key.push_back(p);
   key.push_back(m);
   key.push_back(v);
-  if (!r->gexec || key != r->gkey) {
-    if (r->gexec) {
-      SP_CUDA(cudaStreamSynchronize(st));
-      cudaGraphExecDestroy(r->gexec);
-      r->gexec = nullptr;
-    }
-    cudaGraph_t graph;
-    SP_CUDA(cudaStreamBeginCapture(r->own, cudaStreamCaptureModeThreadLocal));
-    int erc = enqueue_round(r, grads, p, m, v, r->own, nullptr);
-    cudaError_t e = cudaStreamEndCapture(r->own, &graph);
-    if (erc) return erc;
-    if (e != cudaSuccess) return fail(SP_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
-    e = cudaGraphInstantiate(&r->gexec, graph, 0);
-    cudaGraphDestroy(graph);
-    if (e != cudaSuccess) return fail(SP_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
-    r->gkey = key;
-  }
-  rc = upload_hparams(r, step, st);
-  if (rc) return rc;
-  SP_CUDA(cudaGraphLaunch(r->gexec, st));
-  return SP_OK;
+  key.push_back(nullptr);  // mode tag: caller-owned gradients, host weights
+  return launch_graph(r, key, grads, p, m, v, step, st);
 }
 
 int sp_round_run_phased(sp_round* r, const float* const* grads, float* p, float* m, float* v,
@@ -1015,6 +1053,83 @@ int sp_round_read(sp_round* r, int which, int local_peer, size_t offset_bytes, v
   SP_CUDA(cudaSetDevice(r->cfg.device));
   SP_CUDA(cudaDeviceSynchronize());
   SP_CUDA(cudaMemcpy(host_dst, src + offset_bytes, bytes, cudaMemcpyDeviceToHost));
+  return SP_OK;
+}
+
+namespace {
+
+int ensure_accumulators(sp_round* r, int buf) {
+  if (r->acc[buf][0]) return SP_OK;
+  SP_CUDA(cudaSetDevice(r->cfg.device));
+  for (int l = 0; l < r->L; ++l) SP_CUDA(cudaMalloc(&r->acc[buf][l], (size_t)r->n * sizeof(float)));
+  if (!r->d_stage) SP_CUDA(cudaMalloc(&r->d_stage, 2 * (size_t)r->L * sizeof(double)));
+  return SP_OK;
+}
+
+}  // namespace
+
+int sp_round_accumulate(sp_round* r, int buf, int local_peer, const float* grad, double samples,
+                        void* stream) {
+  if (!r || !grad) return fail(SP_ERR_ARG, "null argument");
+  if (buf < 0 || buf > 1) return fail(SP_ERR_ARG, "buf must be 0 or 1");
+  if (local_peer < 0 || local_peer >= r->L) return fail(SP_ERR_ARG, "local_peer out of range");
+  if (!(samples >= 0.0) || !std::isfinite(samples)) return fail(SP_ERR_ARG, "samples must be >= 0");
+  if ((reinterpret_cast<uintptr_t>(grad) & 15) != 0) return fail(SP_ERR_SHAPE, "grad must be 16-byte aligned");
+  if (int rc = ensure_accumulators(r, buf)) return rc;
+  SP_CUDA(cudaSetDevice(r->cfg.device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : r->own;
+  const int overwrite = r->host_count[buf][local_peer] == 0.0 ? 1 : 0;
+  k_accumulate<<<grid_for(r->n / 4 + 1, 256, r->sm_count, 8), 256, 0, st>>>(
+      r->acc[buf][local_peer], grad, r->n, overwrite);
+  SP_CUDA(cudaGetLastError());
+  r->host_count[buf][local_peer] += samples;
+  return SP_OK;
+}
+
+float* sp_round_accumulator_ptr(sp_round* r, int buf, int local_peer) {
+  if (!r || buf < 0 || buf > 1 || local_peer < 0 || local_peer >= r->L) return nullptr;
+  if (ensure_accumulators(r, buf)) return nullptr;
+  return r->acc[buf][local_peer];
+}
+
+double sp_round_samples(const sp_round* r, int buf, int local_peer) {
+  if (!r || buf < 0 || buf > 1 || local_peer < 0 || local_peer >= r->L) return -1.0;
+  return r->host_count[buf][local_peer];
+}
+
+int sp_round_add_samples(sp_round* r, int buf, int local_peer, double samples) {
+  if (!r || buf < 0 || buf > 1 || local_peer < 0 || local_peer >= r->L)
+    return fail(SP_ERR_ARG, "bad buffer or peer");
+  if (!(samples >= 0.0) || !std::isfinite(samples)) return fail(SP_ERR_ARG, "samples must be >= 0");
+  r->host_count[buf][local_peer] += samples;
+  return SP_OK;
+}
+
+int sp_round_run_accumulated(sp_round* r, int buf, float* p, float* m, float* v, int step,
+                             void* stream) {
+  if (!r) return fail(SP_ERR_ARG, "null round");
+  if (buf < 0 || buf > 1) return fail(SP_ERR_ARG, "buf must be 0 or 1");
+  if (r->fused_round) return fail(SP_ERR_STATE, "accumulated rounds use the kernel pipeline");
+  if (int rc = ensure_accumulators(r, buf)) return rc;
+  const float* grads[SP_MAX_LOCAL];
+  for (int l = 0; l < r->L; ++l) grads[l] = r->acc[buf][l];
+  int rc = check_run_args(r, grads, p, m, v);
+  if (rc) return rc;
+  SP_CUDA(cudaSetDevice(r->cfg.device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : r->own;
+  SP_CUDA(cudaMemcpyAsync(r->d_stage + (size_t)buf * r->L, r->host_count[buf],
+                          (size_t)r->L * sizeof(double), cudaMemcpyHostToDevice, st));
+  r->acc_buf = buf;
+  std::vector<const void*> key;
+  for (int l = 0; l < r->L; ++l) key.push_back(grads[l]);
+  key.push_back(p);
+  key.push_back(m);
+  key.push_back(v);
+  key.push_back(reinterpret_cast<const void*>((uintptr_t)(buf + 1)));  // mode tag
+  rc = launch_graph(r, key, grads, p, m, v, step, st);
+  r->acc_buf = -1;
+  if (rc) return rc;
+  for (int l = 0; l < r->L; ++l) r->host_count[buf][l] = 0.0;  // next accumulate overwrites
   return SP_OK;
 }
 

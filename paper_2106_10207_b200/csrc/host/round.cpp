@@ -93,4 +93,23 @@ sp_phase_times AveragingRound::run_phased(const float* const* grads, float* p, f
   return t;
 }
 
+void AveragingRound::accumulate(int buf, int local_peer, const float* grad, double samples,
+                                void* stream) {
+  check_status(sp_round_accumulate(h_, buf, local_peer, grad, samples, stream));
+}
+
+float* AveragingRound::accumulator(int buf, int local_peer) {
+  float* p = sp_round_accumulator_ptr(h_, buf, local_peer);
+  if (!p) throw std::invalid_argument("accumulator: bad buffer or peer");
+  return p;
+}
+
+double AveragingRound::samples(int buf, int local_peer) const {
+  return sp_round_samples(h_, buf, local_peer);
+}
+
+void AveragingRound::run_accumulated(int buf, float* p, float* m, float* v, int step, void* stream) {
+  check_status(sp_round_run_accumulated(h_, buf, p, m, v, step, stream));
+}
+
 }  // namespace swarmplan::round

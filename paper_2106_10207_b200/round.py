@@ -149,6 +149,40 @@ class AveragingRound:
                                                 int(step), st, ctypes.byref(t)))
         return {k: float(getattr(t, k)) for k, _ in nat.SpPhaseTimes._fields_}
 
+    # -- device-side accumulation (round step 1) ---------------------------
+    def accumulate(self, local_peer: int, grad, samples: float, buf: int = 0, stream=None) -> None:
+        """acc[buf][local_peer] (+)= grad (fp32, device) and count `samples`."""
+        st = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
+        nat.check(self._lib.sp_round_accumulate(self._h, buf, local_peer, self._dptr(grad, self.n),
+                                                float(samples), st))
+
+    def accumulator(self, local_peer: int = 0, buf: int = 0):
+        """The accumulator as a torch tensor (zero-copy view of executor memory)."""
+        import torch
+
+        ptr = self._lib.sp_round_accumulator_ptr(self._h, buf, local_peer)
+        if not ptr:
+            raise RuntimeError(nat.lib().sp_last_error().decode())
+
+        class _View:  # __cuda_array_interface__ v3
+            __cuda_array_interface__ = {"shape": (self.n,), "typestr": "<f4",
+                                        "data": (int(ptr), False), "version": 3}
+
+        return torch.as_tensor(_View(), device=f"cuda:{self.device}")
+
+    def add_samples(self, local_peer: int, samples: float, buf: int = 0) -> None:
+        nat.check(self._lib.sp_round_add_samples(self._h, buf, local_peer, float(samples)))
+
+    def samples(self, local_peer: int = 0, buf: int = 0) -> float:
+        return float(self._lib.sp_round_samples(self._h, buf, local_peer))
+
+    def run_accumulated(self, p, m, v, step: int, buf: int = 0, stream=None) -> None:
+        """Round over the accumulators of `buf`, weighted by their sample counts."""
+        st = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
+        nat.check(self._lib.sp_round_run_accumulated(self._h, buf, self._dptr(p, self.n),
+                                                     self._dptr(m, self.n), self._dptr(v, self.n),
+                                                     int(step), st))
+
     # -- buffers ------------------------------------------------------------
     def wire_ptr(self, local_peer: int = 0) -> int:
         return int(self._lib.sp_round_wire_ptr(self._h, local_peer))

@@ -37,6 +37,8 @@ def main():
     ap.add_argument("--sizes", default="3,1000,70001,2,4096,131075,5")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--block", type=int, default=4096)
+    ap.add_argument("--accumulate", action="store_true",
+                    help="device-side accumulation: per-peer micro-batches, sample-count weights")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -79,9 +81,35 @@ def main():
     scales = [None if q is None else q[1] for q in packed]
     avg, avg_s = O.reduce(wire, wires, scales, w, 0, n, n, block)
 
+    if args.accumulate:  # peer g accumulates g % 3 + 1 micro-batches of g + 1 samples each
+        micro = {g: [(k, float(g + 1)) for k in range(g % 3 + 1)] for g in range(G)}
+        grads_h = []
+        w = []
+        for g in range(G):
+            acc = None
+            for k, _ in micro[g]:
+                x = O.fill_synthetic(n, 31 + k, g, SIGMA)
+                acc = x.copy() if acc is None else (acc + x).astype(np.float32)
+            grads_h.append(acc)
+            w.append(sum(s for _, s in micro[g]))
+        packed = [O.pack(wire, x, block) for x in grads_h]
+        wires = [q[0] for q in packed]
+        scales = [q[1] for q in packed]
+        avg, avg_s = O.reduce(wire, wires, scales, w, 0, n, n, block)
+
     errors = []
     for step in range(1, args.steps + 1):
-        rnd.run(grads, p, m, v, step)
+        if args.accumulate:
+            buf = step % 2
+            for l in range(L):
+                g = rank * L + l
+                for k, smp in micro[g]:
+                    t = torch.empty(n, device="cuda")
+                    fill_synthetic(t, 31 + k, g, SIGMA)
+                    rnd.accumulate(l, t, smp, buf=buf)
+            rnd.run_accumulated(p, m, v, step, buf=buf)
+        else:
+            rnd.run(grads, p, m, v, step)
         torch.cuda.synchronize()
         got, gs = rnd.read_wire(nat.SP_BUF_AVG)
         if not np.array_equal(got, avg):
@@ -99,7 +127,7 @@ def main():
     dist.all_gather(allg, digest)
     if any(not torch.equal(allg[0], x) for x in allg):
         errors.append("replicas disagree across ranks")
-    t = rnd.run_phased(grads, p, m, v, args.steps + 1)
+    t = {} if args.accumulate else rnd.run_phased(grads, p, m, v, args.steps + 1)
     res = {"rank": rank, "world": world, "G": G, "wire": wire, "errors": errors, "phases": t}
     out = [None] * world
     dist.all_gather_object(out, res)

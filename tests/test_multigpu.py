@@ -70,3 +70,10 @@ def test_one_kernel_round(wire):
     """The opt-in single persistent kernel (pack/scatter, reduce/push, LAMB
     in one launch with per-cell readiness counters) is bit-exact too."""
     _launch(NGPU, "--wire", wire, "--peers-per-rank", "2", env={"SP_ROUND_FUSED": "1"})
+
+
+@pytest.mark.parametrize("wire", ["fp16", "q8"])
+def test_device_accumulation_multi_gpu(wire):
+    """Micro-batches accumulated on each GPU; sample counts published over
+    NVLink weight the average; buffers alternate per step (DPU)."""
+    _launch(NGPU, "--wire", wire, "--peers-per-rank", "2", "--accumulate")

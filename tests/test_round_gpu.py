@@ -206,3 +206,57 @@ def test_no_writes_outside_user_buffers(wire):
         assert torch.all(t[:guard] == sentinel) and torch.all(t[guard + n:] == sentinel)
     assert torch.isfinite(p[guard:guard + n]).all()
     rnd.close()
+
+
+def _micro(n, seed, peer, k):
+    return O.fill_synthetic(n, seed * 100 + k, peer, SIGMA)
+
+
+@pytest.mark.parametrize("wire", ["fp16", "q8"])
+def test_device_accumulation_weighted_by_sample_counts(wire):
+    """Round step 1 on the device: peers accumulate micro-batches, the sample
+    counts weight the average (per-peer counts 3, 1, 0, 5 micro-batches of 8,
+    2, -, 4 samples), two rounds alternating the two buffers (DPU)."""
+    sizes = RAGGED
+    n = sum(sizes)
+    G = 4
+    plan = {0: [(k, 8.0) for k in range(3)], 1: [(0, 2.0)], 2: [], 3: [(k, 4.0) for k in range(5)]}
+    rnd = AveragingRound(n, sizes, wire=wire, peers_per_rank=G, lr=HP["lr"], eps=HP["eps"],
+                         weight_decay=HP["weight_decay"])
+    rnd.assign([0.25] * 4, [1.0] * 4)  # weights unused by accumulated rounds
+    p_h = O.fill_synthetic(n, 2, 0, 0.02, 0)
+    m_h = np.zeros(n, np.float32)
+    v_h = np.zeros(n, np.float32)
+    p_d, m_d, v_d = _dev(p_h.copy()), _dev(m_h.copy()), _dev(v_h.copy())
+    for step, buf in ((1, 0), (2, 1), (3, 0)):
+        accs, counts = [], []
+        for g in range(G):
+            acc = None
+            for k, smp in plan[g]:
+                x = _micro(n, step, g, k)
+                rnd.accumulate(g, _dev(x), smp, buf=buf)
+                acc = x.copy() if acc is None else (acc + x).astype(np.float32)
+            accs.append(acc)
+            counts.append(sum(s for _, s in plan[g]))
+            assert rnd.samples(g, buf) == counts[-1]
+        rnd.run_accumulated(p_d, m_d, v_d, step, buf=buf)
+        torch.cuda.synchronize()
+        assert rnd.samples(0, buf) == 0.0  # counts reset after the round
+        packed = [None if a is None else O.pack(wire, a) for a in accs]
+        wires = [np.zeros(1, np.float32) if q is None else q[0] for q in packed]
+        scales = [None if q is None else q[1] for q in packed]
+        avg, avg_s = O.reduce(wire, wires, scales, counts, 0, n, n)
+        got, gs = rnd.read_wire(nat.SP_BUF_AVG)
+        np.testing.assert_array_equal(got, avg)
+        if wire == "q8":
+            np.testing.assert_array_equal(gs, avg_s)
+        trust = rnd.read_trust()
+        O.lamb(wire, avg, avg_s, p_h, m_h, v_h, sizes, HP, step, trust_in=trust)
+        np.testing.assert_array_equal(p_d.cpu().numpy(), p_h)
+        np.testing.assert_array_equal(m_d.cpu().numpy(), m_h)
+    # writing gradients in place through the accumulator view
+    acc0 = rnd.accumulator(0, buf=1)
+    acc0.copy_(_dev(_micro(n, 9, 0, 0)))
+    rnd.add_samples(0, 6.0, buf=1)
+    assert rnd.samples(0, buf=1) == 6.0
+    rnd.close()
