@@ -181,6 +181,15 @@ double sp_round_samples(const sp_round* r, int buf, int local_peer);
 int sp_round_run_accumulated(sp_round* r, int buf, float* p, float* m, float* v,
                              int step, void* stream);
 
+/* fp64 vector primitives for group all-reduce plans on device-resident rows
+ * (groups::run_plan_device): dst = src * w, dst =
+ * ((0 + s_0) + s_1) + ... (k <= 64), dst = src / d — the operations of
+ * groups::run_plan (/root/reference/proj/src/groups.cpp:120,141-143,158).
+ * Stream-ordered on `stream` (cudaStream_t, NULL = legacy default). */
+int sp_vec_scale(double* dst, const double* src, double w, int64_t n, void* stream);
+int sp_vec_sum(double* dst, const double* const* srcs, int k, int64_t n, void* stream);
+int sp_vec_div(double* dst, const double* src, double d, int64_t n, void* stream);
+
 /* Synthetic accumulated gradient, bit-identical to the CPU oracle's
  * generator (oracle/sp_oracle.c: sp_oracle_fill_synthetic):
  *   u = splitmix64(seed ^ (peer << 40) ^ i) >> 40;

@@ -96,7 +96,8 @@ def build_host(force: bool = False) -> str:
         return out
     if force or _stale(out, HOST_DEPS + [os.path.join(LIB, "libsp_round.so")]):
         _run(["g++", *_host_flags(), "-shared", "-o", out, *HOST_SOURCES,
-              f"-L{LIB}", "-lsp_round", "-Wl,-rpath,$ORIGIN"])
+              f"-L{LIB}", "-lsp_round", f"-L{os.path.join(CUDA_HOME, 'lib64')}", "-lcudart",
+              f"-Wl,-rpath,$ORIGIN:{os.path.join(CUDA_HOME, 'lib64')}"])
     return out
 
 

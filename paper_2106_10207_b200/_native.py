@@ -87,6 +87,9 @@ def lib() -> ctypes.CDLL:
         "sp_round_add_samples": (c_int, [vp, c_int, c_int, ctypes.c_double]),
         "sp_round_samples": (ctypes.c_double, [vp, c_int, c_int]),
         "sp_round_run_accumulated": (c_int, [vp, c_int, vp, vp, vp, c_int, vp]),
+        "sp_vec_scale": (c_int, [vp, vp, ctypes.c_double, i64, vp]),
+        "sp_vec_sum": (c_int, [vp, ctypes.POINTER(vp), c_int, i64, vp]),
+        "sp_vec_div": (c_int, [vp, vp, ctypes.c_double, i64, vp]),
         "sp_fill_synthetic": (c_int, [vp, i64, ctypes.c_uint64, c_int, ctypes.c_float, i64,
                                       ctypes.c_float, vp]),
         "sp_version": (ctypes.c_char_p, []),
@@ -105,7 +108,8 @@ EXPORTED_SYMBOLS = [
     "sp_round_connect", "sp_round_align", "sp_round_set_assignment", "sp_round_run",
     "sp_round_run_phased", "sp_round_wire_ptr", "sp_round_avg_ptr", "sp_round_padded_n",
     "sp_round_trust_ptr", "sp_round_copy_trust", "sp_round_read", "sp_round_accumulate", "sp_round_accumulator_ptr",
-    "sp_round_add_samples", "sp_round_samples", "sp_round_run_accumulated", "sp_fill_synthetic", "sp_version", "sp_last_error",
+    "sp_round_add_samples", "sp_round_samples", "sp_round_run_accumulated",
+    "sp_vec_scale", "sp_vec_sum", "sp_vec_div", "sp_fill_synthetic", "sp_version", "sp_last_error",
 ]
 
 

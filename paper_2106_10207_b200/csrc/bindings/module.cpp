@@ -203,6 +203,38 @@ PYBIND11_MODULE(_swarmplan, m) {
         py::arg("n"), py::arg("m"), py::arg("values"), py::arg("weights") = std::vector<double>{},
         py::arg("failures") = std::vector<std::pair<int, int>>{},
         "groups::run_plan on the CPU (fp64): values is peers x dim.");
+  m.def("run_plan_device",
+        [](int n, int msize, std::vector<std::uintptr_t> values, std::int64_t dim,
+           std::vector<std::uintptr_t> out, std::vector<double> weights,
+           std::vector<std::pair<int, int>> failures, std::uintptr_t stream) {
+          if (static_cast<int>(values.size()) != n || static_cast<int>(out.size()) != n)
+            throw std::invalid_argument("run_plan_device: one device row per peer");
+          groups::GroupPlan plan = groups::build_plan(n, msize);
+          std::vector<const double*> src(n);
+          std::vector<double*> dst(n);
+          for (int i = 0; i < n; ++i) {
+            src[i] = reinterpret_cast<const double*>(values[i]);
+            dst[i] = reinterpret_cast<double*>(out[i]);
+          }
+          std::set<std::pair<int, int>> fs(failures.begin(), failures.end());
+          groups::RunResult res;
+          {
+            py::gil_scoped_release release;
+            res = groups::run_plan_device(plan, src.data(), dim, dst.data(), weights, fs,
+                                          reinterpret_cast<void*>(stream));
+          }
+          py::dict d;
+          std::vector<bool> complete(res.complete.begin(), res.complete.end());
+          d["complete"] = complete;
+          d["coverage"] = res.coverage;
+          d["groups_failed"] = res.groups_failed;
+          return d;
+        },
+        py::arg("n"), py::arg("m"), py::arg("values"), py::arg("dim"), py::arg("out"),
+        py::arg("weights") = std::vector<double>{},
+        py::arg("failures") = std::vector<std::pair<int, int>>{}, py::arg("stream") = 0,
+        "groups::run_plan on the GPU: values/out are device addresses of n fp64 rows of "
+        "length dim; bit-identical to run_plan.");
 
   // ---- LP hooks (tests and tools) -----------------------------------------
   m.def("lp_solve",

@@ -345,6 +345,40 @@ __global__ void k_publish_counts(PublishArgs a) {
   if (t < a.world * a.L) a.table[t / a.L][a.first + t % a.L] = a.staged[t % a.L];
 }
 
+// ------------------------------------------------- group all-reduce (fp64)
+// Vector primitives of groups::run_plan on device-resident rows, in the
+// reference's own arithmetic (fp64; /root/reference/proj/src/groups.cpp:
+// 120 class init w*v, 141-143 merged = 0 + sum in first-seen order, 158
+// sum / weight), so the GPU and CPU plans agree bit for bit.
+
+struct VecList {
+  const double* src[SP_MAX_PEERS];
+  int k;
+};
+
+__global__ void k_vec_scale(double* __restrict__ dst, const double* __restrict__ src, double w,
+                            int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __dmul_rn(src[i], w);
+}
+
+__global__ void k_vec_sum(double* __restrict__ dst, VecList l, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < l.k; ++c) s = __dadd_rn(s, l.src[c][i]);
+    dst[i] = s;
+  }
+}
+
+__global__ void k_vec_div(double* __restrict__ dst, const double* __restrict__ src, double d,
+                          int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __ddiv_rn(src[i], d);
+}
+
 // -------------------------------------------------------------------- pack
 // K1. fp32 accumulated gradient -> wire format. blockIdx.y = local peer.
 

@@ -1133,6 +1133,39 @@ int sp_round_run_accumulated(sp_round* r, int buf, float* p, float* m, float* v,
   return SP_OK;
 }
 
+int sp_vec_scale(double* dst, const double* src, double w, int64_t n, void* stream) {
+  if (!dst || !src || n < 0) return fail(SP_ERR_ARG, "bad vector");
+  if (n == 0) return SP_OK;
+  k_vec_scale<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0,
+                static_cast<cudaStream_t>(stream)>>>(dst, src, w, n);
+  SP_CUDA(cudaGetLastError());
+  return SP_OK;
+}
+
+int sp_vec_sum(double* dst, const double* const* srcs, int k, int64_t n, void* stream) {
+  if (!dst || !srcs || k < 1 || k > SP_MAX_PEERS || n < 0) return fail(SP_ERR_ARG, "bad vector list");
+  if (n == 0) return SP_OK;
+  VecList l{};
+  for (int c = 0; c < k; ++c) {
+    if (!srcs[c]) return fail(SP_ERR_ARG, "null source vector");
+    l.src[c] = srcs[c];
+  }
+  l.k = k;
+  k_vec_sum<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0,
+              static_cast<cudaStream_t>(stream)>>>(dst, l, n);
+  SP_CUDA(cudaGetLastError());
+  return SP_OK;
+}
+
+int sp_vec_div(double* dst, const double* src, double d, int64_t n, void* stream) {
+  if (!dst || !src || n < 0) return fail(SP_ERR_ARG, "bad vector");
+  if (n == 0) return SP_OK;
+  k_vec_div<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0,
+              static_cast<cudaStream_t>(stream)>>>(dst, src, d, n);
+  SP_CUDA(cudaGetLastError());
+  return SP_OK;
+}
+
 int sp_fill_synthetic(float* dev, int64_t n, uint64_t seed, int peer, float scale,
                       int64_t outlier_every, float outlier_mult, void* stream) {
   if (!dev || n < 0) return fail(SP_ERR_ARG, "bad buffer");

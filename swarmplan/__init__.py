@@ -17,6 +17,7 @@ from paper_2106_10207_b200._swarmplan import (  # noqa: F401
     solve_strategy,
     validate_spec,
 )
+from paper_2106_10207_b200.groups import run_plan_gpu  # noqa: F401
 from paper_2106_10207_b200.round import AveragingRound  # noqa: F401
 
 

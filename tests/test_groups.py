@@ -111,3 +111,38 @@ def test_expected_iterations_monte_carlo():
     est = _rounds(n, m) * draws.mean()
     se = _rounds(n, m) * draws.std() / math.sqrt(trials)
     assert abs(sp.expected_iterations(n, m, p) - est) < 3 * se + 1e-9
+
+
+def test_run_plan_device_rejects_bad_rows():
+    # argument checks happen before any device work (CPU-safe)
+    with pytest.raises(ValueError):
+        sp.run_plan_device(4, 2, [0, 0, 0], 8, [0, 0, 0, 0])
+
+
+GPU_CASES = [(4, 2, []), (5, 2, []), (9, 3, []), (16, 4, []), (13, 5, []), (8, 8, []),
+             (6, 2, [(0, 1)]), (9, 3, [(1, 0)]), (16, 2, [(0, 3), (2, 1)]), (10, 4, [(0, 0), (1, 2)])]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,m,failures", GPU_CASES)
+@pytest.mark.parametrize("weighted", [False, True])
+def test_run_plan_gpu_bit_exact(n, m, failures, weighted):
+    import torch
+
+    from paper_2106_10207_b200.groups import run_plan_gpu
+
+    rng = np.random.default_rng(n * 100 + m)
+    dim = 4097
+    vals = rng.standard_normal((n, dim))
+    w = [float(x) for x in rng.integers(0, 9, n)] if weighted else []
+    if weighted:
+        w[0] = max(w[0], 1.0)
+    ref = sp.run_plan(n, m, vals, w, failures)
+    got = run_plan_gpu(n, m, torch.from_numpy(vals).cuda(), w, failures)
+    torch.cuda.synchronize()
+    g = got["values"].cpu().numpy()
+    # 0/0 (an all-zero-weight class) gives NaN on both sides
+    np.testing.assert_array_equal(g, ref["values"])
+    assert got["complete"] == ref["complete"]
+    assert got["coverage"] == ref["coverage"]
+    assert got["groups_failed"] == ref["groups_failed"]
