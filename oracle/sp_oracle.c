@@ -181,6 +181,12 @@ void sp_oracle_reduce(int wire, const void* const* wires, const float* const* sc
     return;
   }
   const int64_t b0 = lo / block, b1 = (hi + block - 1) / block;
+  if (np == 1) { /* one contributor (weight 1): its codes and scales, unchanged */
+    const int g = idx[0];
+    memcpy((int8_t*)out_wire + lo, (const int8_t*)wires[g] + lo, (size_t)(hi - lo));
+    for (int64_t b = b0; b < b1; ++b) out_scales[b] = scales[g][b];
+    return;
+  }
 #pragma omp parallel
   {
     float* tmp = (float*)malloc(sizeof(float) * (size_t)block);

@@ -70,7 +70,10 @@ void sp_oracle_weighted_average_f64(const double* const* values,
  * acc = wn_first * x_first, then acc = fmaf(wn_g, x_g, acc), x_g the dequantized wire value (q8: (float)q * scale); result
  * re-encoded in the wire format into out_wire (and out_scales for q8, whose
  * blocks are aligned: lo % block == 0). wire[g]/scales[g] are peer g's full
- * buffers. */
+ * buffers. q8 with a single contributor forwards its codes and scales
+ * unchanged: the exact average of one peer is that peer's values, and
+ * requantizing them reproduces the codes but can move the scale by one ulp
+ * (fl(fl(127 s)/127) != s for 0.8% of mantissas). */
 void sp_oracle_reduce(int wire, const void* const* wires,
                       const float* const* scales, const double* weights,
                       int G, int64_t lo, int64_t hi, int block,

@@ -151,7 +151,7 @@ struct LambArgs {
   const float* hp;          // device: [lr, 1/(1-b1^t), 1/(1-b2^t)]
   const float* step_scale;  // per tensor lr * trust (update kernel only)
   float b1, b2, omb1, omb2, eps, wd;
-  int qblock;
+  int qshift;               // log2(q8 block): scale index = i >> qshift
   int l2_hints;             // fused LAMB: keep p/m/v of pass 1 in L2 for pass 2
 };
 
@@ -253,6 +253,51 @@ __device__ __forceinline__ float block_max(float x, float* smem32) {
   y = warp_max(y);
   __syncthreads();
   return y;
+}
+
+// 16 values -> 16 packed 8-bit codes, code = clamp(rint(x*inv), +-127).
+// Fast path: y = x*inv is rounded to an integer by adding 1.5*2^23 (exact
+// RNE for |y| < 2^22) and the code is the low byte of the sum; every caller
+// has |x| <= amax and inv = 127/amax, so |y| <= 127*(1+2^-23) < 127.5 and
+// the clamp is implied. A non-finite inv (amax < 127/FLT_MAX) takes the
+// converting path; the block-uniform branch costs nothing otherwise.
+__device__ __forceinline__ int4 quant16(const float* x, float inv) {
+  uint32_t w[4];
+  if (inv <= 3.0e38f) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t t[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) t[j] = __float_as_uint(__fadd_rn(__fmul_rn(x[4 * k + j], inv), 12582912.0f));
+      w[k] = __byte_perm(__byte_perm(t[0], t[1], 0x0040), __byte_perm(t[2], t[3], 0x0040), 0x5410);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t packed = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) packed |= (uint32_t)(q8_code(x[4 * k + j], inv) & 0xff) << (8 * j);
+      w[k] = packed;
+    }
+  }
+  return make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]);
+}
+
+// 4 int8 codes (one word) -> 4 exact floats: each byte, biased by 0x80, is
+// placed in the mantissa of 2^23 (one PRMT) and 2^23 + 128 is subtracted.
+__device__ __forceinline__ float4 dequant4(uint32_t u) {
+  const uint32_t b = u ^ 0x80808080u;
+  return make_float4(__fsub_rn(__uint_as_float(__byte_perm(b, 0x4B000000u, 0x7440)), 8388736.0f),
+                     __fsub_rn(__uint_as_float(__byte_perm(b, 0x4B000000u, 0x7441)), 8388736.0f),
+                     __fsub_rn(__uint_as_float(__byte_perm(b, 0x4B000000u, 0x7442)), 8388736.0f),
+                     __fsub_rn(__uint_as_float(__byte_perm(b, 0x4B000000u, 0x7443)), 8388736.0f));
+}
+
+__device__ __forceinline__ float absmax16(const float* x) {
+  float m = 0.0f;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) m = fmaxf(m, fabsf(x[j]));
+  return m;
 }
 
 // --------------------------------------------------------------- synthetic
@@ -448,45 +493,37 @@ __global__ void __launch_bounds__(256) k_pack_fp16(PackArgs a) {
 
 // Blockwise absmax int8. One CTA (qblock/16 threads) per q8 block; thread t
 // owns 16 contiguous elements. Codes at dst[0, npad), scales at dst + npad.
-__global__ void k_pack_q8(PackArgs a) {
+__device__ __forceinline__ void load16(const float* __restrict__ src, int64_t e0, int64_t n, float* x) {
+  if (e0 + 16 <= n) {
+    const float4* s4 = reinterpret_cast<const float4*>(src + e0);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4 t = __ldg(s4 + k);
+      x[4 * k] = t.x; x[4 * k + 1] = t.y; x[4 * k + 2] = t.z; x[4 * k + 3] = t.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) x[j] = e0 + j < n ? src[e0 + j] : 0.0f;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_pack_q8(PackArgs a) {
   __shared__ float red[32];
   const float* __restrict__ src = a.src[blockIdx.y];
   int j = 0;
   while (j + 1 < a.nr && (int)blockIdx.x >= a.cta0[j + 1]) ++j;
   const int64_t nblk = src ? a.pref[j + 1] - a.pref[j] : 0;
   const int nct = a.cta0[j + 1] - a.cta0[j];
+  int8_t* __restrict__ codes = static_cast<int8_t*>(a.dst[blockIdx.y][a.owner[j]]);
+  float* __restrict__ scales = reinterpret_cast<float*>(codes + a.npad);
   for (int64_t bb = blockIdx.x - a.cta0[j]; bb < nblk; bb += nct) {
     const int64_t b = a.lo[j] + bb;
-    int8_t* __restrict__ codes = static_cast<int8_t*>(a.dst[blockIdx.y][a.owner[j]]);
-    float* __restrict__ scales = reinterpret_cast<float*>(codes + a.npad);
     const int64_t e0 = b * a.qblock + threadIdx.x * 16;
     float x[16];
-    if (e0 + 16 <= a.n) {
-      const float4* s4 = reinterpret_cast<const float4*>(src + e0);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        float4 t = __ldg(s4 + k);
-        x[4 * k] = t.x; x[4 * k + 1] = t.y; x[4 * k + 2] = t.z; x[4 * k + 3] = t.w;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) x[j] = e0 + j < a.n ? src[e0 + j] : 0.0f;
-    }
-    float amax = 0.0f;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) amax = fmaxf(amax, fabsf(x[j]));
-    amax = block_max(amax, red);
+    load16(src, e0, a.n, x);
+    const float amax = block_max(absmax16(x), red);
     const float inv = amax > 0.0f ? __fdiv_rn(127.0f, amax) : 0.0f;
-    uint32_t w[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      uint32_t packed = 0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        packed |= (uint32_t)(q8_code(x[4 * k + j], inv) & 0xff) << (8 * j);
-      w[k] = packed;
-    }
-    st_v4(codes + e0, make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]));
+    st_v4(codes + e0, quant16(x, inv));
     if (threadIdx.x == 0) scales[b] = __fdiv_rn(amax, 127.0f);
   }
 }
@@ -597,11 +634,11 @@ __device__ __forceinline__ void fma_q8x16(float* acc, float w, float scale, int4
   const uint32_t u[4] = {(uint32_t)r.x, (uint32_t)r.y, (uint32_t)r.z, (uint32_t)r.w};
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int q = (int)(int8_t)((u[k] >> (8 * j)) & 0xff);
-      acc[4 * k + j] = __fmaf_rn(w, __fmul_rn((float)q, scale), acc[4 * k + j]);
-    }
+    const float4 q = dequant4(u[k]);
+    acc[4 * k] = __fmaf_rn(w, __fmul_rn(q.x, scale), acc[4 * k]);
+    acc[4 * k + 1] = __fmaf_rn(w, __fmul_rn(q.y, scale), acc[4 * k + 1]);
+    acc[4 * k + 2] = __fmaf_rn(w, __fmul_rn(q.z, scale), acc[4 * k + 2]);
+    acc[4 * k + 3] = __fmaf_rn(w, __fmul_rn(q.w, scale), acc[4 * k + 3]);
   }
 }
 
@@ -609,59 +646,64 @@ __device__ __forceinline__ void mul_q8x16(float* acc, float w, float scale, int4
   const uint32_t u[4] = {(uint32_t)r.x, (uint32_t)r.y, (uint32_t)r.z, (uint32_t)r.w};
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int q = (int)(int8_t)((u[k] >> (8 * j)) & 0xff);
-      acc[4 * k + j] = __fmul_rn(w, __fmul_rn((float)q, scale));
-    }
+    const float4 q = dequant4(u[k]);
+    acc[4 * k] = __fmul_rn(w, __fmul_rn(q.x, scale));
+    acc[4 * k + 1] = __fmul_rn(w, __fmul_rn(q.y, scale));
+    acc[4 * k + 2] = __fmul_rn(w, __fmul_rn(q.z, scale));
+    acc[4 * k + 3] = __fmul_rn(w, __fmul_rn(q.w, scale));
   }
 }
 
-// One CTA (qblock/16 threads) per q8 block of [lo, hi); lo is block aligned.
-__global__ void k_reduce_q8(ReduceArgs a) {
+// q8 blocks of [lo, hi) (lo block aligned), qblock/16 threads per CTA.
+// Every thread loads the peers' scales itself (warp-broadcast loads issued
+// together with the codes), so the only barriers are the block max's two.
+__device__ __forceinline__ float peer_scale(const PeerView& pv, int g, int64_t npad, int64_t b) {
+  return __ldg(reinterpret_cast<const float*>(static_cast<const char*>(pv.src[g]) + npad) + b);
+}
+
+__global__ void __launch_bounds__(1024) k_reduce_q8(ReduceArgs a) {
   __shared__ float red[32];
-  __shared__ float sc[SP_MAX_PEERS];
   __shared__ PeerView pv;
   load_peers(a, pv);
   if (pv.np == 0) return;
   const int64_t b0 = a.lo / a.qblock;
   const int64_t b1 = (a.hi + a.qblock - 1) / a.qblock;
-  for (int64_t b = b0 + blockIdx.x; b < b1; b += gridDim.x) {
-    __syncthreads();  // sc reuse across iterations
-    if (threadIdx.x < pv.np) {
-      const float* s = reinterpret_cast<const float*>(
-          static_cast<const char*>(pv.src[threadIdx.x]) + a.npad);
-      sc[threadIdx.x] = s[b];
+  if (pv.np == 1) {  // one contributor: its codes and scales, forwarded unchanged
+    for (int64_t b = b0 + blockIdx.x; b < b1; b += gridDim.x) {
+      const int64_t e0 = b * a.qblock + threadIdx.x * 16;
+      const int4 r = ld_nc_v4(static_cast<const char*>(pv.src[0]) + e0);
+      const float sc = peer_scale(pv, 0, a.npad, b);
+      for (int k = 0; k < a.ndst; ++k) {
+        char* d = static_cast<char*>(a.dst[k]);
+        st_v4(d + e0, r);
+        if (threadIdx.x == 0) reinterpret_cast<float*>(d + a.npad)[b] = sc;
+      }
     }
-    __syncthreads();
+    return;
+  }
+  for (int64_t b = b0 + blockIdx.x; b < b1; b += gridDim.x) {
     const int64_t e0 = b * a.qblock + threadIdx.x * 16;
     float acc[16];
-    mul_q8x16(acc, pv.w[0], sc[0], ld_nc_v4(static_cast<const char*>(pv.src[0]) + e0));
+    mul_q8x16(acc, pv.w[0], peer_scale(pv, 0, a.npad, b),
+              ld_nc_v4(static_cast<const char*>(pv.src[0]) + e0));
     int g = 1;
     for (; g + 4 <= pv.np; g += 4) {
       int4 r[4];
+      float sc[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) r[k] = ld_nc_v4(static_cast<const char*>(pv.src[g + k]) + e0);
+      for (int k = 0; k < 4; ++k) {
+        r[k] = ld_nc_v4(static_cast<const char*>(pv.src[g + k]) + e0);
+        sc[k] = peer_scale(pv, g + k, a.npad, b);
+      }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) fma_q8x16(acc, pv.w[g + k], sc[g + k], r[k]);
+      for (int k = 0; k < 4; ++k) fma_q8x16(acc, pv.w[g + k], sc[k], r[k]);
     }
     for (; g < pv.np; ++g)
-      fma_q8x16(acc, pv.w[g], sc[g], ld_nc_v4(static_cast<const char*>(pv.src[g]) + e0));
-    float amax = 0.0f;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) amax = fmaxf(amax, fabsf(acc[j]));
-    amax = block_max(amax, red);
+      fma_q8x16(acc, pv.w[g], peer_scale(pv, g, a.npad, b),
+                ld_nc_v4(static_cast<const char*>(pv.src[g]) + e0));
+    const float amax = block_max(absmax16(acc), red);
     const float inv = amax > 0.0f ? __fdiv_rn(127.0f, amax) : 0.0f;
-    uint32_t w[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      uint32_t packed = 0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        packed |= (uint32_t)(q8_code(acc[4 * k + j], inv) & 0xff) << (8 * j);
-      w[k] = packed;
-    }
-    const int4 o = make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]);
+    const int4 o = quant16(acc, inv);
     const float scale = __fdiv_rn(amax, 127.0f);
     for (int k = 0; k < a.ndst; ++k) {
       char* d = static_cast<char*>(a.dst[k]);
@@ -692,11 +734,9 @@ __device__ __forceinline__ float4 load_grad4(const LambArgs& a, int64_t i) {
     return make_float4(lo.x, lo.y, hi.x, hi.y);
   } else {
     const uint32_t u = *reinterpret_cast<const uint32_t*>(static_cast<const int8_t*>(a.avg) + i);
-    const float s = a.avg_scale[i / a.qblock];
-    return make_float4(__fmul_rn((float)(int8_t)(u & 0xff), s),
-                       __fmul_rn((float)(int8_t)((u >> 8) & 0xff), s),
-                       __fmul_rn((float)(int8_t)((u >> 16) & 0xff), s),
-                       __fmul_rn((float)(int8_t)((u >> 24) & 0xff), s));
+    const float s = a.avg_scale[i >> a.qshift];
+    const float4 q = dequant4(u);
+    return make_float4(__fmul_rn(q.x, s), __fmul_rn(q.y, s), __fmul_rn(q.z, s), __fmul_rn(q.w, s));
   }
 }
 
@@ -707,7 +747,7 @@ __device__ __forceinline__ float load_grad1(const LambArgs& a, int64_t i) {
   } else if constexpr (W == SP_WIRE_FP16) {
     return __half2float(static_cast<const __half*>(a.avg)[i]);
   } else {
-    return __fmul_rn((float)static_cast<const int8_t*>(a.avg)[i], a.avg_scale[i / a.qblock]);
+    return __fmul_rn((float)static_cast<const int8_t*>(a.avg)[i], a.avg_scale[i >> a.qshift]);
   }
 }
 
@@ -715,19 +755,35 @@ struct LambScalars {
   float lr, ibc1, ibc2;
 };
 
+// IEEE sqrt / division with exact-zero operands kept off the library slow
+// path (sqrt(+-0) = +-0; (+-0)/d = +-0 for d > 0), bit-identical results.
+// With the 8-bit wire most small gradients average to exactly 0, so m and v
+// stay 0 and the slow path would otherwise double the kernel's instructions.
+__device__ __forceinline__ float sqrt_rn_z(float x) {
+  const bool z = x == 0.0f;
+  const float r = __fsqrt_rn(z ? 1.0f : x);
+  return z ? x : r;
+}
+
+__device__ __forceinline__ float div_rn_z(float a, float b) {
+  const bool z = (a == 0.0f) & (b > 0.0f);
+  const float r = __fdiv_rn(z ? 1.0f : a, b);
+  return z ? a : r;
+}
+
 __device__ __forceinline__ void lamb_moments(const LambArgs& a, const LambScalars& s,
                                              float g, float p, float& m, float& v,
                                              float& u) {
   m = __fmaf_rn(a.b1, m, __fmul_rn(a.omb1, g));
   v = __fmaf_rn(a.b2, v, __fmul_rn(a.omb2, __fmul_rn(g, g)));
-  const float den = __fadd_rn(__fsqrt_rn(__fmul_rn(v, s.ibc2)), a.eps);
-  u = __fmaf_rn(a.wd, p, __fdiv_rn(__fmul_rn(m, s.ibc1), den));
+  const float den = __fadd_rn(sqrt_rn_z(__fmul_rn(v, s.ibc2)), a.eps);
+  u = __fmaf_rn(a.wd, p, div_rn_z(__fmul_rn(m, s.ibc1), den));
 }
 
 __device__ __forceinline__ float lamb_dir(const LambArgs& a, const LambScalars& s,
                                           float p, float m, float v) {
-  const float den = __fadd_rn(__fsqrt_rn(__fmul_rn(v, s.ibc2)), a.eps);
-  return __fmaf_rn(a.wd, p, __fdiv_rn(__fmul_rn(m, s.ibc1), den));
+  const float den = __fadd_rn(sqrt_rn_z(__fmul_rn(v, s.ibc2)), a.eps);
+  return __fmaf_rn(a.wd, p, div_rn_z(__fmul_rn(m, s.ibc1), den));
 }
 
 // Splits chunk [start, start+len) into a scalar head (until 4-aligned), a

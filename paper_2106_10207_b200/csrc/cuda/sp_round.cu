@@ -334,14 +334,14 @@ int build_round_items(sp_round* r) {
   return SP_OK;
 }
 
-// With one rank and a single contributing peer the fp32/fp16 average is the
-// identity on that peer's wire values (acc = fmaf(1.0f, x, 0) = x, and x is
-// exactly representable in the wire format): the averaged vector IS the
-// peer's inbox slot and the reduce kernel is skipped. q8 requantization is
-// not the identity, so it always reduces.
+// With one rank and a single contributing peer the average is the identity
+// on that peer's wire values: fp32/fp16 because acc = 1.0f * x = x is exactly
+// representable in the wire format, q8 by definition (a single contributor's
+// codes and scales are forwarded; sp_oracle_reduce). The averaged vector IS
+// the peer's inbox slot and the reduce kernel is skipped.
 const char* identity_avg(const sp_round* r) {
   const sp_round_cfg& c = r->cfg;
-  if (c.world != 1 || c.wire == SP_WIRE_Q8 || !r->assigned || r->fused_round || r->acc_buf >= 0)
+  if (c.world != 1 || !r->assigned || r->fused_round || r->acc_buf >= 0)
     return nullptr;
   int np = 0, who = -1;
   for (int g = 0; g < r->G; ++g)
@@ -361,7 +361,7 @@ LambArgs make_lamb_args(sp_round* r, float* p, float* m, float* v) {
   const sp_round_cfg& c = r->cfg;
   LambArgs a{};
   a.avg = avg_buffer(r);
-  a.avg_scale = c.wire == SP_WIRE_Q8 ? reinterpret_cast<const float*>(r->avg(c.rank) + r->npad)
+  a.avg_scale = c.wire == SP_WIRE_Q8 ? reinterpret_cast<const float*>(avg_buffer(r) + r->npad)
                                      : nullptr;
   a.p = p;
   a.m = m;
@@ -376,7 +376,7 @@ LambArgs make_lamb_args(sp_round* r, float* p, float* m, float* v) {
   a.omb2 = 1.0f - c.beta2;
   a.eps = c.eps;
   a.wd = c.weight_decay;
-  a.qblock = c.q8_block;
+  a.qshift = __builtin_ctz((unsigned)std::max(c.q8_block, 1));
   a.l2_hints = r->l2_hints;
   return a;
 }

@@ -249,6 +249,14 @@ __device__ __forceinline__ void fused_reduce(const RoundFused& f, int64_t s, int
         sc[tid] = __ldcg(reinterpret_cast<const float*>(base + (size_t)f.peer[tid] * f.slot_bytes + f.npad) + b);
       __syncthreads();
       const size_t e0 = (size_t)b * 4096 + tid * 16;
+      if (f.npeers == 1) {  // one contributor: codes and scale forwarded unchanged
+        const int4 o = ld_cg_v4(base + (size_t)f.peer[0] * f.slot_bytes + e0);
+        for (int k = 0; k < f.world; ++k) {
+          st_v4(f.avg[k] + e0, o);
+          if (tid == 0) reinterpret_cast<float*>(f.avg[k] + f.npad)[b] = sc[0];
+        }
+        continue;
+      }
       float acc[16];
       mul_q8x16(acc, f.w[0], sc[0], ld_cg_v4(base + (size_t)f.peer[0] * f.slot_bytes + e0));
       int g = 1;

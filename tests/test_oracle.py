@@ -111,6 +111,30 @@ def test_reduce_close_to_fp64_weighted_mean(wire):
     assert np.abs(got - ref).max() <= tol * scale
 
 
+@pytest.mark.parametrize("wire", ["fp32", "fp16", "q8"])
+def test_reduce_single_contributor_is_identity(wire):
+    # one nonzero weight: the average is that peer's wire values, unchanged
+    # (q8 by definition: codes and scales forwarded, no requantization)
+    n, block = 5 * 4096 + 300, 4096
+    packed = [O.pack(wire, O.fill_synthetic(n, 3, g, 1e-3, 997, 100.0), block) for g in range(3)]
+    out, osc = O.reduce(wire, [p[0] for p in packed], [p[1] for p in packed], [0.0, 7.0, 0.0],
+                        0, n, n, block)
+    np.testing.assert_array_equal(out, packed[1][0][:n])
+    if wire == "q8":
+        np.testing.assert_array_equal(osc, packed[1][1])
+
+
+def test_q8_requantize_keeps_codes():
+    # why forwarding is the right definition: requantizing a peer's dequantized
+    # block reproduces every code; only the scale may move by an ulp
+    n, block = 8 * 4096, 4096
+    c, s = O.pack_q8(O.fill_synthetic(n, 4, 0, 1e-3, 997, 100.0), block)
+    deq = O.dequant("q8", c, s, block)
+    c2, s2 = O.pack_q8(deq, block)
+    np.testing.assert_array_equal(c, c2)
+    assert np.all(np.abs(s2.view(np.int32) - s.view(np.int32)) <= 1)
+
+
 # ------------------------------------------------------------------- LAMB
 def _lamb_numpy(g, p, m, v, sizes, hp, step):
     p, m, v = p.astype(np.float64), m.astype(np.float64), v.astype(np.float64)
