@@ -196,6 +196,8 @@ def main():
     ap.add_argument("--peers-per-gpu", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--phased-steps", type=int, default=20)
+    ap.add_argument("--shard-lamb", action="store_true",
+                    help="ZeRO-1 style LAMB: owners step their range, parameters pushed to all ranks")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -234,14 +236,14 @@ def main():
     rnd = AveragingRound(n, tsizes, wire=wire, q8_block=block, peers_per_rank=L, rank=rank,
                          world=world, device=local_rank, lr=HP["lr"],
                          betas=(HP["beta1"], HP["beta2"]), eps=HP["eps"],
-                         weight_decay=HP["weight_decay"])
+                         weight_decay=HP["weight_decay"], shard_lamb=args.shard_lamb)
     offsets = rnd.assign(fractions, weights)
     grads = []
     for l in range(L):
         g = torch.empty(n, dtype=torch.float32, device=dev)
         fill_synthetic(g, 1, rank * L + l, SIGMA)
         grads.append(g)
-    p = torch.empty(n, dtype=torch.float32, device=dev)
+    p = rnd.param_buffer() if args.shard_lamb else torch.empty(n, dtype=torch.float32, device=dev)
     fill_synthetic(p, 2, 0, 0.02, 0)
     m = torch.zeros(n, dtype=torch.float32, device=dev)
     v = torch.zeros(n, dtype=torch.float32, device=dev)
@@ -345,27 +347,41 @@ def main():
         peak, peak_kind = peak_hbm()
         f_r = (offsets[(rank + 1) * L] - offsets[rank * L]) / n
         fused = ph["update_ms"] < 0.1 * ph["moments_ms"]  # fused LAMB: one kernel
+        shard = args.shard_lamb
+        if shard:
+            fused = False
+        f_l = f_r if shard else 1.0  # fraction of the vector this rank's LAMB steps
         alg = {  # algorithmic bytes per launch, this rank
             "pack_ms": (L * n * (4 + b)) if (wire != "fp32" or world > 1) else 0.0,
-            "reduce_ms": (G + world) * f_r * n * b,
+            "reduce_ms": (G + (1 if shard else world)) * f_r * n * b,
             # fused kernel: pass 1 reads g,p,m,v writes m,v; pass 2 reads p,m,v writes p
-            "moments_ms": n * (20 + b) + (n * 16.0 if fused else 0.0),
-            "update_ms": 0.0 if fused else n * 16.0,
+            "moments_ms": f_l * n * (20 + b) + (n * 16.0 if fused else 0.0),
+            "update_ms": 0.0 if fused else f_l * n * 16.0,
         }
         dom = max(("pack_ms", "reduce_ms", "moments_ms", "update_ms"), key=lambda k: ph[k])
-        kname = {"pack_ms": "k_pack", "reduce_ms": "k_reduce",
-                 "moments_ms": "k_lamb_fused" if fused else "k_lamb_moments",
-                 "update_ms": "k_lamb_update"}[dom]
+        widx = {"fp32": 0, "fp16": 1, "q8": 2}[wire]
+        kname = {"pack_ms": f"k_pack_{wire}", "reduce_ms": f"k_reduce_{wire}",
+                 "moments_ms": f"k_lamb_fused<{widx}>" if fused else f"k_lamb_moments<{widx}>",
+                 "update_ms": f"k_lamb_update<{widx}>"}[dom]
         achieved = alg[dom] / (ph[dom] * 1e-3) / 1e9
         bound, pk, unit = "hbm", peak, "GB/s"
-        if dom in ("reduce_ms", "pack_ms") and world > 1:
+        if shard and dom == "update_ms" and world > 1:  # parameter push: (world-1) f 4 B out
+            bound, pk = "nvlink", NVLINK_GBS
+            achieved = (world - 1) * f_r * 4.0 * n / (ph[dom] * 1e-3) / 1e9
+        elif dom in ("reduce_ms", "pack_ms") and world > 1:
             bound, pk = "nvlink", NVLINK_GBS
             # per direction: pack scatters (1-f) b n, reduce pushes (G-1) f b n
             nvl = ((1 - f_r) * b * n) if dom == "pack_ms" else ((world - 1) * f_r * b * n)
             achieved = nvl / (ph[dom] * 1e-3) / 1e9
         # whole-round roofline: serialized HBM + NVLink phases
-        hbm_round = ((4 + b) * L if wire != "fp32" else 0.0) + G * f_r * b + f_r * b + 24 + b
-        nvl_round = ((1 - f_r) * b + (G - 1) * f_r * b) if world > 1 else 0.0
+        # (G = 1: the average of one peer is its wire values, no reduce pass)
+        hbm_round = ((4 + b) * L if (wire != "fp32" or world > 1) else 0.0) + \
+            ((G + (1 if shard else world)) * f_r * b if G > 1 else 0.0) + \
+            f_l * (24 + b)  # one-pass LAMB ideal
+        if shard:  # scatter the gradient parts, push the updated fp32 parameters
+            nvl_round = ((1 - f_r) * b + (world - 1) * f_r * 4.0) if world > 1 else 0.0
+        else:
+            nvl_round = ((1 - f_r) * b + (G - 1) * f_r * b) if world > 1 else 0.0
         t_roof = hbm_round * n / (peak * 1e9) + nvl_round * n / (NVLINK_GBS * 1e9)
         lp_times = None
         try:
@@ -399,11 +415,16 @@ def main():
             "config": {"workload": f"{args.workload}: DeDLOC butterfly round + LAMB",
                        "params": n, "tensors": len(tsizes), "peers": G, "peers_per_gpu": L,
                        "wire": wire, "q8_block": block if wire == "q8" else None,
+                       "lamb": "sharded (ZeRO-1: owners step, fp32 params pushed)" if args.shard_lamb
+                               else "replicated (averaged gradient all-gathered)",
                        "fractions": "uniform 1/G (LP, homogeneous fleet)",
                        "l2": f"no flush: per-step working set {(n * (12 + 4 * L + 2 * b)) / 1e9:.2f} GB > 126 MB L2",
                        "parallelism": f"dp{world} (one peer per GPU, CUDA IPC over NVLink)"},
             # per round: pack + reduce + LAMB (1 fused / 3 unfused) + 2 barriers if N > 1
-            "gpu_launches": args.steps * (2 + (1 if fused else 3) + (2 if world > 1 else 0)),
+            # (one rank with a single peer skips the reduce: identity average)
+            "gpu_launches": args.steps * (
+                (1 + (1 if G > 1 else 0) + 4 + (4 if world > 1 else 0)) if shard else
+                (1 + (1 if G > 1 else 0) + (1 if fused else 3) + (2 if world > 1 else 0))),
             "kernel_ms": {k: round(v_, 5) for k, v_ in ph.items()},
             "roofline": {"bound": bound, "kernel": dom.replace("_ms", ""),
                          "achieved": round(achieved, 1), "peak": pk, "unit": unit,

@@ -75,6 +75,12 @@ typedef struct {
   float lr, beta1, beta2, eps, weight_decay;
   int bias_correction; /* 1: Adam-style bias correction of m and v           */
   double barrier_timeout_s; /* cross-rank spin limit (0 -> 20 s)             */
+  int shard_lamb;      /* 1: sharded LAMB (ZeRO-1 style): each
+                        * rank steps only the range it owns, per-tensor norm
+                        * partials are exchanged over NVLink, and the updated
+                        * parameters (not the averaged gradient) are pushed to
+                        * every rank. p must be sp_round_param_ptr(); m and v
+                        * stay full-length but only the owned range is kept. */
 } sp_round_cfg;
 
 /* Per-kernel device times of the last sp_round_run_phased call (ms). */
@@ -138,6 +144,11 @@ int sp_round_run_phased(sp_round* r, const float* const* grads, float* p,
  * rank's all-gathered averaged vector in the wire format; q8 scales follow
  * the codes at avg + padded_n. */
 void* sp_round_wire_ptr(sp_round* r, int local_peer);
+
+/* shard_lamb: this rank's flat fp32[n] parameter vector, inside the
+ * IPC-shared allocation so that owners can store their updated ranges into
+ * every rank's copy (NULL without shard_lamb). */
+float* sp_round_param_ptr(sp_round* r);
 void* sp_round_avg_ptr(sp_round* r);
 int64_t sp_round_padded_n(const sp_round* r);
 /* Per-tensor trust ratios of the last step (device float[num_tensors]). */

@@ -39,6 +39,7 @@ class SpRoundCfg(ctypes.Structure):
         ("weight_decay", ctypes.c_float),
         ("bias_correction", ctypes.c_int),
         ("barrier_timeout_s", ctypes.c_double),
+        ("shard_lamb", ctypes.c_int),
     ]
 
 
@@ -78,6 +79,7 @@ def lib() -> ctypes.CDLL:
                                         ctypes.POINTER(SpPhaseTimes)]),
         "sp_round_wire_ptr": (vp, [vp, c_int]),
         "sp_round_avg_ptr": (vp, [vp]),
+        "sp_round_param_ptr": (vp, [vp]),
         "sp_round_padded_n": (i64, [vp]),
         "sp_round_trust_ptr": (vp, [vp]),
         "sp_round_copy_trust": (c_int, [vp, vp, vp]),
@@ -106,7 +108,8 @@ def lib() -> ctypes.CDLL:
 EXPORTED_SYMBOLS = [
     "sp_round_create", "sp_round_destroy", "sp_round_handle_bytes", "sp_round_export",
     "sp_round_connect", "sp_round_align", "sp_round_set_assignment", "sp_round_run",
-    "sp_round_run_phased", "sp_round_wire_ptr", "sp_round_avg_ptr", "sp_round_padded_n",
+    "sp_round_run_phased", "sp_round_wire_ptr", "sp_round_avg_ptr", "sp_round_param_ptr",
+    "sp_round_padded_n",
     "sp_round_trust_ptr", "sp_round_copy_trust", "sp_round_read", "sp_round_accumulate", "sp_round_accumulator_ptr",
     "sp_round_add_samples", "sp_round_samples", "sp_round_run_accumulated",
     "sp_vec_scale", "sp_vec_sum", "sp_vec_div", "sp_fill_synthetic", "sp_version", "sp_last_error",

@@ -1182,4 +1182,99 @@ __global__ void __launch_bounds__(kLambThreads) k_lamb_update(LambArgs a) {
   }
 }
 
+// ------------------------------------------------------ sharded LAMB (N1)
+// ZeRO-1 style step: the owner of [lo, hi) runs pass 1
+// (k_lamb_moments) on its range only. Per tensor it sums its chunk partials
+// in fp64 (chunk order) and stores the pair into slot [rank][t] of every
+// rank's norm table; after a barrier every rank adds the world slots in rank
+// order, so all ranks hold identical trust ratios; pass 2 updates the owned
+// range and stores p' into every rank's parameter vector over NVLink.
+
+struct ShardNormArgs {
+  const float2* partial;
+  const int2* tchunks;             // this rank's chunks of tensor t (may be empty)
+  double2* table[SP_MAX_RANKS];    // push order: next rank first, self last
+  int ndst, rank, T;
+};
+
+__global__ void __launch_bounds__(256) k_shard_norms(ShardNormArgs a) {
+  __shared__ double sx[256], sy[256];
+  const int t = blockIdx.x;
+  const int2 r = a.tchunks[t];
+  double x = 0.0, y = 0.0;
+  for (int c = r.x + threadIdx.x; c < r.y; c += blockDim.x) {
+    const float2 q = a.partial[c];
+    x += (double)q.x;
+    y += (double)q.y;
+  }
+  sx[threadIdx.x] = x;
+  sy[threadIdx.x] = y;
+  __syncthreads();
+  for (int h = blockDim.x / 2; h > 0; h >>= 1) {
+    if (threadIdx.x < h) {
+      sx[threadIdx.x] += sx[threadIdx.x + h];
+      sy[threadIdx.x] += sy[threadIdx.x + h];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < a.ndst) a.table[threadIdx.x][(size_t)a.rank * a.T + t] = make_double2(sx[0], sy[0]);
+}
+
+// trust[t] = sqrt(sum_k pp[k][t]) / sqrt(sum_k uu[k][t]) over ranks in order
+// (1 if either is 0); step_scale[t] = lr * trust[t].
+__global__ void k_shard_trust(const double2* __restrict__ table, int world, int T,
+                              const float* __restrict__ hp, float* __restrict__ trust,
+                              float* __restrict__ step_scale) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
+    double x = 0.0, y = 0.0;
+    for (int k = 0; k < world; ++k) {
+      const double2 v = __ldcg(table + (size_t)k * T + t);
+      x += v.x;
+      y += v.y;
+    }
+    const double r1 = sqrt(x), r2 = sqrt(y);
+    const float tr = (r1 > 0.0 && r2 > 0.0) ? (float)(r1 / r2) : 1.0f;
+    trust[t] = tr;
+    step_scale[t] = __fmul_rn(hp[0], tr);
+  }
+}
+
+struct ParamPush {
+  float* dst[SP_MAX_RANKS];  // every rank's parameter vector, next rank first, self last
+  int ndst;
+};
+
+// Pass 2 of the owned chunks: p' = p - lr*trust*u, stored into every rank's
+// copy (the local one last, so the local read of p precedes the local write).
+template <int W>
+__global__ void __launch_bounds__(kLambThreads) k_lamb_update_push(LambArgs a, ParamPush d) {
+  const Chunk c = a.chunks[blockIdx.x];
+  const LambScalars s{a.hp[0], a.hp[1], a.hp[2]};
+  const float neg = -__ldcg(a.step_scale + c.tensor);
+  const ChunkSplit sp = split_chunk(c);
+  const int t = threadIdx.x;
+  int64_t si = -1;
+  if (t < sp.head) si = sp.start + t;
+  else if (t >= 32 && t - 32 < sp.tail) si = sp.start + sp.head + 4 * (int64_t)sp.nbody4 + (t - 32);
+  if (si >= 0) {
+    const float p = a.p[si];
+    const float q = __fmaf_rn(neg, lamb_dir(a, s, p, a.m[si], a.v[si]), p);
+    for (int k = 0; k < d.ndst; ++k) d.dst[k][si] = q;
+  }
+  const int64_t b0 = sp.start + sp.head;
+  for (int k = t; k < sp.nbody4; k += kLambThreads) {
+    const int64_t i = b0 + 4 * (int64_t)k;
+    float4 p = *reinterpret_cast<const float4*>(a.p + i);
+    const float4 m = *reinterpret_cast<const float4*>(a.m + i);
+    const float4 v = *reinterpret_cast<const float4*>(a.v + i);
+    p.x = __fmaf_rn(neg, lamb_dir(a, s, p.x, m.x, v.x), p.x);
+    p.y = __fmaf_rn(neg, lamb_dir(a, s, p.y, m.y, v.y), p.y);
+    p.z = __fmaf_rn(neg, lamb_dir(a, s, p.z, m.z, v.z), p.z);
+    p.w = __fmaf_rn(neg, lamb_dir(a, s, p.w, m.w, v.w), p.w);
+    const int4 o = make_int4(__float_as_int(p.x), __float_as_int(p.y), __float_as_int(p.z),
+                             __float_as_int(p.w));
+    for (int q = 0; q < d.ndst; ++q) st_v4(d.dst[q] + i, o);
+  }
+}
+
 }  // namespace sp

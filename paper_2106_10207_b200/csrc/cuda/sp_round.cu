@@ -115,7 +115,12 @@ struct sp_round {
   std::vector<const void*> gkey;
   cudaEvent_t ev[8] = {};
   int sm_count = 148;
+  // sharded LAMB (cfg.shard_lamb): flat parameter vector + per-rank norm table
+  bool shard = false;
+  size_t param_off = 0, norms_off = 0;
 
+  float* param(int rank) const { return reinterpret_cast<float*>(base[rank] + param_off); }
+  double2* norms(int rank) const { return reinterpret_cast<double2*>(base[rank] + norms_off); }
   char* wire(int rank, int g) const {
     return base[rank] + flags_bytes + ctr_bytes + (size_t)g * buf_bytes;
   }
@@ -185,13 +190,19 @@ int build_lamb_tables(sp_round* r, bool with_cuts) {
   std::sort(cuts.begin(), cuts.end());
   std::vector<Chunk> chunks;
   std::vector<int2> tch;
+  // sharded LAMB: only the range this rank owns
+  int64_t own_lo = 0, own_hi = r->n;
+  if (r->shard && !r->offsets.empty()) {
+    own_lo = r->offsets[(size_t)r->cfg.rank * r->L];
+    own_hi = r->offsets[(size_t)(r->cfg.rank + 1) * r->L];
+  }
   int64_t off = 0;
   size_t ci = 0;
   for (size_t t = 0; t < r->tsizes.size(); ++t) {
-    const int64_t end = off + r->tsizes[t];
+    const int64_t end = std::min(off + r->tsizes[t], own_hi);
     int2 rg;
     rg.x = (int)chunks.size();
-    int64_t s = off;
+    int64_t s = std::max(off, own_lo);
     while (s < end) {
       int64_t e = std::min(end, (s / r->lamb_chunk + 1) * r->lamb_chunk);
       while (ci < cuts.size() && cuts[ci] <= s) ++ci;
@@ -201,7 +212,7 @@ int build_lamb_tables(sp_round* r, bool with_cuts) {
     }
     rg.y = (int)chunks.size();
     tch.push_back(rg);
-    off = end;
+    off += r->tsizes[t];
   }
   if ((int)chunks.size() > r->nchunks_cap) return fail(SP_ERR_STATE, "LAMB chunk table overflow");
   const int K = with_cuts ? r->segments : 1;
@@ -475,6 +486,59 @@ int launch_lamb(sp_round* r, LambArgs a, int first_item, int nitems, bool final_
   return SP_OK;
 }
 
+// Sharded LAMB (cfg.shard_lamb): pass 1 over the owned chunks, per-tensor
+// norm partials pushed to every rank + barrier, trust (rank-ordered sum),
+// pass 2 storing p' into every rank's parameter vector + barrier (no rank
+// may read parameters before every owner has stored its range).
+int enqueue_shard_lamb(sp_round* r, const LambArgs& la, const BarrierArgs& ba, cudaStream_t st,
+                       cudaEvent_t* ev) {
+  const sp_round_cfg& c = r->cfg;
+  const int nc = r->nchunks, T = c.num_tensors;
+  if (nc > 0) {
+    switch (c.wire) {
+      case SP_WIRE_FP32: k_lamb_moments<SP_WIRE_FP32><<<nc, kLambThreads, 0, st>>>(la); break;
+      case SP_WIRE_FP16: k_lamb_moments<SP_WIRE_FP16><<<nc, kLambThreads, 0, st>>>(la); break;
+      default: k_lamb_moments<SP_WIRE_Q8><<<nc, kLambThreads, 0, st>>>(la); break;
+    }
+    SP_CUDA(cudaGetLastError());
+  }
+  if (ev) SP_CUDA(cudaEventRecord(ev[5], st));
+  ShardNormArgs na{};
+  na.partial = r->d_partial;
+  na.tchunks = r->d_tchunks;
+  na.ndst = c.world;
+  for (int k = 0; k < c.world; ++k) na.table[k] = r->norms((c.rank + 1 + k) % c.world);
+  na.rank = c.rank;
+  na.T = T;
+  k_shard_norms<<<T, 256, 0, st>>>(na);
+  SP_CUDA(cudaGetLastError());
+  if (c.world > 1) {
+    k_barrier<<<1, 32, 0, st>>>(ba);
+    SP_CUDA(cudaGetLastError());
+  }
+  k_shard_trust<<<(T + 255) / 256, 256, 0, st>>>(r->norms(c.rank), c.world, T, r->d_hp, r->d_trust,
+                                                 r->d_step_scale);
+  SP_CUDA(cudaGetLastError());
+  if (ev) SP_CUDA(cudaEventRecord(ev[6], st));
+  ParamPush pp{};
+  pp.ndst = c.world;
+  for (int k = 0; k < c.world; ++k) pp.dst[k] = r->param((c.rank + 1 + k) % c.world);
+  if (nc > 0) {
+    switch (c.wire) {
+      case SP_WIRE_FP32: k_lamb_update_push<SP_WIRE_FP32><<<nc, kLambThreads, 0, st>>>(la, pp); break;
+      case SP_WIRE_FP16: k_lamb_update_push<SP_WIRE_FP16><<<nc, kLambThreads, 0, st>>>(la, pp); break;
+      default: k_lamb_update_push<SP_WIRE_Q8><<<nc, kLambThreads, 0, st>>>(la, pp); break;
+    }
+    SP_CUDA(cudaGetLastError());
+  }
+  if (c.world > 1) {
+    k_barrier<<<1, 32, 0, st>>>(ba);
+    SP_CUDA(cudaGetLastError());
+  }
+  if (ev) SP_CUDA(cudaEventRecord(ev[7], st));
+  return SP_OK;
+}
+
 // Enqueues the whole round on `st`. ev != nullptr records phase events.
 //
 // Kernel pipeline per segment s = 0..K-1 (K = 1 with one rank):
@@ -593,8 +657,9 @@ int enqueue_round(sp_round* r, const float* const* grads, float* p, float* m, fl
         ra.G = r->G;
         ra.err = r->d_err;
       }
-      ra.ndst = c.world;
-      for (int k = 0; k < c.world; ++k) ra.dst[k] = r->avg((c.rank + 1 + k) % c.world);
+      // sharded LAMB steps only the owned range: the average stays local
+      ra.ndst = r->shard ? 1 : c.world;
+      for (int k = 0; k < ra.ndst; ++k) ra.dst[k] = r->avg((c.rank + 1 + k + (r->shard ? c.world - 1 : 0)) % c.world);
       ra.lo = seg_cut(r, c.rank, s);
       ra.hi = seg_cut(r, c.rank, s + 1);
       ra.npad = r->npad;
@@ -626,6 +691,7 @@ int enqueue_round(sp_round* r, const float* const* grads, float* p, float* m, fl
     }
   }
   if (ev) SP_CUDA(cudaEventRecord(ev[4], st));
+  if (r->shard) return enqueue_shard_lamb(r, la, ba, st, ev);
   // K3/K4 LAMB on this rank's replica
   if (r->fused_lamb) {
     if (K > 1) {
@@ -676,6 +742,8 @@ int check_run_args(sp_round* r, const float* const* grads, float* p, float* m, f
   if (!grads || !p || !m || !v) return fail(SP_ERR_ARG, "null buffer");
   auto aligned = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
   if (!aligned(p) || !aligned(m) || !aligned(v)) return fail(SP_ERR_SHAPE, "p/m/v must be 16-byte aligned");
+  if (r->shard && p != r->param(r->cfg.rank))
+    return fail(SP_ERR_ARG, "shard_lamb: p must be sp_round_param_ptr() (owners store into every rank's copy)");
   for (int l = 0; l < r->L; ++l) {
     const int g = r->cfg.rank * r->L + l;
     if (!grads[l] && r->weights[g] != 0.0)
@@ -775,6 +843,13 @@ int sp_round_create(const sp_round_cfg* cfg, sp_round** out) {
   }
   r->flags_bytes = 256 + round_up((int64_t)2 * r->G * 8, 256);
   r->shared_bytes = r->flags_bytes + r->ctr_bytes + (size_t)(r->G + 1) * r->buf_bytes;
+  if (cfg->shard_lamb) {  // [params fp32 npad][norm table world x T double2]
+    r->shard = true;
+    r->fused_round = false;
+    r->param_off = r->shared_bytes;
+    r->norms_off = r->param_off + round_up(r->npad * 4, 256);
+    r->shared_bytes = r->norms_off + round_up((int64_t)cfg->world * cfg->num_tensors * 16, 256);
+  }
   int dev_sms = 0;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, cfg->device);
   if (dev_sms > 0) r->sm_count = dev_sms;
@@ -797,7 +872,7 @@ int sp_round_create(const sp_round_cfg* cfg, sp_round** out) {
     const bool unfused = unf && unf[0] == '1';
     if (const char* g = std::getenv("SP_SEG_LAMB_GRID")) r->seg_lamb_grid = std::max(1, std::atoi(g));
     if (const char* x = std::getenv("SP_XCHG_PER_SM")) r->xchg_per_sm = std::max(1, std::atoi(x));
-    r->segments = (cfg->world > 1 && !unfused && !r->fused_round)
+    r->segments = (cfg->world > 1 && !unfused && !r->fused_round && !r->shard)
                       ? std::max(1, std::min(8, seg_env ? std::atoi(seg_env) : 1))
                       : 1;
   }
@@ -1019,6 +1094,8 @@ void* sp_round_wire_ptr(sp_round* r, int local_peer) {
   if (!r || local_peer < 0 || local_peer >= r->L) return nullptr;
   return r->wire(r->cfg.rank, r->cfg.rank * r->L + local_peer);
 }
+
+float* sp_round_param_ptr(sp_round* r) { return r && r->shard ? r->param(r->cfg.rank) : nullptr; }
 
 void* sp_round_avg_ptr(sp_round* r) { return r ? const_cast<char*>(avg_buffer(r)) : nullptr; }
 

@@ -50,7 +50,7 @@ class AveragingRound:
                  q8_block: int = 4096, peers_per_rank: int = 1, rank: int = 0, world: int = 1,
                  device: int | None = None, lr: float = 1.76e-3, betas=(0.9, 0.999),
                  eps: float = 1e-6, weight_decay: float = 0.01, bias_correction: bool = True,
-                 barrier_timeout_s: float = 20.0, process_group=None):
+                 barrier_timeout_s: float = 20.0, process_group=None, shard_lamb: bool = False):
         import torch
 
         if wire not in nat.WIRE_FORMATS:
@@ -69,7 +69,9 @@ class AveragingRound:
             n=self.n, wire=nat.WIRE_FORMATS[wire], q8_block=self.q8_block,
             num_tensors=len(self.tensor_sizes), tensor_sizes=self._sizes, lr=lr,
             beta1=betas[0], beta2=betas[1], eps=eps, weight_decay=weight_decay,
-            bias_correction=int(bool(bias_correction)), barrier_timeout_s=barrier_timeout_s)
+            bias_correction=int(bool(bias_correction)), barrier_timeout_s=barrier_timeout_s,
+            shard_lamb=int(bool(shard_lamb)))
+        self.shard_lamb = bool(shard_lamb)
         self._lib = nat.lib()
         self._h = ctypes.c_void_p()
         nat.check(self._lib.sp_round_create(ctypes.byref(cfg), ctypes.byref(self._h)))
@@ -169,6 +171,29 @@ class AveragingRound:
                                         "data": (int(ptr), False), "version": 3}
 
         return torch.as_tensor(_View(), device=f"cuda:{self.device}")
+
+    def param_buffer(self):
+        """shard_lamb: the flat fp32[n] parameter vector the round updates (a
+        zero-copy torch view of executor memory; pass it as `p`). Owners store
+        their updated ranges into every rank's copy."""
+        import torch
+
+        ptr = self._lib.sp_round_param_ptr(self._h)
+        if not ptr:
+            raise RuntimeError("param_buffer() needs shard_lamb=True")
+
+        class _View:  # __cuda_array_interface__ v3
+            __cuda_array_interface__ = {"shape": (self.n,), "typestr": "<f4",
+                                        "data": (int(ptr), False), "version": 3}
+
+        return torch.as_tensor(_View(), device=f"cuda:{self.device}")
+
+    def own_range(self) -> tuple[int, int]:
+        """[lo, hi) of the flattened vector this rank owns (averages, and with
+        shard_lamb also steps)."""
+        if self.offsets is None:
+            raise RuntimeError("assign() first")
+        return self.offsets[self.rank * self.L], self.offsets[(self.rank + 1) * self.L]
 
     def add_samples(self, local_peer: int, samples: float, buf: int = 0) -> None:
         nat.check(self._lib.sp_round_add_samples(self._h, buf, local_peer, float(samples)))

@@ -37,6 +37,8 @@ def main():
     ap.add_argument("--sizes", default="3,1000,70001,2,4096,131075,5")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--block", type=int, default=4096)
+    ap.add_argument("--shard-lamb", action="store_true",
+                    help="sharded LAMB: owners step their range, parameters pushed to all ranks")
     ap.add_argument("--accumulate", action="store_true",
                     help="device-side accumulation: per-peer micro-batches, sample-count weights")
     args = ap.parse_args()
@@ -55,8 +57,10 @@ def main():
 
     rnd = AveragingRound(n, sizes, wire=wire, q8_block=block, peers_per_rank=L, rank=rank,
                          world=world, device=local, lr=HP["lr"], eps=HP["eps"],
-                         weight_decay=HP["weight_decay"], barrier_timeout_s=30.0)
+                         weight_decay=HP["weight_decay"], barrier_timeout_s=30.0,
+                         shard_lamb=args.shard_lamb)
     rnd.assign(fr, w)
+    lo, hi = rnd.own_range() if args.shard_lamb else (0, n)
     grads = []
     for l in range(L):
         g = rank * L + l
@@ -66,7 +70,7 @@ def main():
         t = torch.empty(n, device="cuda")
         fill_synthetic(t, 21, g, SIGMA)
         grads.append(t)
-    p = torch.empty(n, device="cuda")
+    p = rnd.param_buffer() if args.shard_lamb else torch.empty(n, device="cuda")
     fill_synthetic(p, 22, 0, 0.02, 0)
     m = torch.zeros(n, device="cuda")
     v = torch.zeros(n, device="cuda")
@@ -112,17 +116,20 @@ def main():
             rnd.run(grads, p, m, v, step)
         torch.cuda.synchronize()
         got, gs = rnd.read_wire(nat.SP_BUF_AVG)
-        if not np.array_equal(got, avg):
+        if not np.array_equal(got[lo:hi], avg[lo:hi]):  # sharded: only the owned range is local
             errors.append(f"step {step}: averaged vector differs ({int((got != avg).sum())} elems)")
-        if wire == "q8" and not np.array_equal(gs, avg_s):
+        if wire == "q8" and not np.array_equal(gs[lo // block:(hi + block - 1) // block],
+                                               avg_s[lo // block:(hi + block - 1) // block]):
             errors.append(f"step {step}: averaged q8 scales differ")
         trust = rnd.read_trust()
         O.lamb(wire, avg, avg_s, ph, mh, vh, sizes, HP, step, block, trust_in=trust)
-        for name, dev, host in (("m", m, mh), ("v", v, vh), ("p", p, ph)):
-            if not np.array_equal(dev.cpu().numpy(), host):
+        # sharded: m and v are kept on the owned range, p everywhere
+        for name, dev, host, a, b in (("m", m, mh, lo, hi), ("v", v, vh, lo, hi), ("p", p, ph, 0, n)):
+            if not np.array_equal(dev.cpu().numpy()[a:b], host[a:b]):
                 errors.append(f"step {step}: {name} differs")
     # all replicas identical
-    digest = torch.tensor([float(p.double().sum()), float(m.double().sum())], device="cuda")
+    digest = torch.tensor([float(p.double().sum()),
+                           0.0 if args.shard_lamb else float(m.double().sum())], device="cuda")
     allg = [torch.zeros_like(digest) for _ in range(world)]
     dist.all_gather(allg, digest)
     if any(not torch.equal(allg[0], x) for x in allg):

@@ -77,3 +77,21 @@ def test_device_accumulation_multi_gpu(wire):
     """Micro-batches accumulated on each GPU; sample counts published over
     NVLink weight the average; buffers alternate per step (DPU)."""
     _launch(NGPU, "--wire", wire, "--peers-per-rank", "2", "--accumulate")
+
+
+@pytest.mark.parametrize("wire", ["fp32", "fp16", "q8"])
+def test_sharded_lamb(wire):
+    """ZeRO-1 style LAMB: owners step their range; per-tensor
+    norms cross NVLink; parameters pushed to every rank. p bit-exact on every
+    rank given the device trust; m, v bit-exact on the owned range."""
+    _launch(NGPU, "--wire", wire, "--shard-lamb")
+
+
+def test_sharded_lamb_ragged_owners():
+    # a rank that owns nothing (zero-length parts) still publishes zero norms
+    # and receives every parameter
+    fr = [0.0] * NGPU
+    fr[-1] = 0.6
+    fr[0] = 0.4
+    _launch(NGPU, "--wire", "fp16", "--shard-lamb", "--fractions", ",".join(map(str, fr)))
+    _launch(NGPU, "--wire", "q8", "--shard-lamb", "--peers-per-rank", "2", "--accumulate")

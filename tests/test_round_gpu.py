@@ -32,7 +32,8 @@ def _dev(x):
     return torch.from_numpy(x).cuda()
 
 
-def _run_case(wire, fractions, weights, sizes, steps=1, block=4096, warm=False, seed=11):
+def _run_case(wire, fractions, weights, sizes, steps=1, block=4096, warm=False, seed=11,
+              shard=False):
     G = len(fractions)
     n = sum(sizes)
     grads_h = [O.fill_synthetic(n, seed, g, SIGMA) for g in range(G)]
@@ -54,7 +55,11 @@ def _run_case(wire, fractions, weights, sizes, steps=1, block=4096, warm=False, 
     p_d, m_d, v_d = _dev(p_h.copy()), _dev(m_h.copy()), _dev(v_h.copy())
     rnd = AveragingRound(n, sizes, wire=wire, q8_block=block, peers_per_rank=G,
                          lr=HP["lr"], betas=(HP["beta1"], HP["beta2"]), eps=HP["eps"],
-                         weight_decay=HP["weight_decay"])
+                         weight_decay=HP["weight_decay"], shard_lamb=shard)
+    if shard:  # the round owns the flat parameter vector
+        pb = rnd.param_buffer()
+        pb.copy_(p_d)
+        p_d = pb
     offs = rnd.assign(fractions, weights)
     assert offs[0] == 0 and offs[-1] == n
 
@@ -103,6 +108,31 @@ def _run_case(wire, fractions, weights, sizes, steps=1, block=4096, warm=False, 
 ])
 def test_round_parity_ragged(wire, fractions, weights):
     _run_case(wire, fractions, weights, RAGGED, block=4096 if wire != "q8" else 4096)
+
+
+@pytest.mark.parametrize("wire", ["fp32", "fp16", "q8"])
+def test_round_parity_sharded_lamb_one_rank(wire):
+    # shard_lamb on one rank: the owned range is the whole vector; exercises
+    # the norm table, rank-ordered trust and the parameter push kernels
+    _run_case(wire, [0.25, 0.25, 0.25, 0.25], [5.0, 0.0, 3.0, 8.0], RAGGED, steps=3, warm=True,
+              shard=True)
+
+
+def test_sharded_lamb_requires_param_buffer():
+    n = sum(RAGGED)
+    rnd = AveragingRound(n, RAGGED, wire="fp16", shard_lamb=True)
+    rnd.assign([1.0], [1.0])
+    g = torch.zeros(n, device="cuda")
+    p, m, v = torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda")
+    with pytest.raises(ValueError, match="param_ptr"):
+        rnd.run([g], p, m, v, 1)
+    rnd.run([g], rnd.param_buffer(), m, v, 1)
+    torch.cuda.synchronize()
+    rnd.close()
+    r2 = AveragingRound(n, RAGGED, wire="fp16")
+    with pytest.raises(RuntimeError):
+        r2.param_buffer()
+    r2.close()
 
 
 @pytest.mark.parametrize("wire", ["fp16", "q8"])
