@@ -39,6 +39,12 @@ struct SimConfig {
   int group_size = 0;
   int ps_server = -1;
   unsigned long seed = 1;
+  // Measured executor round times in seconds, indexed by Algorithm
+  // (AllReduce, ParameterServer, Adaptive); 0 keeps the fluid model. When
+  // set, the measured time replaces the model's comm_s (reference
+  // netsim.cpp:146-201) and round_s in compare_strategies,
+  // e.g. times from paper_2106_10207_b200.measure.measure_round_times().
+  double measured_round_s[3] = {0.0, 0.0, 0.0};
 };
 
 // Seconds for one averaging round over the whole fleet; `server` applies to

@@ -6,6 +6,8 @@
 // The GPU round itself is driven from Python through the C-ABI
 // (paper_2106_10207_b200/round.py); the GIL is released around solves.
 
+#include <map>
+
 #include <pybind11/numpy.h>
 #include <pybind11/pybind11.h>
 #include <pybind11/stl.h>
@@ -122,12 +124,15 @@ PYBIND11_MODULE(_swarmplan, m) {
         py::arg("spec_json"), py::arg("algorithm"), py::arg("server") = -1,
         "Seconds for one averaging round (allreduce, parameter_server or adaptive).");
   m.def("compare_strategies",
-        [](const std::string& spec_json) {
+        [](const std::string& spec_json, std::map<std::string, double> measured) {
           CollaborationSpec spec = spec_from_json(spec_json);
+          netsim::SimConfig cfg;
+          for (const auto& [name, sec] : measured)
+            cfg.measured_round_s[static_cast<int>(netsim::algorithm_from_name(name))] = sec;
           std::vector<netsim::StrategyComparison> rows;
           {
             py::gil_scoped_release release;
-            rows = netsim::compare_strategies(spec);
+            rows = netsim::compare_strategies(spec, cfg);
           }
           py::list out;
           for (const auto& c : rows) {
@@ -139,7 +144,9 @@ PYBIND11_MODULE(_swarmplan, m) {
           }
           return out;
         },
-        py::arg("spec_json"));
+        py::arg("spec_json"), py::arg("measured") = std::map<std::string, double>{},
+        "Static-fleet round time and steps/hour per algorithm; `measured` maps algorithm "
+        "names to executor round times (s) that replace the fluid model's comm time.");
   m.def("build_plan", [](int n, int msize) { return groups::build_plan(n, msize).rounds; },
         py::arg("n"), py::arg("m"));
   m.def("expected_iterations", &groups::expected_iterations, py::arg("n"), py::arg("m"), py::arg("p"));

@@ -81,6 +81,12 @@ struct Timing {
   double compute_s = 0.0, comm_s = 0.0;
 };
 
+double measured(const SimConfig& cfg, Algorithm alg) {
+  const double m = cfg.measured_round_s[static_cast<int>(alg)];
+  if (m < 0.0 || !std::isfinite(m)) throw std::invalid_argument("measured round time must be finite and >= 0");
+  return m;
+}
+
 Timing static_timing(const CollaborationSpec& spec, const SimConfig& cfg) {
   Timing t;
   double rate = 0.0;
@@ -113,6 +119,7 @@ Timing static_timing(const CollaborationSpec& spec, const SimConfig& cfg) {
       }
     }
   }
+  if (const double m = measured(cfg, cfg.algorithm); m > 0.0) t.comm_s = m;
   return t;
 }
 
@@ -137,7 +144,8 @@ std::vector<StrategyComparison> compare_strategies(const CollaborationSpec& spec
     const Timing tm = static_timing(spec, cfg);
     StrategyComparison c;
     c.algorithm = alg;
-    c.round_s = simulate_averaging(spec, alg, config.ps_server);
+    const double m = measured(config, alg);
+    c.round_s = m > 0.0 ? m : simulate_averaging(spec, alg, config.ps_server);
     const double step = config.delay_parameter_updates ? std::max(tm.compute_s, tm.comm_s)
                                                        : tm.compute_s + tm.comm_s;
     c.steps_per_hour = step > 0 ? 3600.0 / step : 0.0;

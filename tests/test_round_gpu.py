@@ -290,3 +290,20 @@ def test_device_accumulation_weighted_by_sample_counts(wire):
     rnd.add_samples(0, 6.0, buf=1)
     assert rnd.samples(0, buf=1) == 6.0
     rnd.close()
+
+
+def test_measured_round_times_feed_compare_strategies():
+    # each algorithm's partition run on the executor and timed
+    import json
+
+    from golden.fleets import spec
+    from paper_2106_10207_b200.measure import compare_strategies_measured
+
+    s = spec("het4b")
+    s["param_count"] = 1_000_000
+    rows = {r["algorithm"]: r for r in compare_strategies_measured(json.dumps(s), steps=5)}
+    assert set(rows) == {"allreduce", "parameter_server", "adaptive"}
+    for r in rows.values():
+        assert 0 < r["measured_round_s"] < 0.1
+        assert r["round_s"] == r["measured_round_s"]
+        assert r["steps_per_hour"] > 0

@@ -266,3 +266,33 @@ def test_highs_oracle_agrees(name):
     assert s["steps_per_sec"] == pytest.approx(xi_h, rel=1e-9)
     if name in FRACTIONS_APPENDIX_A or name in ("homogeneous8", "aux_server"):
         np.testing.assert_allclose(s["fractions"], fr_h, atol=1e-6)
+
+
+def test_compare_strategies_with_measured_round_times():
+    # executor round times replace the fluid model's comm time
+    sj = spec_json("het4b")
+    model = {r["algorithm"]: r for r in sp.compare_strategies(sj)}
+    meas = {"allreduce": 2e-4, "parameter_server": 5e-4, "adaptive": 1e-4}
+    rows = {r["algorithm"]: r for r in sp.compare_strategies(sj, meas)}
+    spec = json.loads(sj)
+    compute_s = spec["batch_size"] / sum(p["samples_per_sec"] for p in spec["peers"])
+    for alg, sec in meas.items():
+        assert rows[alg]["round_s"] == sec
+        if alg != "adaptive":  # adaptive's compute uses duty-cycled rates
+            assert rows[alg]["steps_per_hour"] == pytest.approx(3600.0 / max(compute_s, sec))
+    # a partial map keeps the model for the rest
+    part = {r["algorithm"]: r for r in sp.compare_strategies(sj, {"adaptive": 1e-4})}
+    assert part["allreduce"] == model["allreduce"]
+    with pytest.raises(ValueError):
+        sp.compare_strategies(sj, {"gossip": 1.0})
+    with pytest.raises(ValueError):
+        sp.compare_strategies(sj, {"adaptive": -1.0})
+
+
+def test_measured_fractions_per_algorithm():
+    from paper_2106_10207_b200.measure import fractions_for
+
+    sj = spec_json("het4b")
+    assert fractions_for(sj, "allreduce") == [0.25] * 4
+    assert fractions_for(sj, "parameter_server") == [0.0, 0.0, 0.0, 1.0]
+    np.testing.assert_allclose(fractions_for(sj, "adaptive"), [1 / 22] * 3 + [19 / 22], atol=1e-9)
