@@ -202,7 +202,12 @@ class AveragingRound:
         return float(self._lib.sp_round_samples(self._h, buf, local_peer))
 
     def run_accumulated(self, p, m, v, step: int, buf: int = 0, stream=None) -> None:
-        """Round over the accumulators of `buf`, weighted by their sample counts."""
+        """Round over the accumulators of `buf`, weighted by their sample counts.
+
+        DPU (delayed parameter updates): step s+1 may
+        accumulate into the other buffer on another stream while this round
+        runs; order that stream after the round that last read the buffer it
+        writes (an event recorded after run_accumulated(..., buf=b))."""
         st = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
         nat.check(self._lib.sp_round_run_accumulated(self._h, buf, self._dptr(p, self.n),
                                                      self._dptr(m, self.n), self._dptr(v, self.n),

@@ -307,3 +307,55 @@ def test_measured_round_times_feed_compare_strategies():
         assert 0 < r["measured_round_s"] < 0.1
         assert r["round_s"] == r["measured_round_s"]
         assert r["steps_per_hour"] > 0
+
+
+@pytest.mark.parametrize("wire", ["fp16", "q8"])
+def test_dpu_overlap_accumulate_during_round(wire):
+    """SURVEY §8f N4 (the reference models it as
+    max(compute, comm), netsim.cpp:291-293): step s's round runs on one
+    stream while step s+1's micro-batches accumulate into the other buffer on
+    a second stream. The result is bit-identical to the serial schedule."""
+    sizes = RAGGED
+    n = sum(sizes)
+    G, steps = 2, 4
+    micro = {(s, g, k): _dev(_micro(n, s, g, k)) for s in range(1, steps + 2) for g in range(G)
+             for k in range(g + 1)}
+    torch.cuda.synchronize()
+
+    def fresh():
+        rnd = AveragingRound(n, sizes, wire=wire, peers_per_rank=G, lr=HP["lr"], eps=HP["eps"],
+                             weight_decay=HP["weight_decay"])
+        rnd.assign([0.5, 0.5], [1.0, 1.0])
+        p = _dev(O.fill_synthetic(n, 2, 0, 0.02, 0))
+        return rnd, p, torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda")
+
+    def acc(rnd, s, stream):
+        for g in range(G):
+            for k in range(g + 1):
+                rnd.accumulate(g, micro[(s, g, k)], 4.0 + g, buf=s % 2, stream=stream)
+
+    # serial: accumulate, then round, one stream
+    rnd, p1, m1, v1 = fresh()
+    for s in range(1, steps + 1):
+        acc(rnd, s, None)
+        rnd.run_accumulated(p1, m1, v1, s, buf=s % 2)
+    torch.cuda.synchronize()
+    rnd.close()
+    # overlapped: round s on stream A || accumulation of s+1 on stream B
+    rnd, p2, m2, v2 = fresh()
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    acc(rnd, 1, sb)
+    done = {}
+    for s in range(1, steps + 1):
+        sa.wait_stream(sb)  # step s's accumulators are complete
+        rnd.run_accumulated(p2, m2, v2, s, buf=s % 2, stream=sa)
+        done[s] = torch.cuda.Event()
+        done[s].record(sa)
+        if s < steps:
+            if s - 1 in done:  # round s-1 has finished reading the buffer s+1 reuses
+                sb.wait_event(done[s - 1])
+            acc(rnd, s + 1, sb)  # the other buffer, concurrently with round s
+    torch.cuda.synchronize()
+    rnd.close()
+    for a, b in ((p1, p2), (m1, m2), (v1, v2)):
+        assert torch.equal(a, b)
