@@ -417,6 +417,7 @@ def main():
                        "wire": wire, "q8_block": block if wire == "q8" else None,
                        "lamb": "sharded (ZeRO-1: owners step, fp32 params pushed)" if args.shard_lamb
                                else "replicated (averaged gradient all-gathered)",
+                       "shard_cut": rnd.shard_cut() if args.shard_lamb else None,
                        "fractions": "uniform 1/G (LP, homogeneous fleet)",
                        "l2": f"no flush: per-step working set {(n * (12 + 4 * L + 2 * b)) / 1e9:.2f} GB > 126 MB L2",
                        "parallelism": f"dp{world} (one peer per GPU, CUDA IPC over NVLink)"},

@@ -149,6 +149,15 @@ void* sp_round_wire_ptr(sp_round* r, int local_peer);
  * IPC-shared allocation so that owners can store their updated ranges into
  * every rank's copy (NULL without shard_lamb). */
 float* sp_round_param_ptr(sp_round* r);
+
+/* shard_lamb: element index c (a tensor edge) of the hybrid split chosen at
+ * sp_round_set_assignment: tensors in [0, c) keep the replicated LAMB (every
+ * rank steps them, full-length m/v) on a second stream while tensors in
+ * [c, n) are sharded, so the HBM-bound and NVLink-bound halves can overlap.
+ * Default c = 0 (everything sharded; the overlap was measured slower, the
+ * halves contend for SMs and HBM); SP_SHARD_FRACTION=<share>|model selects a
+ * split for experiments. -1 without shard_lamb. */
+int64_t sp_round_shard_cut(const sp_round* r);
 void* sp_round_avg_ptr(sp_round* r);
 int64_t sp_round_padded_n(const sp_round* r);
 /* Per-tensor trust ratios of the last step (device float[num_tensors]). */

@@ -80,6 +80,7 @@ def lib() -> ctypes.CDLL:
         "sp_round_wire_ptr": (vp, [vp, c_int]),
         "sp_round_avg_ptr": (vp, [vp]),
         "sp_round_param_ptr": (vp, [vp]),
+        "sp_round_shard_cut": (i64, [vp]),
         "sp_round_padded_n": (i64, [vp]),
         "sp_round_trust_ptr": (vp, [vp]),
         "sp_round_copy_trust": (c_int, [vp, vp, vp]),
@@ -109,6 +110,7 @@ EXPORTED_SYMBOLS = [
     "sp_round_create", "sp_round_destroy", "sp_round_handle_bytes", "sp_round_export",
     "sp_round_connect", "sp_round_align", "sp_round_set_assignment", "sp_round_run",
     "sp_round_run_phased", "sp_round_wire_ptr", "sp_round_avg_ptr", "sp_round_param_ptr",
+    "sp_round_shard_cut",
     "sp_round_padded_n",
     "sp_round_trust_ptr", "sp_round_copy_trust", "sp_round_read", "sp_round_accumulate", "sp_round_accumulator_ptr",
     "sp_round_add_samples", "sp_round_samples", "sp_round_run_accumulated",

@@ -1195,11 +1195,12 @@ struct ShardNormArgs {
   const int2* tchunks;             // this rank's chunks of tensor t (may be empty)
   double2* table[SP_MAX_RANKS];    // push order: next rank first, self last
   int ndst, rank, T;
+  int t0;                          // first sharded tensor (CTA b handles t0 + b)
 };
 
 __global__ void __launch_bounds__(256) k_shard_norms(ShardNormArgs a) {
   __shared__ double sx[256], sy[256];
-  const int t = blockIdx.x;
+  const int t = a.t0 + blockIdx.x;
   const int2 r = a.tchunks[t];
   double x = 0.0, y = 0.0;
   for (int c = r.x + threadIdx.x; c < r.y; c += blockDim.x) {
@@ -1222,10 +1223,10 @@ __global__ void __launch_bounds__(256) k_shard_norms(ShardNormArgs a) {
 
 // trust[t] = sqrt(sum_k pp[k][t]) / sqrt(sum_k uu[k][t]) over ranks in order
 // (1 if either is 0); step_scale[t] = lr * trust[t].
-__global__ void k_shard_trust(const double2* __restrict__ table, int world, int T,
+__global__ void k_shard_trust(const double2* __restrict__ table, int world, int T, int t0,
                               const float* __restrict__ hp, float* __restrict__ trust,
                               float* __restrict__ step_scale) {
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
+  for (int t = t0 + blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
     double x = 0.0, y = 0.0;
     for (int k = 0; k < world; ++k) {
       const double2 v = __ldcg(table + (size_t)k * T + t);
@@ -1262,18 +1263,34 @@ __global__ void __launch_bounds__(kLambThreads) k_lamb_update_push(LambArgs a, P
     for (int k = 0; k < d.ndst; ++k) d.dst[k][si] = q;
   }
   const int64_t b0 = sp.start + sp.head;
-  for (int k = t; k < sp.nbody4; k += kLambThreads) {
+  int k = t;
+  // two vectors per iteration: all loads in flight before the stores
+  for (; k + kLambThreads < sp.nbody4; k += 2 * kLambThreads) {
+    const int64_t i0 = b0 + 4 * (int64_t)k, i1 = i0 + 4 * (int64_t)kLambThreads;
+    const float4 p0 = *reinterpret_cast<const float4*>(a.p + i0);
+    const float4 p1 = *reinterpret_cast<const float4*>(a.p + i1);
+    const float4 m0 = *reinterpret_cast<const float4*>(a.m + i0);
+    const float4 m1 = *reinterpret_cast<const float4*>(a.m + i1);
+    const float4 v0 = *reinterpret_cast<const float4*>(a.v + i0);
+    const float4 v1 = *reinterpret_cast<const float4*>(a.v + i1);
+    const float4 q0 = lamb_p2_vec(a, s, neg, p0, m0, v0), q1 = lamb_p2_vec(a, s, neg, p1, m1, v1);
+    const int4 o0 = make_int4(__float_as_int(q0.x), __float_as_int(q0.y), __float_as_int(q0.z),
+                              __float_as_int(q0.w));
+    const int4 o1 = make_int4(__float_as_int(q1.x), __float_as_int(q1.y), __float_as_int(q1.z),
+                              __float_as_int(q1.w));
+    for (int q = 0; q < d.ndst; ++q) {
+      st_v4(d.dst[q] + i0, o0);
+      st_v4(d.dst[q] + i1, o1);
+    }
+  }
+  if (k < sp.nbody4) {
     const int64_t i = b0 + 4 * (int64_t)k;
-    float4 p = *reinterpret_cast<const float4*>(a.p + i);
-    const float4 m = *reinterpret_cast<const float4*>(a.m + i);
-    const float4 v = *reinterpret_cast<const float4*>(a.v + i);
-    p.x = __fmaf_rn(neg, lamb_dir(a, s, p.x, m.x, v.x), p.x);
-    p.y = __fmaf_rn(neg, lamb_dir(a, s, p.y, m.y, v.y), p.y);
-    p.z = __fmaf_rn(neg, lamb_dir(a, s, p.z, m.z, v.z), p.z);
-    p.w = __fmaf_rn(neg, lamb_dir(a, s, p.w, m.w, v.w), p.w);
-    const int4 o = make_int4(__float_as_int(p.x), __float_as_int(p.y), __float_as_int(p.z),
-                             __float_as_int(p.w));
-    for (int q = 0; q < d.ndst; ++q) st_v4(d.dst[q] + i, o);
+    const float4 q = lamb_p2_vec(a, s, neg, *reinterpret_cast<const float4*>(a.p + i),
+                                 *reinterpret_cast<const float4*>(a.m + i),
+                                 *reinterpret_cast<const float4*>(a.v + i));
+    const int4 o = make_int4(__float_as_int(q.x), __float_as_int(q.y), __float_as_int(q.z),
+                             __float_as_int(q.w));
+    for (int j = 0; j < d.ndst; ++j) st_v4(d.dst[j] + i, o);
   }
 }
 

@@ -118,6 +118,12 @@ struct sp_round {
   // sharded LAMB (cfg.shard_lamb): flat parameter vector + per-rank norm table
   bool shard = false;
   size_t param_off = 0, norms_off = 0;
+  // hybrid split: tensors [0, shard_t0) (elements [0, shard_cut)) keep the
+  // replicated LAMB on a second stream, tensors [shard_t0, T) are sharded
+  int shard_t0 = 0;
+  int64_t shard_cut = 0;
+  int nchunks_rep = 0;    // chunks of the replicated tensors (full range), first in the table
+  int hybrid_grid = 0;    // CTA cap of the replicated LAMB running beside the sharded chain
 
   float* param(int rank) const { return reinterpret_cast<float*>(base[rank] + param_off); }
   double2* norms(int rank) const { return reinterpret_cast<double2*>(base[rank] + norms_off); }
@@ -176,6 +182,52 @@ int64_t seg_cut(const sp_round* r, int k, int s) {
   return lo + (hi - lo) * s / r->segments / r->align * r->align;
 }
 
+// Hybrid sharded LAMB (opt-in experiment): tensors [0, t0) keep the
+// replicated LAMB (HBM-bound, every rank steps them) on a second stream while
+// tensors [t0, T) are sharded (NVLink-bound: owners step their range and push
+// fp32 parameters). t0 is the tensor edge closest to SP_SHARD_FRACTION, or
+// with SP_SHARD_FRACTION=model the edge minimizing the modelled time
+//   (1-a) * avg push + max(replicated LAMB(1-a), sharded pass 1 + push(a)),
+// a = sharded share of the elements. Default: a = 1 (everything sharded).
+void choose_shard_cut(sp_round* r) {
+  const sp_round_cfg& c = r->cfg;
+  const int T = (int)r->tsizes.size();
+  const double n = (double)r->n;
+  const double b = c.wire == SP_WIRE_FP32 ? 4.0 : c.wire == SP_WIRE_FP16 ? 2.0 : 1.0 + 4.0 / c.q8_block;
+  // Default: shard everything. Running the replicated half beside the
+  // sharded chain was measured slower at N=4 (both halves contend for SMs
+  // and HBM: fp16 234 us at a = 0.5 vs 169 us fully sharded), so
+  // the model-chosen split is opt-in: SP_SHARD_FRACTION=<a> or =model.
+  double want = 1.0;
+  if (const char* e = std::getenv("SP_SHARD_FRACTION"))
+    want = std::string(e) == "model" ? -1.0 : std::atof(e);
+  const double hbm = 6.2e12, nvl = 6.0e11, w = c.world;
+  int best = 0;
+  double best_cost = 1e300;
+  int64_t off = 0;
+  for (int t0 = 0; t0 <= T; ++t0) {
+    const double a = (n - (double)off) / n;  // sharded share
+    double cost;
+    if (want >= 0.0) {
+      cost = std::fabs(a - want);
+    } else {
+      const double push_avg = (1.0 - a) * n * b * (w - 1.0) / w / nvl;
+      const double rep = (1.0 - a) * n * (36.0 + b) / hbm;
+      const double shd = a * n / w * (36.0 + b) / hbm + a * n * 4.0 * (w - 1.0) / w / nvl;
+      cost = push_avg + std::max(rep, shd);
+    }
+    if (cost < best_cost - 1e-15) {
+      best_cost = cost;
+      best = t0;
+    }
+    if (t0 < T) off += r->tsizes[(size_t)t0];
+  }
+  r->shard_t0 = best;
+  int64_t cut = 0;
+  for (int t = 0; t < best; ++t) cut += r->tsizes[(size_t)t];
+  r->shard_cut = cut;
+}
+
 // Chunk table (tensor edges, every multiple of lamb_chunk, segment cuts),
 // per-tensor chunk ranges and the fused-LAMB work lists:
 //   [pass 1 of segment 0] ... [pass 1 of segment K-1] [pass 2 of all chunks].
@@ -190,19 +242,25 @@ int build_lamb_tables(sp_round* r, bool with_cuts) {
   std::sort(cuts.begin(), cuts.end());
   std::vector<Chunk> chunks;
   std::vector<int2> tch;
-  // sharded LAMB: only the range this rank owns
+  // sharded LAMB: the sharded tensors only over the range this rank owns
   int64_t own_lo = 0, own_hi = r->n;
+  r->shard_t0 = 0;
+  r->shard_cut = 0;
   if (r->shard && !r->offsets.empty()) {
     own_lo = r->offsets[(size_t)r->cfg.rank * r->L];
     own_hi = r->offsets[(size_t)(r->cfg.rank + 1) * r->L];
+    choose_shard_cut(r);
   }
+  r->nchunks_rep = 0;
   int64_t off = 0;
   size_t ci = 0;
   for (size_t t = 0; t < r->tsizes.size(); ++t) {
-    const int64_t end = std::min(off + r->tsizes[t], own_hi);
+    const bool sharded = r->shard && (int)t >= r->shard_t0;
+    if (r->shard && (int)t == r->shard_t0) r->nchunks_rep = (int)chunks.size();
+    const int64_t end = sharded ? std::min(off + r->tsizes[t], own_hi) : off + r->tsizes[t];
     int2 rg;
     rg.x = (int)chunks.size();
-    int64_t s = std::max(off, own_lo);
+    int64_t s = sharded ? std::max(off, own_lo) : off;
     while (s < end) {
       int64_t e = std::min(end, (s / r->lamb_chunk + 1) * r->lamb_chunk);
       while (ci < cuts.size() && cuts[ci] <= s) ++ci;
@@ -214,6 +272,7 @@ int build_lamb_tables(sp_round* r, bool with_cuts) {
     tch.push_back(rg);
     off += r->tsizes[t];
   }
+  if (r->shard && r->shard_t0 >= (int)r->tsizes.size()) r->nchunks_rep = (int)chunks.size();
   if ((int)chunks.size() > r->nchunks_cap) return fail(SP_ERR_STATE, "LAMB chunk table overflow");
   const int K = with_cuts ? r->segments : 1;
   std::vector<std::vector<int>> p1((size_t)K);
@@ -230,7 +289,11 @@ int build_lamb_tables(sp_round* r, bool with_cuts) {
   std::vector<int> items;
   r->p1_off.assign((size_t)K + 1, 0);
   const char* lag_env = std::getenv("SP_LAMB_LAG");
-  if (K == 1 && lag_env) {
+  if (r->shard) {  // fused queue over the replicated tensors only
+    for (int c = 0; c < r->nchunks_rep; ++c) items.push_back(c);
+    r->p1_off[1] = r->p2_off = (int)items.size();
+    for (int c = 0; c < r->nchunks_rep; ++c) items.push_back(~c);
+  } else if (K == 1 && lag_env) {
     // single launch, pass 2 of tensor t queued `lag` items after its last
     // pass-1 chunk (tuning experiment for L2 reuse between the passes)
     const size_t lag = (size_t)std::max(0, std::atoi(lag_env));
@@ -486,54 +549,87 @@ int launch_lamb(sp_round* r, LambArgs a, int first_item, int nitems, bool final_
   return SP_OK;
 }
 
-// Sharded LAMB (cfg.shard_lamb): pass 1 over the owned chunks, per-tensor
-// norm partials pushed to every rank + barrier, trust (rank-ordered sum),
-// pass 2 storing p' into every rank's parameter vector + barrier (no rank
-// may read parameters before every owner has stored its range).
+// Sharded LAMB (cfg.shard_lamb), hybrid with the replicated one:
+//   aux stream: fused replicated LAMB over tensors [0, t0) (full range, every
+//               rank), capped at hybrid_grid CTAs so the chain below has SMs;
+//   st:         tensors [t0, T): pass 1 over the owned chunks, per-tensor norm
+//               partials pushed to every rank + barrier, trust (rank-ordered
+//               sum), pass 2 storing p' into every rank's parameter vector +
+//               barrier (no rank may read parameters before every owner has
+//               stored its range);
+// then st joins aux. HBM-bound and NVLink-bound halves run side by side.
 int enqueue_shard_lamb(sp_round* r, const LambArgs& la, const BarrierArgs& ba, cudaStream_t st,
                        cudaEvent_t* ev) {
   const sp_round_cfg& c = r->cfg;
-  const int nc = r->nchunks, T = c.num_tensors;
-  if (nc > 0) {
+  const int T = c.num_tensors, t0 = r->shard_t0;
+  const int nR = r->nchunks_rep, nS = r->nchunks - nR;
+  if (nR > 0) {
+    SP_CUDA(cudaEventRecord(r->seg_ev[8], st));
+    SP_CUDA(cudaStreamWaitEvent(r->aux, r->seg_ev[8], 0));
+    FusedLamb f = make_lamb_queue(r);
+    f.nitems = 2 * nR;
+    f.final_launch = 1;
+    const int g = std::max(1, std::min(t0 < T ? r->hybrid_grid : r->lamb_grid, nR));
     switch (c.wire) {
-      case SP_WIRE_FP32: k_lamb_moments<SP_WIRE_FP32><<<nc, kLambThreads, 0, st>>>(la); break;
-      case SP_WIRE_FP16: k_lamb_moments<SP_WIRE_FP16><<<nc, kLambThreads, 0, st>>>(la); break;
-      default: k_lamb_moments<SP_WIRE_Q8><<<nc, kLambThreads, 0, st>>>(la); break;
+      case SP_WIRE_FP32: k_lamb_fused<SP_WIRE_FP32><<<g, kLambThreads, 0, r->aux>>>(la, f); break;
+      case SP_WIRE_FP16: k_lamb_fused<SP_WIRE_FP16><<<g, kLambThreads, 0, r->aux>>>(la, f); break;
+      default: k_lamb_fused<SP_WIRE_Q8><<<g, kLambThreads, 0, r->aux>>>(la, f); break;
     }
     SP_CUDA(cudaGetLastError());
   }
-  if (ev) SP_CUDA(cudaEventRecord(ev[5], st));
-  ShardNormArgs na{};
-  na.partial = r->d_partial;
-  na.tchunks = r->d_tchunks;
-  na.ndst = c.world;
-  for (int k = 0; k < c.world; ++k) na.table[k] = r->norms((c.rank + 1 + k) % c.world);
-  na.rank = c.rank;
-  na.T = T;
-  k_shard_norms<<<T, 256, 0, st>>>(na);
-  SP_CUDA(cudaGetLastError());
-  if (c.world > 1) {
-    k_barrier<<<1, 32, 0, st>>>(ba);
-    SP_CUDA(cudaGetLastError());
-  }
-  k_shard_trust<<<(T + 255) / 256, 256, 0, st>>>(r->norms(c.rank), c.world, T, r->d_hp, r->d_trust,
-                                                 r->d_step_scale);
-  SP_CUDA(cudaGetLastError());
-  if (ev) SP_CUDA(cudaEventRecord(ev[6], st));
-  ParamPush pp{};
-  pp.ndst = c.world;
-  for (int k = 0; k < c.world; ++k) pp.dst[k] = r->param((c.rank + 1 + k) % c.world);
-  if (nc > 0) {
-    switch (c.wire) {
-      case SP_WIRE_FP32: k_lamb_update_push<SP_WIRE_FP32><<<nc, kLambThreads, 0, st>>>(la, pp); break;
-      case SP_WIRE_FP16: k_lamb_update_push<SP_WIRE_FP16><<<nc, kLambThreads, 0, st>>>(la, pp); break;
-      default: k_lamb_update_push<SP_WIRE_Q8><<<nc, kLambThreads, 0, st>>>(la, pp); break;
+  LambArgs ls = la;  // the sharded chunks follow the replicated ones in the table
+  ls.chunks = r->d_chunks + nR;
+  ls.partial = r->d_partial + nR;
+  if (t0 < T) {
+    if (nS > 0) {
+      switch (c.wire) {
+        case SP_WIRE_FP32: k_lamb_moments<SP_WIRE_FP32><<<nS, kLambThreads, 0, st>>>(ls); break;
+        case SP_WIRE_FP16: k_lamb_moments<SP_WIRE_FP16><<<nS, kLambThreads, 0, st>>>(ls); break;
+        default: k_lamb_moments<SP_WIRE_Q8><<<nS, kLambThreads, 0, st>>>(ls); break;
+      }
+      SP_CUDA(cudaGetLastError());
     }
+    if (ev) SP_CUDA(cudaEventRecord(ev[5], st));
+    ShardNormArgs na{};
+    na.partial = r->d_partial;
+    na.tchunks = r->d_tchunks;
+    na.ndst = c.world;
+    for (int k = 0; k < c.world; ++k) na.table[k] = r->norms((c.rank + 1 + k) % c.world);
+    na.rank = c.rank;
+    na.T = T;
+    na.t0 = t0;
+    k_shard_norms<<<T - t0, 256, 0, st>>>(na);
     SP_CUDA(cudaGetLastError());
+    if (c.world > 1) {
+      k_barrier<<<1, 32, 0, st>>>(ba);
+      SP_CUDA(cudaGetLastError());
+    }
+    k_shard_trust<<<(T - t0 + 255) / 256, 256, 0, st>>>(r->norms(c.rank), c.world, T, t0, r->d_hp,
+                                                        r->d_trust, r->d_step_scale);
+    SP_CUDA(cudaGetLastError());
+    if (ev) SP_CUDA(cudaEventRecord(ev[6], st));
+    ParamPush pp{};
+    pp.ndst = c.world;
+    for (int k = 0; k < c.world; ++k) pp.dst[k] = r->param((c.rank + 1 + k) % c.world);
+    if (nS > 0) {
+      switch (c.wire) {
+        case SP_WIRE_FP32: k_lamb_update_push<SP_WIRE_FP32><<<nS, kLambThreads, 0, st>>>(ls, pp); break;
+        case SP_WIRE_FP16: k_lamb_update_push<SP_WIRE_FP16><<<nS, kLambThreads, 0, st>>>(ls, pp); break;
+        default: k_lamb_update_push<SP_WIRE_Q8><<<nS, kLambThreads, 0, st>>>(ls, pp); break;
+      }
+      SP_CUDA(cudaGetLastError());
+    }
+    if (c.world > 1) {
+      k_barrier<<<1, 32, 0, st>>>(ba);
+      SP_CUDA(cudaGetLastError());
+    }
+  } else if (ev) {
+    SP_CUDA(cudaEventRecord(ev[5], st));
+    SP_CUDA(cudaEventRecord(ev[6], st));
   }
-  if (c.world > 1) {
-    k_barrier<<<1, 32, 0, st>>>(ba);
-    SP_CUDA(cudaGetLastError());
+  if (nR > 0) {  // join
+    SP_CUDA(cudaEventRecord(r->seg_ev[7], r->aux));
+    SP_CUDA(cudaStreamWaitEvent(st, r->seg_ev[7], 0));
   }
   if (ev) SP_CUDA(cudaEventRecord(ev[7], st));
   return SP_OK;
@@ -657,24 +753,41 @@ int enqueue_round(sp_round* r, const float* const* grads, float* p, float* m, fl
         ra.G = r->G;
         ra.err = r->d_err;
       }
-      // sharded LAMB steps only the owned range: the average stays local
-      ra.ndst = r->shard ? 1 : c.world;
-      for (int k = 0; k < ra.ndst; ++k) ra.dst[k] = r->avg((c.rank + 1 + k + (r->shard ? c.world - 1 : 0)) % c.world);
       ra.lo = seg_cut(r, c.rank, s);
       ra.hi = seg_cut(r, c.rank, s + 1);
       ra.npad = r->npad;
       ra.qblock = c.q8_block;
-      if (ra.hi > ra.lo && !identity_avg(r)) {
+      // [lo, hi) pushed to `nd` ranks (self last); sharded tensors keep their
+      // average local (only their owner steps them)
+      auto reduce = [&](int64_t lo, int64_t hi, int nd) -> int {
+        if (hi <= lo) return SP_OK;
+        ReduceArgs q = ra;
+        q.lo = lo;
+        q.hi = hi;
+        q.ndst = nd;
+        for (int k = 0; k < nd; ++k) q.dst[k] = r->avg((c.rank + 1 + k + (c.world - nd)) % c.world);
         if (c.wire == SP_WIRE_Q8) {
-          const int64_t nb = (ra.hi + c.q8_block - 1) / c.q8_block - ra.lo / c.q8_block;
+          const int64_t nb = (hi + c.q8_block - 1) / c.q8_block - lo / c.q8_block;
           const int grid = (int)std::min<int64_t>(nb, (int64_t)r->sm_count * 16);
-          k_reduce_q8<<<grid, c.q8_block / 16, 0, st>>>(ra);
+          k_reduce_q8<<<grid, c.q8_block / 16, 0, st>>>(q);
         } else if (c.wire == SP_WIRE_FP16) {
-          k_reduce_fp16<<<grid_for((ra.hi - ra.lo + 7) / 8, 256, r->sm_count, r->xchg_per_sm), 256, 0, st>>>(ra);
+          k_reduce_fp16<<<grid_for((hi - lo + 7) / 8, 256, r->sm_count, r->xchg_per_sm), 256, 0, st>>>(q);
         } else {
-          k_reduce_fp32<<<grid_for((ra.hi - ra.lo + 3) / 4, 256, r->sm_count, r->xchg_per_sm), 256, 0, st>>>(ra);
+          k_reduce_fp32<<<grid_for((hi - lo + 3) / 4, 256, r->sm_count, r->xchg_per_sm), 256, 0, st>>>(q);
         }
         SP_CUDA(cudaGetLastError());
+        return SP_OK;
+      };
+      if (ra.hi > ra.lo && !identity_avg(r)) {
+        if (r->shard) {
+          // the replicated prefix (up to the cut, rounded up to a wire unit)
+          // goes to every rank
+          const int64_t cu = std::min<int64_t>(r->n, round_up(r->shard_cut, r->align));
+          if (int rc = reduce(ra.lo, std::min(ra.hi, cu), c.world)) return rc;
+          if (int rc = reduce(std::max(ra.lo, cu), ra.hi, 1)) return rc;
+        } else if (int rc = reduce(ra.lo, ra.hi, c.world)) {
+          return rc;
+        }
       }
     }
     if (ev && s == 0) SP_CUDA(cudaEventRecord(ev[3], st));
@@ -909,6 +1022,10 @@ int sp_round_create(const sp_round_cfg* cfg, sp_round** out) {
     // order and only wait on earlier ones)
     r->lamb_grid = std::max(1, per_sm * r->sm_count);
     if (const char* lg = std::getenv("SP_LAMB_GRID")) r->lamb_grid = std::max(1, std::min(r->lamb_grid, std::atoi(lg)));
+    // hybrid sharded LAMB: the replicated part leaves one CTA slot per SM to
+    // the sharded chain running beside it
+    r->hybrid_grid = std::max(1, r->lamb_grid - r->sm_count);
+    if (const char* hg = std::getenv("SP_HYBRID_LAMB_GRID")) r->hybrid_grid = std::max(1, std::atoi(hg));
     if ((e = cudaMalloc(&r->d_qstate, (2 + ntens) * sizeof(int))) != cudaSuccess ||
         (e = cudaMalloc(&r->d_ready, ntens * sizeof(unsigned int))) != cudaSuccess)
       return cleanup(fail(SP_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e)));
@@ -1096,6 +1213,8 @@ void* sp_round_wire_ptr(sp_round* r, int local_peer) {
 }
 
 float* sp_round_param_ptr(sp_round* r) { return r && r->shard ? r->param(r->cfg.rank) : nullptr; }
+
+int64_t sp_round_shard_cut(const sp_round* r) { return r && r->shard ? r->shard_cut : -1; }
 
 void* sp_round_avg_ptr(sp_round* r) { return r ? const_cast<char*>(avg_buffer(r)) : nullptr; }
 

@@ -188,6 +188,11 @@ class AveragingRound:
 
         return torch.as_tensor(_View(), device=f"cuda:{self.device}")
 
+    def shard_cut(self) -> int:
+        """shard_lamb: tensors before this element index keep the replicated
+        LAMB (full m/v on every rank); tensors from it on are sharded."""
+        return int(self._lib.sp_round_shard_cut(self._h))
+
     def own_range(self) -> tuple[int, int]:
         """[lo, hi) of the flattened vector this rank owns (averages, and with
         shard_lamb also steps)."""

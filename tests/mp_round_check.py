@@ -116,16 +116,29 @@ def main():
             rnd.run(grads, p, m, v, step)
         torch.cuda.synchronize()
         got, gs = rnd.read_wire(nat.SP_BUF_AVG)
-        if not np.array_equal(got[lo:hi], avg[lo:hi]):  # sharded: only the owned range is local
+        cut = rnd.shard_cut() if args.shard_lamb else n
+        have = np.zeros(n, bool)  # sharded: the average of sharded tensors stays with the owner
+        have[:min(n, -(-cut // rnd.align) * rnd.align)] = True
+        have[lo:hi] = True
+        if not np.array_equal(got[have], avg[have]):
             errors.append(f"step {step}: averaged vector differs ({int((got != avg).sum())} elems)")
-        if wire == "q8" and not np.array_equal(gs[lo // block:(hi + block - 1) // block],
-                                               avg_s[lo // block:(hi + block - 1) // block]):
+        if wire == "q8":
+            hs = np.zeros(len(avg_s), bool)
+            hs[:-(-min(n, -(-cut // block) * block) // block)] = True
+            hs[lo // block:(hi + block - 1) // block] = True
+        if wire == "q8" and not np.array_equal(gs[hs], avg_s[hs]):
             errors.append(f"step {step}: averaged q8 scales differ")
         trust = rnd.read_trust()
         O.lamb(wire, avg, avg_s, ph, mh, vh, sizes, HP, step, block, trust_in=trust)
-        # sharded: m and v are kept on the owned range, p everywhere
-        for name, dev, host, a, b in (("m", m, mh, lo, hi), ("v", v, vh, lo, hi), ("p", p, ph, 0, n)):
-            if not np.array_equal(dev.cpu().numpy()[a:b], host[a:b]):
+        # sharded: m and v are kept on the replicated prefix and the owned
+        # range of the sharded tensors; p everywhere
+        cut = rnd.shard_cut() if args.shard_lamb else n
+        keep = np.zeros(n, bool)
+        keep[:cut] = True
+        keep[max(lo, cut):hi] = True
+        for name, dev, host, msk in (("m", m, mh, keep), ("v", v, vh, keep), ("p", p, ph, None)):
+            d = dev.cpu().numpy()
+            if not (np.array_equal(d, host) if msk is None else np.array_equal(d[msk], host[msk])):
                 errors.append(f"step {step}: {name} differs")
     # all replicas identical
     digest = torch.tensor([float(p.double().sum()),

@@ -95,3 +95,9 @@ def test_sharded_lamb_ragged_owners():
     fr[0] = 0.4
     _launch(NGPU, "--wire", "fp16", "--shard-lamb", "--fractions", ",".join(map(str, fr)))
     _launch(NGPU, "--wire", "q8", "--shard-lamb", "--peers-per-rank", "2", "--accumulate")
+
+
+def test_sharded_lamb_hybrid_split():
+    # opt-in split: replicated LAMB for the leading tensors on a second stream
+    # beside the sharded chain (measured slower; kept bit-exact)
+    _launch(NGPU, "--wire", "fp16", "--shard-lamb", env={"SP_SHARD_FRACTION": "0.5"})
