@@ -196,13 +196,20 @@ def main():
     ap.add_argument("--peers-per-gpu", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--phased-steps", type=int, default=20)
-    ap.add_argument("--shard-lamb", action="store_true",
-                    help="ZeRO-1 style LAMB: owners step their range, parameters pushed to all ranks")
+    ap.add_argument("--lamb", choices=["auto", "replicated", "sharded"], default="auto",
+                    help="replicated: every GPU steps the all-gathered average; sharded: ZeRO-1 "
+                         "style, owners step their range and push fp32 parameters (faster at "
+                         "N > 1 for every wire, profiles/r01/overlap_experiments.txt); auto: "
+                         "sharded when N > 1")
+    ap.add_argument("--shard-lamb", action="store_true", help="alias of --lamb sharded")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.shard_lamb:
+        args.lamb = "sharded"
+    args.shard_lamb = args.lamb == "sharded" or (args.lamb == "auto" and world > 1)
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         log(f"note: WORLD_SIZE={world} but --gpus={args.gpus}; using WORLD_SIZE")
@@ -351,11 +358,13 @@ def main():
         if shard:
             fused = False
         f_l = f_r if shard else 1.0  # fraction of the vector this rank's LAMB steps
+        # one GPU, one peer, fp32/fp16: the pack runs inside LAMB pass 1
+        fused_pack = world == 1 and L == 1 and wire != "q8" and fused
         alg = {  # algorithmic bytes per launch, this rank
-            "pack_ms": (L * n * (4 + b)) if (wire != "fp32" or world > 1) else 0.0,
+            "pack_ms": 0.0 if fused_pack else (L * n * (4 + b)),
             "reduce_ms": (G + (1 if shard else world)) * f_r * n * b,
             # fused kernel: pass 1 reads g,p,m,v writes m,v; pass 2 reads p,m,v writes p
-            "moments_ms": f_l * n * (20 + b) + (n * 16.0 if fused else 0.0),
+            "moments_ms": f_l * n * (20 + b + (4 + b if fused_pack else 0.0)) + (n * 16.0 if fused else 0.0),
             "update_ms": 0.0 if fused else f_l * n * 16.0,
         }
         dom = max(("pack_ms", "reduce_ms", "moments_ms", "update_ms"), key=lambda k: ph[k])
@@ -425,7 +434,8 @@ def main():
             # (one rank with a single peer skips the reduce: identity average)
             "gpu_launches": args.steps * (
                 (1 + (1 if G > 1 else 0) + 4 + (4 if world > 1 else 0)) if shard else
-                (1 + (1 if G > 1 else 0) + (1 if fused else 3) + (2 if world > 1 else 0))),
+                ((0 if fused_pack else 1) + (1 if G > 1 else 0) + (1 if fused else 3)
+                 + (2 if world > 1 else 0))),
             "kernel_ms": {k: round(v_, 5) for k, v_ in ph.items()},
             "roofline": {"bound": bound, "kernel": dom.replace("_ms", ""),
                          "achieved": round(achieved, 1), "peak": pk, "unit": unit,

@@ -153,6 +153,11 @@ struct LambArgs {
   float b1, b2, omb1, omb2, eps, wd;
   int qshift;               // log2(q8 block): scale index = i >> qshift
   int l2_hints;             // fused LAMB: keep p/m/v of pass 1 in L2 for pass 2
+  // one rank, one peer, fp32/fp16 wire: the pack is fused into pass 1, which
+  // reads the fp32 gradient, rounds it to the wire format (the identity
+  // average) and also stores the wire values (nullptr: read `avg`)
+  const float* g32;
+  void* wire_out;
 };
 
 // ---------------------------------------------------------------- helpers
@@ -726,6 +731,20 @@ __global__ void __launch_bounds__(1024) k_reduce_q8(ReduceArgs a) {
 
 template <int W>
 __device__ __forceinline__ float4 load_grad4(const LambArgs& a, int64_t i) {
+  if constexpr (W != SP_WIRE_Q8) {
+    if (a.g32) {  // fused pack
+      const float4 x = *reinterpret_cast<const float4*>(a.g32 + i);
+      if constexpr (W == SP_WIRE_FP32) {
+        *reinterpret_cast<float4*>(static_cast<float*>(a.wire_out) + i) = x;
+        return x;
+      } else {
+        const uint32_t lo = pack_half2(x.x, x.y), hi = pack_half2(x.z, x.w);
+        *reinterpret_cast<uint2*>(static_cast<__half*>(a.wire_out) + i) = make_uint2(lo, hi);
+        const float2 f0 = unpack_half2(lo), f1 = unpack_half2(hi);
+        return make_float4(f0.x, f0.y, f1.x, f1.y);
+      }
+    }
+  }
   if constexpr (W == SP_WIRE_FP32) {
     return *reinterpret_cast<const float4*>(static_cast<const float*>(a.avg) + i);
   } else if constexpr (W == SP_WIRE_FP16) {
@@ -742,6 +761,19 @@ __device__ __forceinline__ float4 load_grad4(const LambArgs& a, int64_t i) {
 
 template <int W>
 __device__ __forceinline__ float load_grad1(const LambArgs& a, int64_t i) {
+  if constexpr (W != SP_WIRE_Q8) {
+    if (a.g32) {  // fused pack
+      const float x = a.g32[i];
+      if constexpr (W == SP_WIRE_FP32) {
+        static_cast<float*>(a.wire_out)[i] = x;
+        return x;
+      } else {
+        const __half h = __float2half_rn(x);
+        static_cast<__half*>(a.wire_out)[i] = h;
+        return __half2float(h);
+      }
+    }
+  }
   if constexpr (W == SP_WIRE_FP32) {
     return static_cast<const float*>(a.avg)[i];
   } else if constexpr (W == SP_WIRE_FP16) {

@@ -660,7 +660,18 @@ int enqueue_round(sp_round* r, const float* const* grads, float* p, float* m, fl
     const double to = c.barrier_timeout_s > 0 ? c.barrier_timeout_s : 20.0;
     ba.timeout_ns = (unsigned long long)(to * 1e9);
   }
-  const LambArgs la = make_lamb_args(r, p, m, v);
+  LambArgs la = make_lamb_args(r, p, m, v);
+  // one rank, one contributing peer, fp32/fp16: the average is the peer's
+  // rounded gradient, so the pack runs inside LAMB pass 1 (saves the wire
+  // re-read and a launch); the wire buffer is still written
+  const bool fuse_pack = c.world == 1 && r->L == 1 && c.wire != SP_WIRE_Q8 && r->fused_lamb &&
+                         r->acc_buf < 0 && !r->shard && grads[0] && identity_avg(r) &&
+                         (const void*)grads[0] != (const void*)r->wire(c.rank, 0) &&
+                         std::getenv("SP_NO_FUSED_PACK") == nullptr;
+  if (fuse_pack) {
+    la.g32 = grads[0];
+    la.wire_out = r->wire(c.rank, 0);
+  }
   if (r->acc_buf >= 0) {  // accumulated round: every rank learns every peer's sample count
     PublishArgs pa{};
     pa.staged = r->d_stage + (size_t)r->acc_buf * r->L;
@@ -706,7 +717,7 @@ int enqueue_round(sp_round* r, const float* const* grads, float* p, float* m, fl
     a.npad = r->npad;
     a.qblock = c.q8_block;
     const int64_t units = a.pref[a.nr];
-    if (any && units > 0) {
+    if (any && units > 0 && !fuse_pack) {
       const int threads = c.wire == SP_WIRE_Q8 ? c.q8_block / 16 : 256;
       const int64_t per_cta = c.wire == SP_WIRE_Q8 ? 1 : 256;  // units per CTA per pass
       const int want = c.wire == SP_WIRE_Q8
