@@ -34,20 +34,35 @@ NVLINK_GBS = 660.0  # measured all-to-all kernel push per GPU per direction, 4x 
 L2_BYTES = 126e6
 
 WORKLOADS = {
-    # name: (tensor table, wire, q8 block)
-    "albert-large-fp16": ("albert-large", "fp16", 4096),
-    "albert-large-fp32": ("albert-large", "fp32", 4096),
-    "albert-large-q8": ("albert-large", "q8", 4096),
-    "resnet50-q8": ("resnet50", "q8", 4096),
-    "albert-base-fp32": ("albert-base", "fp32", 4096),
+    # name: (tensor table, wire, q8 block, fleet). fleet None: G homogeneous
+    # peers; otherwise a named collaboration (paper_2106_10207_b200/fleets.py)
+    # whose peer count fixes G. Either way the LP (solve_strategy) plans the
+    # round: fractions -> part offsets, sample counts -> weights.
+    "albert-large-fp16": ("albert-large", "fp16", 4096, None),
+    "albert-large-fp32": ("albert-large", "fp32", 4096, None),
+    "albert-large-q8": ("albert-large", "q8", 4096, None),
+    "resnet50-q8": ("resnet50", "q8", 4096, None),
+    "albert-base-fp32": ("albert-base", "fp32", 4096, None),
+    # BASELINE config 1 (reference CPU scenario): ALBERT-base, fp32, 4 heterogeneous peers
+    "het4b-fp32": ("albert-base", "fp32", 4096, "het4b"),
+    # BASELINE config 4: 8 peers incl. a client, fractions 1/20 x6, 0, 7/10
+    "het8c-fp16": ("albert-large", "fp16", 4096, "het8c"),
+    # BASELINE config 5: --params N, --wire {fp32,fp16,q8}; 4 Mi-element tensors
+    "sweep": ("uniform4m", None, 4096, None),
 }
+TARGET_BATCH = 4096.0  # PAPER.md:842; the LP's sample counts are scaled to it
 
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-def tensor_table(name: str) -> list[int]:
+def tensor_table(name: str, params: int = 0) -> list[int]:
+    if name == "uniform4m":  # sweep: 4,194,304-element tensors, remainder last
+        if params < 1:
+            raise SystemExit("--workload sweep needs --params N")
+        t = 4 * 1024 * 1024
+        return [t] * (params // t) + ([params % t] if params % t else [])
     with open(os.path.join(ROOT, "tests", "golden", "tensor_tables.json")) as f:
         return json.load(f)[name]
 
@@ -165,8 +180,7 @@ def cpu_round_time(tsizes, wire, block, G, weights, reps: int, threads: int = 0)
 def lp_solve_times() -> dict:
     """Host LP (strategy solve) time, median of 5, for the fleets the budget is
     quoted on (< 50 ms at n = 16: PAPER.md:140)."""
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from golden.fleets import homogeneous, spec_json
+    from paper_2106_10207_b200.fleets import homogeneous, spec_json
 
     from paper_2106_10207_b200 import _swarmplan
 
@@ -183,6 +197,35 @@ def lp_solve_times() -> dict:
             ts.append(time.perf_counter() - t0)
         out[name] = round(statistics.median(ts) * 1e3, 2)
     return out
+
+
+def rank_model(r, offsets, L, world, n, b, wire, shard, fused, fused_pack) -> dict:
+    """Algorithmic bytes per element for rank r: per-kernel
+    launch bytes (`alg`), whole-round HBM bytes and NVLink bytes per
+    direction (the larger of out and in), for the part fraction f it owns."""
+    G = L * world
+    f = (offsets[(r + 1) * L] - offsets[r * L]) / n
+    f_l = f if shard else 1.0  # fraction of the vector this rank's LAMB steps
+    alg = {
+        "pack_ms": 0.0 if fused_pack else (L * n * (4 + b)),
+        "reduce_ms": (G + (1 if shard else world)) * f * n * b,
+        # fused kernel: pass 1 reads g,p,m,v writes m,v; pass 2 reads p,m,v writes p
+        "moments_ms": f_l * n * (20 + b + (4 + b if fused_pack else 0.0)) + (n * 16.0 if fused else 0.0),
+        "update_ms": 0.0 if fused else f_l * n * 16.0,
+    }
+    # G = 1: the average of one peer is its wire values, no reduce pass;
+    # fp32 on one GPU: the wire is the gradient itself (zero-copy)
+    hbm = (((4 + b) * L if (wire != "fp32" or world > 1) else 0.0)
+           + ((G + (1 if shard else world)) * f * b if G > 1 else 0.0)
+           + f_l * (24 + b))  # one-pass LAMB ideal
+    if world == 1:
+        nvl = 0.0
+    else:  # scatter the gradient parts; all-gather averaged parts (or fp32 params)
+        back = 4.0 if shard else b
+        out_ = L * (1 - f) * b + (world - 1) * f * back
+        in_ = (G - L) * f * b + (1 - f) * back
+        nvl = max(out_, in_)
+    return {"f": f, "alg": alg, "hbm": hbm, "nvl": nvl}
 
 
 # ------------------------------------------------------------------ main
@@ -202,6 +245,9 @@ def main():
                          "N > 1 for every wire, profiles/r01/overlap_experiments.txt); auto: "
                          "sharded when N > 1")
     ap.add_argument("--shard-lamb", action="store_true", help="alias of --lamb sharded")
+    ap.add_argument("--params", type=int, default=0, help="--workload sweep: vector length")
+    ap.add_argument("--wire", choices=["fp32", "fp16", "q8"], default=None,
+                    help="override the workload's wire format (required for sweep)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -214,13 +260,32 @@ def main():
     if world != args.gpus:
         log(f"note: WORLD_SIZE={world} but --gpus={args.gpus}; using WORLD_SIZE")
 
-    table, wire, block = WORKLOADS[args.workload]
-    tsizes = tensor_table(table)
+    table, wire, block, fleet = WORKLOADS[args.workload]
+    wire = args.wire or wire
+    if wire is None:
+        raise SystemExit(f"--workload {args.workload} needs --wire")
+    tsizes = tensor_table(table, args.params)
     n = sum(tsizes)
-    L = args.peers_per_gpu
+    from paper_2106_10207_b200 import fleets
+    from paper_2106_10207_b200.dist import plan_round
+
+    if fleet:
+        spec_j = fleets.spec_json(fleet)
+        n_peers = len(json.loads(spec_j)["peers"])
+        if n_peers % world:
+            raise SystemExit(f"fleet {fleet} has {n_peers} peers; WORLD_SIZE={world} must divide it")
+        L = n_peers // world
+    else:
+        L = args.peers_per_gpu
+        spec_j = json.dumps(fleets.homogeneous(L * world, 1.0, 1000.0, TARGET_BATCH, n))
     G = L * world
-    fractions = [1.0 / G] * G  # homogeneous fleet: LP gives 1/G each (test_strategy.cpp:186-195)
-    weights = [4096.0 / G] * G  # target batch 4096 split evenly
+    # host LP plan (every rank solves the same deterministic program;
+    # AveragingRound.set_assignment checks they agree)
+    align = block if wire == "q8" else 8  # sp_round_align: no q8 block straddles owners
+    plan = plan_round(spec_j, n, align)
+    offsets = [int(x) for x in plan["offsets"]]
+    wsum = sum(plan["weights"])
+    weights = [w * TARGET_BATCH / wsum for w in plan["weights"]]  # sample counts, sum = batch
     b = wire_bytes(wire, block)
 
     if args.impl == "reference":
@@ -244,7 +309,9 @@ def main():
                          world=world, device=local_rank, lr=HP["lr"],
                          betas=(HP["beta1"], HP["beta2"]), eps=HP["eps"],
                          weight_decay=HP["weight_decay"], shard_lamb=args.shard_lamb)
-    offsets = rnd.assign(fractions, weights)
+    if rnd.align != align:
+        raise SystemExit(f"align mismatch: library {rnd.align}, planned {align}")
+    rnd.set_assignment(offsets, weights)
     grads = []
     for l in range(L):
         g = torch.empty(n, dtype=torch.float32, device=dev)
@@ -350,47 +417,43 @@ def main():
     e2e_step = e2e_ms / e2e_steps
     e2e_value = grad_bytes / (e2e_step * 1e-3) / 1e9
 
+    all_ph = [ph]
+    if world > 1:
+        all_ph = [None] * world
+        torch.distributed.all_gather_object(all_ph, ph)
+
     if rank == 0:
         peak, peak_kind = peak_hbm()
-        f_r = (offsets[(rank + 1) * L] - offsets[rank * L]) / n
-        fused = ph["update_ms"] < 0.1 * ph["moments_ms"]  # fused LAMB: one kernel
         shard = args.shard_lamb
-        if shard:
-            fused = False
-        f_l = f_r if shard else 1.0  # fraction of the vector this rank's LAMB steps
+        fused = ph["update_ms"] < 0.1 * ph["moments_ms"] and not shard  # fused LAMB: one kernel
         # one GPU, one peer, fp32/fp16: the pack runs inside LAMB pass 1
         fused_pack = world == 1 and L == 1 and wire != "q8" and fused
-        alg = {  # algorithmic bytes per launch, this rank
-            "pack_ms": 0.0 if fused_pack else (L * n * (4 + b)),
-            "reduce_ms": (G + (1 if shard else world)) * f_r * n * b,
-            # fused kernel: pass 1 reads g,p,m,v writes m,v; pass 2 reads p,m,v writes p
-            "moments_ms": f_l * n * (20 + b + (4 + b if fused_pack else 0.0)) + (n * 16.0 if fused else 0.0),
-            "update_ms": 0.0 if fused else f_l * n * 16.0,
-        }
-        dom = max(("pack_ms", "reduce_ms", "moments_ms", "update_ms"), key=lambda k: ph[k])
+        models = [rank_model(r, offsets, L, world, n, b, wire, shard, fused, fused_pack)
+                  for r in range(world)]
+        # critical rank: the one whose phased round is longest (non-uniform
+        # LP splits put the big owner on the critical path)
+        rc = max(range(world), key=lambda r: all_ph[r]["total_ms"])
+        phc, mc = all_ph[rc], models[rc]
+        f_r, alg = mc["f"], mc["alg"]
+        dom = max(("pack_ms", "reduce_ms", "moments_ms", "update_ms"), key=lambda k: phc[k])
         widx = {"fp32": 0, "fp16": 1, "q8": 2}[wire]
         kname = {"pack_ms": f"k_pack_{wire}", "reduce_ms": f"k_reduce_{wire}",
                  "moments_ms": f"k_lamb_fused<{widx}>" if fused else f"k_lamb_moments<{widx}>",
                  "update_ms": f"k_lamb_update<{widx}>"}[dom]
-        achieved = alg[dom] / (ph[dom] * 1e-3) / 1e9
+        achieved = alg[dom] / (phc[dom] * 1e-3) / 1e9
         bound, pk, unit = "hbm", peak, "GB/s"
         if shard and dom == "update_ms" and world > 1:  # parameter push: (world-1) f 4 B out
             bound, pk = "nvlink", NVLINK_GBS
-            achieved = (world - 1) * f_r * 4.0 * n / (ph[dom] * 1e-3) / 1e9
+            achieved = (world - 1) * f_r * 4.0 * n / (phc[dom] * 1e-3) / 1e9
         elif dom in ("reduce_ms", "pack_ms") and world > 1:
             bound, pk = "nvlink", NVLINK_GBS
-            # per direction: pack scatters (1-f) b n, reduce pushes (G-1) f b n
-            nvl = ((1 - f_r) * b * n) if dom == "pack_ms" else ((world - 1) * f_r * b * n)
-            achieved = nvl / (ph[dom] * 1e-3) / 1e9
-        # whole-round roofline: serialized HBM + NVLink phases
-        # (G = 1: the average of one peer is its wire values, no reduce pass)
-        hbm_round = ((4 + b) * L if (wire != "fp32" or world > 1) else 0.0) + \
-            ((G + (1 if shard else world)) * f_r * b if G > 1 else 0.0) + \
-            f_l * (24 + b)  # one-pass LAMB ideal
-        if shard:  # scatter the gradient parts, push the updated fp32 parameters
-            nvl_round = ((1 - f_r) * b + (world - 1) * f_r * 4.0) if world > 1 else 0.0
-        else:
-            nvl_round = ((1 - f_r) * b + (G - 1) * f_r * b) if world > 1 else 0.0
+            # per direction: pack scatters L (1-f) b n, reduce pushes (world-1) f b n
+            nvl = (L * (1 - f_r) * b * n) if dom == "pack_ms" else ((world - 1) * f_r * b * n)
+            achieved = nvl / (phc[dom] * 1e-3) / 1e9
+        # whole-round roofline: serialized HBM + NVLink
+        # phases, each taken on its critical-path GPU
+        hbm_round = max(x["hbm"] for x in models)
+        nvl_round = max(x["nvl"] for x in models)
         t_roof = hbm_round * n / (peak * 1e9) + nvl_round * n / (NVLINK_GBS * 1e9)
         lp_times = None
         try:
@@ -407,6 +470,7 @@ def main():
                                  f"{wire} wire, median of 3 rounds"}
             except Exception as e:
                 log("cpu baseline failed:", e)
+        fr = [round(x, 6) for x in plan["fractions"]]
         out = {
             "metric": METRIC,
             "value": round(value, 3),
@@ -427,9 +491,12 @@ def main():
                        "lamb": "sharded (ZeRO-1: owners step, fp32 params pushed)" if args.shard_lamb
                                else "replicated (averaged gradient all-gathered)",
                        "shard_cut": rnd.shard_cut() if args.shard_lamb else None,
-                       "fractions": "uniform 1/G (LP, homogeneous fleet)",
+                       "fleet": fleet or f"homogeneous{G}",
+                       "fractions": fr if G <= 16 else f"{min(fr)}..{max(fr)}",
+                       "plan": "solve_strategy (host LP) -> part_offsets; weights = LP sample "
+                               f"counts scaled to batch {TARGET_BATCH:g}",
                        "l2": f"no flush: per-step working set {(n * (12 + 4 * L + 2 * b)) / 1e9:.2f} GB > 126 MB L2",
-                       "parallelism": f"dp{world} (one peer per GPU, CUDA IPC over NVLink)"},
+                       "parallelism": f"dp{world} (one process per GPU, {L} peer(s) each, CUDA IPC over NVLink)"},
             # per round: pack + reduce + LAMB (1 fused / 3 unfused) + 2 barriers if N > 1
             # (one rank with a single peer skips the reduce: identity average)
             "gpu_launches": args.steps * (
@@ -437,9 +504,11 @@ def main():
                 ((0 if fused_pack else 1) + (1 if G > 1 else 0) + (1 if fused else 3)
                  + (2 if world > 1 else 0))),
             "kernel_ms": {k: round(v_, 5) for k, v_ in ph.items()},
-            "roofline": {"bound": bound, "kernel": dom.replace("_ms", ""),
+            "kernel_ms_critical_rank": {k: round(v_, 5) for k, v_ in phc.items()} if rc else None,
+            "roofline": {"bound": bound, "kernel": dom.replace("_ms", ""), "rank": rc,
                          "achieved": round(achieved, 1), "peak": pk, "unit": unit,
-                         "frac": round(achieved / pk, 4), "traffic": ncu_traffic(kname),
+                         "frac": round(achieved / pk, 4),
+                         "traffic": ncu_traffic(kname) if table == "albert-large" else None,
                          "algorithmic_bytes": alg[dom],
                          "peak_kind": peak_kind if bound == "hbm" else "measured all-to-all push (profiles/r01/p2p_bw.txt)"},
             "round_roofline": {"t_roof_us": round(t_roof * 1e6, 2),

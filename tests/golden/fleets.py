@@ -4,30 +4,7 @@ The reference fixtures (/root/reference/proj/scenarios/*.json) are uniform
 groups of peers; each entry below names the file it restates and lists
 (count, samples_per_sec, download_mbps, upload_mbps, extra flags). het8c /
 het4b are the unique-fraction fixtures of SURVEY.md Appendix A."""
-import json
-
-FLEETS = {
-    # name: (batch_size, param_count, [(count, s, d, u, flags)], source)
-    "homogeneous8": (8.0, 25.6e6, [(8, 1.0, 1000.0, 1000.0, {})], "scenarios/homogeneous8.json"),
-    "table1_a": (8.0, 25.6e6, [(8, 1.0, 1000.0, 1000.0, {})], "scenarios/table1_a.json"),
-    "table1_b": (1.0, 25.6e6, [(16, 1.0, 200.0, 200.0, {})], "scenarios/table1_b.json"),
-    "table1_c": (1.0, 25.6e6, [(8, 1.0, 1000.0, 1000.0, {}), (16, 1.0, 200.0, 200.0, {})],
-                 "scenarios/table1_c.json"),
-    "table1_d": (1.0, 25.6e6, [(16, 1.0, 200.0, 200.0, {}), (1, 1.0, 2500.0, 2500.0, {})],
-                 "scenarios/table1_d.json"),
-    "daynight": (8.0, 1e6, [(24, 1.0, 1000.0, 1000.0, {})], "scenarios/daynight.json"),
-    "static16": (8.0, 1e6, [(16, 1.0, 1000.0, 1000.0, {})], "scenarios/static16.json"),
-    "aux_server": (4.0, 25.6e6, [(8, 1.0, 1000.0, 1000.0, {}),
-                                 (1, 0.0, 100000.0, 100000.0, {"can_compute": False})],
-                   "scenarios/aux_server.json"),
-    "no_compute": (1.0, 25.6e6, [(4, 0.0, 1000.0, 1000.0, {"can_compute": False})],
-                   "scenarios/no_compute.json"),
-    # SURVEY.md Appendix A (unique fractions; HiGHS DS = IPM)
-    "het8c": (8.0, 17847474.0, [(6, 1.0, 200.0, 200.0, {}), (1, 1.0, 200.0, 200.0, {"client_mode": True}),
-                                (1, 1.0, 800.0, 800.0, {})], "SURVEY.md Appendix A"),
-    "het4b": (4.0, 11813810.0, [(3, 1.0, 200.0, 200.0, {}), (1, 1.0, 500.0, 500.0, {})],
-              "SURVEY.md Appendix A"),
-}
+from paper_2106_10207_b200.fleets import FLEETS, homogeneous, spec, spec_json  # noqa: F401
 
 # frozen xi goldens (/root/reference/proj/tests/cpp/test_strategy.cpp:189,200,213-220)
 XI_GOLDEN = {
@@ -38,25 +15,3 @@ XI_GOLDEN = {
 # SURVEY.md Appendix A (PROBE, HiGHS)
 XI_APPENDIX_A = {"het8c": 0.269376624821, "het4b": 0.484955037085}
 FRACTIONS_APPENDIX_A = {"het8c": [1 / 20] * 6 + [0.0, 7 / 10], "het4b": [1 / 22] * 3 + [19 / 22]}
-
-
-def spec(name: str) -> dict:
-    batch, params, groups, _ = FLEETS[name]
-    peers = []
-    for count, s, d, u, flags in groups:
-        for _ in range(count):
-            p = {"id": f"peer{len(peers)}", "samples_per_sec": s, "download_mbps": d,
-                 "upload_mbps": u}
-            p.update(flags)
-            peers.append(p)
-    return {"peers": peers, "batch_size": batch, "param_count": params, "bits_per_param": 32.0}
-
-
-def spec_json(name: str) -> str:
-    return json.dumps(spec(name))
-
-
-def homogeneous(n, samples=1.0, mbps=1000.0, batch=1.0, params=1e6):
-    return {"peers": [{"id": f"peer{i}", "samples_per_sec": samples, "download_mbps": mbps,
-                       "upload_mbps": mbps} for i in range(n)],
-            "batch_size": batch, "param_count": params, "bits_per_param": 32.0}
