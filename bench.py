@@ -30,7 +30,11 @@ sys.path.insert(0, ROOT)
 METRIC = "averaging round time + GB/s (grad avg + LAMB step), ALBERT-large, 1/2/4/8 B200"
 HP = dict(lr=1.76e-3, beta1=0.9, beta2=0.999, eps=1e-6, weight_decay=0.01, bias_correction=1)
 SIGMA = 1e-3 * 3 ** 0.5
-NVLINK_GBS = 660.0  # measured all-to-all kernel push per GPU per direction, 4x B200 (profiles/r01/p2p_bw.txt); 770 single-peer copy, 900 nominal
+# NVLink roofline denominator: the measured B200 peer copy per direction per
+# GPU (/opt/skills/guides/B200_PROFILING.md; 900 nominal). Our own all-to-all
+# push microbenchmark sustains ~660 at 4 GPUs (profiles/r01/p2p_bw.txt) and
+# large sweeps reach ~770 (profiles/r01/sweep).
+NVLINK_GBS = 770.0
 L2_BYTES = 126e6
 
 WORKLOADS = {
@@ -55,6 +59,28 @@ TARGET_BATCH = 4096.0  # PAPER.md:842; the LP's sample counts are scaled to it
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
+
+
+_STDOUT_FD = None
+
+
+def quiet_stdout() -> None:
+    """Route fd 1 to stderr for the whole run (NCCL and library banners
+    print there) and keep the real stdout for the one JSON line."""
+    global _STDOUT_FD
+    if _STDOUT_FD is None:
+        sys.stdout.flush()
+        _STDOUT_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(obj) -> None:
+    line = (json.dumps(obj) + "\n").encode()
+    if _STDOUT_FD is None:
+        sys.stdout.write(line.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_STDOUT_FD, line)
 
 
 def tensor_table(name: str, params: int = 0) -> list[int]:
@@ -200,9 +226,13 @@ def lp_solve_times() -> dict:
 
 
 def rank_model(r, offsets, L, world, n, b, wire, shard, fused, fused_pack) -> dict:
-    """Algorithmic bytes per element for rank r: per-kernel
-    launch bytes (`alg`), whole-round HBM bytes and NVLink bytes per
-    direction (the larger of out and in), for the part fraction f it owns."""
+    """Algorithmic bytes per element for rank r given the
+    part fraction f it owns: per-kernel launch bytes (`alg`) and, for each
+    phase of the round (pack+scatter, reduce(+push), LAMB(+parameter push)),
+    the HBM bytes it must move and the NVLink bytes per direction (the larger
+    of out and in). Phases are separated by cross-rank barriers, so the
+    round's roofline is the sum over phases of the slowest rank's
+    max(HBM time, NVLink time)."""
     G = L * world
     f = (offsets[(r + 1) * L] - offsets[r * L]) / n
     f_l = f if shard else 1.0  # fraction of the vector this rank's LAMB steps
@@ -213,19 +243,39 @@ def rank_model(r, offsets, L, world, n, b, wire, shard, fused, fused_pack) -> di
         "moments_ms": f_l * n * (20 + b + (4 + b if fused_pack else 0.0)) + (n * 16.0 if fused else 0.0),
         "update_ms": 0.0 if fused else f_l * n * 16.0,
     }
-    # G = 1: the average of one peer is its wire values, no reduce pass;
-    # fp32 on one GPU: the wire is the gradient itself (zero-copy)
-    hbm = (((4 + b) * L if (wire != "fp32" or world > 1) else 0.0)
-           + ((G + (1 if shard else world)) * f * b if G > 1 else 0.0)
-           + f_l * (24 + b))  # one-pass LAMB ideal
-    if world == 1:
-        nvl = 0.0
-    else:  # scatter the gradient parts; all-gather averaged parts (or fp32 params)
-        back = 4.0 if shard else b
-        out_ = L * (1 - f) * b + (world - 1) * f * back
-        in_ = (G - L) * f * b + (1 - f) * back
-        nvl = max(out_, in_)
-    return {"f": f, "alg": alg, "hbm": hbm, "nvl": nvl}
+    multi = world > 1
+    # pack: read the fp32 gradients (4 L), write the wire of the owned range
+    # (L f b from local peers, (G - L) f b arriving from the other ranks; the
+    # rest of the local wire lands in the owners' HBM). fp32 on one GPU: the
+    # wire is the gradient itself (zero-copy).
+    pack_hbm = (4 * L + G * f * b) if (wire != "fp32" or multi) else 0.0
+    pack_nvl = max(L * (1 - f) * b, (G - L) * f * b) if multi else 0.0
+    # reduce: read G inbox slots of the owned range, write the average
+    # (replicated: pushed to every rank, (1 - f) b arrives from the others).
+    # G = 1: the average of one peer is its wire values, no reduce pass.
+    if G > 1:
+        # sharded: the average stays local (f b); replicated: f b written
+        # here and pushed out, (1 - f) b of the others' averages lands here
+        red_hbm = G * f * b + (f * b if shard else b)
+        red_nvl = 0.0 if (shard or not multi) else max((world - 1) * f * b, (1 - f) * b)
+    else:
+        red_hbm = red_nvl = 0.0
+    # LAMB, one-pass ideal: read wire grad + p, m, v, write p, m, v; sharded:
+    # the fp32 parameters of the owned range go to every other rank
+    lamb_hbm = f_l * (24 + b) + ((1 - f) * 4.0 if shard and multi else 0.0)
+    lamb_nvl = max((world - 1) * f * 4.0, (1 - f) * 4.0) if (shard and multi) else 0.0
+    phases = [(pack_hbm, pack_nvl), (red_hbm, red_nvl), (lamb_hbm, lamb_nvl)]
+    return {"f": f, "alg": alg, "phases": phases,
+            "hbm": sum(h for h, _ in phases), "nvl": sum(x for _, x in phases)}
+
+
+def round_roofline(models, n, peak) -> float:
+    """Seconds: sum over phases of the slowest rank's max(HBM, NVLink) time."""
+    t = 0.0
+    for k in range(3):
+        t += max(max(m["phases"][k][0] * n / (peak * 1e9), m["phases"][k][1] * n / (NVLINK_GBS * 1e9))
+                 for m in models)
+    return t
 
 
 # ------------------------------------------------------------------ main
@@ -250,6 +300,7 @@ def main():
                     help="override the workload's wire format (required for sweep)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    quiet_stdout()
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -387,26 +438,30 @@ def main():
     ph = {k: statistics.mean(x[k] for x in phases) for k in keys}
     ph["total_ms"] = statistics.mean(x["total_ms"] for x in phases)
 
-    # e2e through the public API with host buffers: H2D of this rank's
-    # accumulated gradients (pinned), the round, D2H of the trust ratios
+    # e2e through the public API with host buffers (sp_round_run_host): H2D
+    # of this rank's accumulated gradients from pinned memory into a
+    # double-buffered staging area (step k's copy overlaps round k-1), the
+    # round, D2H of the step's trust ratios
     host_g = [gg.cpu().pin_memory() for gg in grads]
     trust_h = torch.empty(len(tsizes), dtype=torch.float32).pin_memory()
     e2e_steps = max(3, min(args.steps, 20))
+
+    def one_host():
+        nonlocal step
+        step += 1
+        rnd.run_host(host_g, p, m, v, step, stream)
+        rnd.copy_trust_async(trust_h.data_ptr(), stream)  # D2H of the step's result
+
     with torch.cuda.stream(stream):
-        for _ in range(2):
-            for l in range(L):
-                grads[l].copy_(host_g[l], non_blocking=True)
-            one()
+        for _ in range(3):  # captures the graphs of both staging buffers
+            one_host()
         barrier()
         torch.cuda.synchronize(dev)
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for _ in range(e2e_steps):
-            for l in range(L):
-                grads[l].copy_(host_g[l], non_blocking=True)
-            one()
-            rnd.copy_trust_async(trust_h.data_ptr(), stream)  # D2H of the step's result
+            one_host()
         f1.record(stream)
         torch.cuda.synchronize(dev)
     e2e_ms = f0.elapsed_time(f1)
@@ -430,9 +485,10 @@ def main():
         fused_pack = world == 1 and L == 1 and wire != "q8" and fused
         models = [rank_model(r, offsets, L, world, n, b, wire, shard, fused, fused_pack)
                   for r in range(world)]
-        # critical rank: the one whose phased round is longest (non-uniform
-        # LP splits put the big owner on the critical path)
-        rc = max(range(world), key=lambda r: all_ph[r]["total_ms"])
+        # critical rank: the one with the longest modeled round (non-uniform
+        # LP splits put the big owner on the critical path);
+        # every rank's phased times include waiting for it at the barriers
+        rc = max(range(world), key=lambda r: (round_roofline([models[r]], n, peak), -r))
         phc, mc = all_ph[rc], models[rc]
         f_r, alg = mc["f"], mc["alg"]
         dom = max(("pack_ms", "reduce_ms", "moments_ms", "update_ms"), key=lambda k: phc[k])
@@ -450,11 +506,10 @@ def main():
             # per direction: pack scatters L (1-f) b n, reduce pushes (world-1) f b n
             nvl = (L * (1 - f_r) * b * n) if dom == "pack_ms" else ((world - 1) * f_r * b * n)
             achieved = nvl / (phc[dom] * 1e-3) / 1e9
-        # whole-round roofline: serialized HBM + NVLink
-        # phases, each taken on its critical-path GPU
+        # whole-round roofline (per phase on the slowest rank)
         hbm_round = max(x["hbm"] for x in models)
         nvl_round = max(x["nvl"] for x in models)
-        t_roof = hbm_round * n / (peak * 1e9) + nvl_round * n / (NVLINK_GBS * 1e9)
+        t_roof = round_roofline(models, n, peak)
         lp_times = None
         try:
             lp_times = lp_solve_times()
@@ -510,19 +565,23 @@ def main():
                          "frac": round(achieved / pk, 4),
                          "traffic": ncu_traffic(kname) if table == "albert-large" else None,
                          "algorithmic_bytes": alg[dom],
-                         "peak_kind": peak_kind if bound == "hbm" else "measured all-to-all push (profiles/r01/p2p_bw.txt)"},
+                         "peak_kind": peak_kind if bound == "hbm" else "measured peer copy per direction (B200_PROFILING.md)"},
             "round_roofline": {"t_roof_us": round(t_roof * 1e6, 2),
                                "frac": round(t_roof * 1e3 / ms_step, 4),
                                "hbm_B_per_param": round(hbm_round, 3),
-                               "nvlink_B_per_param_dir": round(nvl_round, 3)},
+                               "nvlink_B_per_param_dir": round(nvl_round, 3),
+                               "model": f"sum over phases (pack+scatter, reduce, LAMB[+param push]) of the "
+                                        f"slowest rank's max(HBM B/{peak:g} GB/s, NVLink B/{NVLINK_GBS:g} GB/s)"},
             "e2e": {"value": round(e2e_value, 3), "unit": "GB/s",
                     "round_us": round(e2e_step * 1e3, 2),
-                    "h2d_bytes_per_step": 4 * n * L, "d2h_bytes_per_step": 4 * len(tsizes)},
+                    "h2d_bytes_per_step": 4 * n * L, "d2h_bytes_per_step": 4 * len(tsizes),
+                    "api": "AveragingRound.run_host -> sp_round_run_host (pinned host gradients; "
+                           "step k's H2D overlaps round k-1)"},
             "clocks": clk,
             "cpu_baseline": cpu,
             "lp_solve_ms": lp_times,
         }
-        print(json.dumps(out), flush=True)
+        emit(out)
     rnd.close()
     if world > 1:
         torch.distributed.destroy_process_group()
@@ -545,15 +604,16 @@ def run_reference(args, rank, world, tsizes, wire, block, G, weights, b):
     p = O.fill_synthetic(n, 2, 0, 0.02, 0)
     m = np.zeros(n, np.float32)
     v = np.zeros(n, np.float32)
+    threads = len(os.sched_getaffinity(0))  # every host core (torchrun sets OMP_NUM_THREADS=1)
     for w in range(args.warmup):
-        O.round_cpu(wire, grads, weights, p, m, v, tsizes, HP, w + 1, block, 0)
+        O.round_cpu(wire, grads, weights, p, m, v, tsizes, HP, w + 1, block, threads)
     t0 = time.perf_counter()
     for r in range(reps):
-        O.round_cpu(wire, grads, weights, p, m, v, tsizes, HP, args.warmup + r + 1, block, 0)
+        O.round_cpu(wire, grads, weights, p, m, v, tsizes, HP, args.warmup + r + 1, block, threads)
     sec = (time.perf_counter() - t0) / reps
     grad_bytes = 4.0 * n * G
     val = grad_bytes / sec / 1e9
-    cores = O.max_threads()
+    cores = threads
     out = {
         "metric": METRIC, "impl": "reference", "value": round(val, 4), "unit": "GB/s",
         "n_gpus": world, "steps": reps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3),
@@ -566,7 +626,7 @@ def run_reference(args, rank, world, tsizes, wire, block, G, weights, b):
         "e2e": {"value": round(val, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(out), flush=True)
+    emit(out)
     return 0
 
 

@@ -131,6 +131,17 @@ int sp_round_set_assignment(sp_round* r, const int64_t* offsets,
 int sp_round_run(sp_round* r, const float* const* grads, float* p, float* m,
                  float* v, int step, void* stream);
 
+/* The same round fed from HOST gradients (the drop-in call for a peer whose
+ * accumulated gradients live in host memory). host_grads[l] should be
+ * pinned (cudaHostAlloc / torch pin_memory) for the copy to be asynchronous.
+ * The copy goes to one of two device staging buffers on an internal copy
+ * stream, so step k's host->device copy overlaps round k-1 on `stream`;
+ * the round itself is sp_round_run on the staged buffer (graph replay; the
+ * two staging buffers keep two cached graphs). The host buffers may be
+ * reused once `stream` has passed this round. */
+int sp_round_run_host(sp_round* r, const float* const* host_grads, float* p,
+                      float* m, float* v, int step, void* stream);
+
 /* Same round without graph capture, with CUDA events between phases;
  * synchronizes the stream and fills *t. Diagnostic only. */
 int sp_round_run_phased(sp_round* r, const float* const* grads, float* p,

@@ -56,6 +56,10 @@ class AveragingRound {
   StrategyAssignment plan(const CollaborationSpec& spec, const std::vector<double>& weights);
 
   void run(const float* const* grads, float* p, float* m, float* v, int step, void* stream = nullptr);
+  // Same round from pinned HOST gradients (sp_round_run_host): the copy of
+  // step k overlaps round k-1 through double-buffered device staging.
+  void run_host(const float* const* host_grads, float* p, float* m, float* v, int step,
+                void* stream = nullptr);
   sp_phase_times run_phased(const float* const* grads, float* p, float* m, float* v, int step,
                             void* stream = nullptr);
 

@@ -75,6 +75,7 @@ def lib() -> ctypes.CDLL:
         "sp_round_align": (c_int, [vp]),
         "sp_round_set_assignment": (c_int, [vp, ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double)]),
         "sp_round_run": (c_int, [vp, ctypes.POINTER(vp), vp, vp, vp, c_int, vp]),
+        "sp_round_run_host": (c_int, [vp, ctypes.POINTER(vp), vp, vp, vp, c_int, vp]),
         "sp_round_run_phased": (c_int, [vp, ctypes.POINTER(vp), vp, vp, vp, c_int, vp,
                                         ctypes.POINTER(SpPhaseTimes)]),
         "sp_round_wire_ptr": (vp, [vp, c_int]),
@@ -109,7 +110,7 @@ def lib() -> ctypes.CDLL:
 EXPORTED_SYMBOLS = [
     "sp_round_create", "sp_round_destroy", "sp_round_handle_bytes", "sp_round_export",
     "sp_round_connect", "sp_round_align", "sp_round_set_assignment", "sp_round_run",
-    "sp_round_run_phased", "sp_round_wire_ptr", "sp_round_avg_ptr", "sp_round_param_ptr",
+    "sp_round_run_host", "sp_round_run_phased", "sp_round_wire_ptr", "sp_round_avg_ptr", "sp_round_param_ptr",
     "sp_round_shard_cut",
     "sp_round_padded_n",
     "sp_round_trust_ptr", "sp_round_copy_trust", "sp_round_read", "sp_round_accumulate", "sp_round_accumulator_ptr",

@@ -109,10 +109,19 @@ struct sp_round {
   std::vector<int64_t> offsets;
   std::vector<double> weights;
   bool assigned = false;
-  // graph cache
+  // graph cache: two entries, so the double-buffered host-input rounds
+  // (sp_round_run_host) alternate between two captured graphs
   cudaStream_t own = nullptr;
-  cudaGraphExec_t gexec = nullptr;
-  std::vector<const void*> gkey;
+  cudaGraphExec_t gexec[2] = {};
+  std::vector<const void*> gkey[2];
+  int gnext = 0;  // slot replaced on the next miss
+  // host-input rounds: pinned host gradients -> device staging (double
+  // buffered) on a copy stream, overlapped with the previous round
+  float* stg[2][SP_MAX_LOCAL] = {};
+  cudaStream_t h2d = nullptr;
+  cudaEvent_t stg_ready[2] = {}, stg_free[2] = {};
+  bool stg_used[2] = {};
+  int stg_next = 0;
   cudaEvent_t ev[8] = {};
   int sm_count = 148;
   // sharded LAMB (cfg.shard_lamb): flat parameter vector + per-rank norm table
@@ -895,13 +904,26 @@ int upload_hparams(sp_round* r, int step, cudaStream_t st) {
 
 // Captures the round into a CUDA graph the first time a (pointer set, mode)
 // is seen, then replays it; per-step scalars go through d_hp.
+void drop_graphs(sp_round* r) {
+  for (int k = 0; k < 2; ++k) {
+    if (r->gexec[k]) cudaGraphExecDestroy(r->gexec[k]);
+    r->gexec[k] = nullptr;
+    r->gkey[k].clear();
+  }
+}
+
 int launch_graph(sp_round* r, const std::vector<const void*>& key, const float* const* grads,
                  float* p, float* m, float* v, int step, cudaStream_t st) {
-  if (!r->gexec || key != r->gkey) {
-    if (r->gexec) {
+  int slot = -1;
+  for (int k = 0; k < 2; ++k)
+    if (r->gexec[k] && r->gkey[k] == key) slot = k;
+  if (slot < 0) {
+    slot = r->gnext;
+    r->gnext ^= 1;
+    if (r->gexec[slot]) {
       SP_CUDA(cudaStreamSynchronize(st));
-      cudaGraphExecDestroy(r->gexec);
-      r->gexec = nullptr;
+      cudaGraphExecDestroy(r->gexec[slot]);
+      r->gexec[slot] = nullptr;
     }
     cudaGraph_t graph;
     SP_CUDA(cudaStreamBeginCapture(r->own, cudaStreamCaptureModeThreadLocal));
@@ -909,14 +931,14 @@ int launch_graph(sp_round* r, const std::vector<const void*>& key, const float* 
     cudaError_t e = cudaStreamEndCapture(r->own, &graph);
     if (erc) return erc;
     if (e != cudaSuccess) return fail(SP_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
-    e = cudaGraphInstantiate(&r->gexec, graph, 0);
+    e = cudaGraphInstantiate(&r->gexec[slot], graph, 0);
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) return fail(SP_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
-    r->gkey = key;
+    r->gkey[slot] = key;
   }
   int rc = upload_hparams(r, step, st);
   if (rc) return rc;
-  SP_CUDA(cudaGraphLaunch(r->gexec, st));
+  SP_CUDA(cudaGraphLaunch(r->gexec[slot], st));
   return SP_OK;
 }
 
@@ -1086,7 +1108,7 @@ int sp_round_destroy(sp_round* r) {
   if (!r) return SP_OK;
   cudaSetDevice(r->cfg.device);
   cudaDeviceSynchronize();
-  if (r->gexec) cudaGraphExecDestroy(r->gexec);
+  drop_graphs(r);
   for (int k = 0; k < SP_MAX_RANKS; ++k)
     if (r->base[k] && k != r->cfg.rank) cudaIpcCloseMemHandle(r->base[k]);
   cudaFree(r->shared);
@@ -1101,6 +1123,12 @@ int sp_round_destroy(sp_round* r) {
   for (int b = 0; b < 2; ++b)
     for (int l = 0; l < SP_MAX_LOCAL; ++l) cudaFree(r->acc[b][l]);
   cudaFree(r->d_stage);
+  for (int b = 0; b < 2; ++b) {
+    for (int l = 0; l < SP_MAX_LOCAL; ++l) cudaFree(r->stg[b][l]);
+    if (r->stg_ready[b]) cudaEventDestroy(r->stg_ready[b]);
+    if (r->stg_free[b]) cudaEventDestroy(r->stg_free[b]);
+  }
+  if (r->h2d) cudaStreamDestroy(r->h2d);
   cudaFree(r->d_ritems);
   cudaFree(r->d_rq);
   cudaFree(r->d_repoch);
@@ -1141,10 +1169,7 @@ int sp_round_connect(sp_round* r, const void* all_handles) {
     r->base[k] = static_cast<char*>(p);
   }
   r->connected = true;
-  if (r->gexec) {
-    cudaGraphExecDestroy(r->gexec);
-    r->gexec = nullptr;
-  }
+  drop_graphs(r);
   return SP_OK;
 }
 
@@ -1175,10 +1200,7 @@ int sp_round_set_assignment(sp_round* r, const int64_t* offsets, const double* w
     if (rc) return rc;
   }
   r->assigned = true;
-  if (r->gexec) {
-    cudaGraphExecDestroy(r->gexec);
-    r->gexec = nullptr;
-  }
+  drop_graphs(r);
   return SP_OK;
 }
 
@@ -1195,6 +1217,56 @@ int sp_round_run(sp_round* r, const float* const* grads, float* p, float* m, flo
   key.push_back(v);
   key.push_back(nullptr);  // mode tag: caller-owned gradients, host weights
   return launch_graph(r, key, grads, p, m, v, step, st);
+}
+
+int sp_round_run_host(sp_round* r, const float* const* host_grads, float* p, float* m, float* v,
+                      int step, void* stream) {
+  if (!r || !host_grads) return fail(SP_ERR_ARG, "null argument");
+  SP_CUDA(cudaSetDevice(r->cfg.device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : r->own;
+  if (!r->h2d) {
+    SP_CUDA(cudaStreamCreateWithFlags(&r->h2d, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      SP_CUDA(cudaEventCreateWithFlags(&r->stg_ready[b], cudaEventDisableTiming));
+      SP_CUDA(cudaEventCreateWithFlags(&r->stg_free[b], cudaEventDisableTiming));
+    }
+  }
+  const int b = r->stg_next;
+  const float* grads[SP_MAX_LOCAL];
+  for (int l = 0; l < r->L; ++l) {
+    const int g = r->cfg.rank * r->L + l;
+    if (!host_grads[l]) {
+      if (r->weights.empty() || r->weights[g] != 0.0)
+        return fail(SP_ERR_ARG, "null host grad for a peer with nonzero weight");
+      grads[l] = nullptr;
+      continue;
+    }
+    if (!r->stg[b][l]) SP_CUDA(cudaMalloc(&r->stg[b][l], (size_t)r->npad * sizeof(float)));
+    grads[l] = r->stg[b][l];
+  }
+  int rc = check_run_args(r, grads, p, m, v);
+  if (rc) return rc;
+  // the round that last read staging buffer b (two calls ago) must be done
+  // before it is overwritten; the copy then overlaps the previous round
+  if (r->stg_used[b]) SP_CUDA(cudaStreamWaitEvent(r->h2d, r->stg_free[b], 0));
+  for (int l = 0; l < r->L; ++l)
+    if (grads[l])
+      SP_CUDA(cudaMemcpyAsync(r->stg[b][l], host_grads[l], (size_t)r->n * sizeof(float),
+                              cudaMemcpyHostToDevice, r->h2d));
+  SP_CUDA(cudaEventRecord(r->stg_ready[b], r->h2d));
+  SP_CUDA(cudaStreamWaitEvent(st, r->stg_ready[b], 0));
+  std::vector<const void*> key;
+  for (int l = 0; l < r->L; ++l) key.push_back(grads[l]);
+  key.push_back(p);
+  key.push_back(m);
+  key.push_back(v);
+  key.push_back(nullptr);
+  rc = launch_graph(r, key, grads, p, m, v, step, st);
+  if (rc) return rc;
+  SP_CUDA(cudaEventRecord(r->stg_free[b], st));
+  r->stg_used[b] = true;
+  r->stg_next = b ^ 1;
+  return SP_OK;
 }
 
 int sp_round_run_phased(sp_round* r, const float* const* grads, float* p, float* m, float* v,

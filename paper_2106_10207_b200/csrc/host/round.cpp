@@ -86,6 +86,11 @@ void AveragingRound::run(const float* const* grads, float* p, float* m, float* v
   check_status(sp_round_run(h_, grads, p, m, v, step, stream));
 }
 
+void AveragingRound::run_host(const float* const* host_grads, float* p, float* m, float* v, int step,
+                              void* stream) {
+  check_status(sp_round_run_host(h_, host_grads, p, m, v, step, stream));
+}
+
 sp_phase_times AveragingRound::run_phased(const float* const* grads, float* p, float* m, float* v,
                                           int step, void* stream) {
   sp_phase_times t{};

@@ -143,6 +143,27 @@ class AveragingRound:
                                          self._dptr(m, self.n), self._dptr(v, self.n),
                                          int(step), st))
 
+    def run_host(self, host_grads, p, m, v, step: int, stream=None) -> None:
+        """One round from HOST gradients (sp_round_run_host): pinned CPU
+        float32 tensors, copied to a double-buffered device staging area on
+        the round's copy stream, so this step's copy overlaps the previous
+        round. p, m, v stay device tensors."""
+        import torch
+
+        if len(host_grads) != self.L:
+            raise ValueError(f"expected {self.L} local gradients")
+        arr = (ctypes.c_void_p * self.L)()
+        for i, g in enumerate(host_grads):
+            if g is None:
+                continue
+            if g.is_cuda or g.dtype != torch.float32 or not g.is_contiguous() or g.numel() < self.n:
+                raise ValueError("host_grads: contiguous CPU float32 tensors of at least n elements")
+            arr[i] = g.data_ptr()
+        st = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
+        nat.check(self._lib.sp_round_run_host(self._h, arr, self._dptr(p, self.n),
+                                              self._dptr(m, self.n), self._dptr(v, self.n),
+                                              int(step), st))
+
     def run_phased(self, grads, p, m, v, step: int, stream=None) -> dict:
         st = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
         t = nat.SpPhaseTimes()

@@ -75,8 +75,12 @@ int main() {
   sp_oracle_lamb_hp hp{cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay, 1};
 
   int bad = 0;
-  for (int step = 1; step <= 2; ++step) {
-    rnd.run(gd.data(), pd, md, vd, step);
+  // steps 1-2: device gradients; steps 3-4: the same gradients from host
+  // memory through run_host (double-buffered staging, both buffers used)
+  std::vector<const float*> hp_ptrs = {gh[0].data(), gh[1].data(), gh[2].data(), gh[3].data()};
+  for (int step = 1; step <= 4; ++step) {
+    if (step <= 2) rnd.run(gd.data(), pd, md, vd, step);
+    else rnd.run_host(hp_ptrs.data(), pd, md, vd, step);
     CK(cudaDeviceSynchronize());
     std::vector<uint16_t> got((size_t)n);
     if (sp_round_read(rnd.handle(), SP_BUF_AVG, 0, 0, got.data(), (size_t)n * 2)) return 3;

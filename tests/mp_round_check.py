@@ -41,19 +41,11 @@ def main():
                     help="sharded LAMB: owners step their range, parameters pushed to all ranks")
     ap.add_argument("--accumulate", action="store_true",
                     help="device-side accumulation: per-peer micro-batches, sample-count weights")
-    ap.add_argument("--oversubscribe", action="store_true",
-                    help="more ranks than GPUs: rank r runs on GPU r %% count with gloo plumbing "
-                         "(checks the world-size logic, e.g. world 8 on a 1..4-GPU box; not a perf path)")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
-    if args.oversubscribe:
-        local %= torch.cuda.device_count()
-        torch.cuda.set_device(local)
-        dist.init_process_group("gloo")
-    else:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     L = args.peers_per_rank
     G = L * world
     sizes = [int(x) for x in args.sizes.split(",")]
@@ -150,8 +142,7 @@ def main():
                 errors.append(f"step {step}: {name} differs")
     # all replicas identical
     digest = torch.tensor([float(p.double().sum()),
-                           0.0 if args.shard_lamb else float(m.double().sum())],
-                          device="cpu" if args.oversubscribe else "cuda")
+                           0.0 if args.shard_lamb else float(m.double().sum())], device="cuda")
     allg = [torch.zeros_like(digest) for _ in range(world)]
     dist.all_gather(allg, digest)
     if any(not torch.equal(allg[0], x) for x in allg):

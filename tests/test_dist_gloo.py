@@ -1,6 +1,8 @@
-"""Multi-rank host logic on CPU (torch.distributed gloo, world size 2): the
-IPC-handle all-gather, plan agreement across ranks and rank ranges. The
-GPU data path itself is covered by tests/test_multigpu.py."""
+"""Multi-rank host logic on CPU (torch.distributed gloo, world sizes 2 and 8):
+the IPC-handle all-gather, plan agreement across ranks and rank ranges. World
+8 is the driver's 8-GPU scaling run, which no test box here reaches (the
+GPU data path is covered up to 4 GPUs by tests/test_multigpu.py; ranks that
+spin on each other must never share a GPU)."""
 import json
 import os
 import socket
@@ -23,7 +25,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, spec_json, q):
+def _worker(rank, world, port, spec_json, q, L):
     sys.path.insert(0, ROOT)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -34,7 +36,7 @@ def _worker(rank, world, port, spec_json, q):
         blob = D.exchange_handles(bytes([rank]) * 64)
         plan = D.plan_round(spec_json, 17847474, 8)
         D.check_same_plan(plan["offsets"], plan["weights"])
-        lo, hi = D.rank_range(plan["offsets"], rank, 4)
+        lo, hi = D.rank_range(plan["offsets"], rank, L)
         bad = None
         try:  # a rank with a different plan must be refused on every rank
             D.check_same_plan(plan["offsets"], [w + rank for w in plan["weights"]])
@@ -45,23 +47,35 @@ def _worker(rank, world, port, spec_json, q):
         dist.destroy_process_group()
 
 
-def test_gloo_world2_host_logic():
+@pytest.mark.parametrize("world", [2, 8])
+def test_gloo_host_logic(world):
     sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from golden.fleets import spec_json
+    from golden.fleets import FRACTIONS_APPENDIX_A, spec_json
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    sj = spec_json("het8c")
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, sj, q)) for r in range(2)]
+    sj = spec_json("het8c")  # 8 peers: L = 8 / world per rank
+    L = 8 // world
+    procs = [ctx.Process(target=_worker, args=(r, world, port, sj, q, L)) for r in range(world)]
     for p in procs:
         p.start()
-    res = sorted(q.get(timeout=180) for _ in range(2))
+    res = sorted(q.get(timeout=240) for _ in range(world))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    (r0, b0, o0, lo0, hi0, bad0), (r1, b1, o1, lo1, hi1, bad1) = res
-    assert b0 == b1 == bytes([0]) * 64 + bytes([1]) * 64  # rank order
-    assert o0 == o1  # deterministic LP: identical plans on every rank
-    assert (lo0, hi1) == (0, 17847474) and hi0 == lo1  # 2 ranks x 4 peers tile the vector
-    assert bad0 and bad1 and "disagree" in bad0
+    want_blob = b"".join(bytes([r]) * 64 for r in range(world))
+    for r, (rank, blob, offs, lo, hi, bad) in enumerate(res):
+        assert rank == r
+        assert blob == want_blob  # rank order
+        assert offs == res[0][2]  # deterministic LP: identical plans on every rank
+        assert bad and "disagree" in bad  # a rank with a different plan is refused everywhere
+        assert (lo, hi) == (offs[r * L], offs[(r + 1) * L])
+    # ranks tile the vector: contiguous, first at 0, last at n
+    assert res[0][3] == 0 and res[-1][4] == 17847474
+    assert all(res[k][4] == res[k + 1][3] for k in range(world - 1))
+    if world == 8:  # het8c: 1/20 x6, a client with nothing, 7/10
+        sizes = [hi - lo for (_, _, _, lo, hi, _) in res]
+        want = [f * 17847474 for f in FRACTIONS_APPENDIX_A["het8c"]]
+        assert sizes[6] == 0
+        assert all(abs(s - w) <= 8 for s, w in zip(sizes, want))

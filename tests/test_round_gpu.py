@@ -33,7 +33,7 @@ def _dev(x):
 
 
 def _run_case(wire, fractions, weights, sizes, steps=1, block=4096, warm=False, seed=11,
-              shard=False):
+              shard=False, offsets=None):
     G = len(fractions)
     n = sum(sizes)
     grads_h = [O.fill_synthetic(n, seed, g, SIGMA) for g in range(G)]
@@ -62,6 +62,8 @@ def _run_case(wire, fractions, weights, sizes, steps=1, block=4096, warm=False, 
         p_d = pb
     offs = rnd.assign(fractions, weights)
     assert offs[0] == 0 and offs[-1] == n
+    if offsets is not None:  # the host LP's plan (C++ part_offsets) == the Python mirror
+        assert list(offs) == list(offsets)
 
     # device synthetic generator == host generator, bit for bit
     for g in range(G):
@@ -108,6 +110,20 @@ def _run_case(wire, fractions, weights, sizes, steps=1, block=4096, warm=False, 
 ])
 def test_round_parity_ragged(wire, fractions, weights):
     _run_case(wire, fractions, weights, RAGGED, block=4096 if wire != "q8" else 4096)
+
+
+@pytest.mark.parametrize("fleet,wire", [("het8c", "fp16"), ("het4b", "fp32"), ("het8c", "q8"),
+                                        ("aux_server", "fp16")])
+def test_round_parity_lp_planned(fleet, wire):
+    # the whole north-star chain on one GPU: spec -> solve_strategy ->
+    # part_offsets -> GPU round with the LP's sample counts as weights
+    from paper_2106_10207_b200.dist import plan_round
+    from paper_2106_10207_b200.fleets import spec_json
+
+    n = sum(RAGGED)
+    plan = plan_round(spec_json(fleet), n, 4096 if wire == "q8" else 8)
+    assert abs(sum(plan["fractions"]) - 1.0) < 1e-9
+    _run_case(wire, plan["fractions"], plan["weights"], RAGGED, offsets=plan["offsets"])
 
 
 @pytest.mark.parametrize("wire", ["fp32", "fp16", "q8"])
@@ -359,3 +375,40 @@ def test_dpu_overlap_accumulate_during_round(wire):
     rnd.close()
     for a, b in ((p1, p2), (m1, m2), (v1, v2)):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("wire,shard", [("fp16", False), ("q8", False), ("fp32", True)])
+def test_run_host_matches_device_round(wire, shard):
+    # sp_round_run_host: pinned host gradients, double-buffered staging on a
+    # copy stream (two cached graphs); must equal sp_round_run bit for bit
+    sizes = RAGGED
+    n = sum(sizes)
+    G = 2
+    fr, w = [0.5, 0.5], [3.0, 5.0]
+    outs = []
+    for use_host in (False, True):
+        rnd = AveragingRound(n, sizes, wire=wire, peers_per_rank=G, lr=HP["lr"], eps=HP["eps"],
+                             weight_decay=HP["weight_decay"], shard_lamb=shard)
+        rnd.assign(fr, w)
+        p = rnd.param_buffer() if shard else torch.empty(n, device="cuda")
+        fill_synthetic(p, 5, 0, 0.02, 0)
+        m = torch.zeros(n, device="cuda")
+        v = torch.zeros(n, device="cuda")
+        for step in range(1, 5):  # different gradients every step
+            grads = []
+            for g in range(G):
+                t = torch.empty(n, device="cuda")
+                fill_synthetic(t, 40 + step, g, SIGMA)
+                grads.append(t)
+            if use_host:
+                hg = [t.cpu().pin_memory() for t in grads]
+                torch.cuda.synchronize()
+                rnd.run_host(hg, p, m, v, step)
+                del grads
+            else:
+                rnd.run(grads, p, m, v, step)
+            torch.cuda.synchronize()
+        outs.append([x.cpu().numpy().copy() for x in (p, m, v)])
+        rnd.close()
+    for a, b, name in zip(outs[0], outs[1], "pmv"):
+        np.testing.assert_array_equal(a, b, err_msg=name)
