@@ -620,6 +620,7 @@ int enqueue_shard_lamb(sp_round* r, const LambArgs& la, const BarrierArgs& ba, c
     ParamPush pp{};
     pp.ndst = c.world;
     for (int k = 0; k < c.world; ++k) pp.dst[k] = r->param((c.rank + 1 + k) % c.world);
+
     if (nS > 0) {
       switch (c.wire) {
         case SP_WIRE_FP32: k_lamb_update_push<SP_WIRE_FP32><<<nS, kLambThreads, 0, st>>>(ls, pp); break;

@@ -237,6 +237,72 @@ StrategyProblem build_lp(const CollaborationSpec& spec) {
   return sp;
 }
 
+// Canonical tie-break among optimal strategies. Peers with identical specs
+// (and the same duty cycle in the solution) are interchangeable: permuting
+// them maps the program of every stage onto itself, so averaging the
+// solution over those permutations stays feasible and keeps every stage's
+// objective (linear ones exactly, stage C's concave sum of minima cannot
+// drop below its optimum). The vertex the simplex stops at is arbitrary when
+// the optimum is not unique -- two identical peers can come back as
+// fractions [1, 0] ("multiple optimal strategies with equal
+// training throughputs") -- while the averaged point is the symmetric one
+// (an interior-point solver's answer). Peers named in a
+// per-link limit keep their own class.
+static void symmetrize(const CollaborationSpec& spec, StrategyAssignment& out) {
+  const int n = spec.size();
+  std::vector<int> cls(n, -1);
+  std::vector<std::vector<int>> members;
+  std::vector<bool> linked(n, false);
+  for (const LinkLimit& l : spec.links) {
+    if (l.from >= 0 && l.from < n) linked[l.from] = true;
+    if (l.to >= 0 && l.to < n) linked[l.to] = true;
+  }
+  for (int i = 0; i < n; ++i) {
+    const PeerSpec& p = spec.peers[i];
+    for (std::size_t k = 0; k < members.size() && cls[i] < 0; ++k) {
+      const int j = members[k][0];
+      const PeerSpec& q = spec.peers[j];
+      if (!linked[i] && !linked[j] && p.samples_per_sec == q.samples_per_sec &&
+          p.download_bps == q.download_bps && p.upload_bps == q.upload_bps &&
+          p.can_compute == q.can_compute && p.client_mode == q.client_mode &&
+          out.compute[i] == out.compute[j] && std::fabs(out.c_raw[i] - out.c_raw[j]) <= 1e-9)
+        cls[i] = static_cast<int>(k);
+    }
+    if (cls[i] < 0) {
+      cls[i] = static_cast<int>(members.size());
+      members.push_back({});
+    }
+    members[cls[i]].push_back(i);
+  }
+  if (static_cast<int>(members.size()) == n) return;  // no two peers interchangeable
+  for (Eigen::MatrixXd* mat : {&out.a, &out.g}) {
+    Eigen::MatrixXd& m = *mat;
+    const Eigen::MatrixXd src = m;
+    for (const auto& A : members)
+      for (const auto& B : members) {
+        double off = 0.0, diag = 0.0;
+        int noff = 0, ndiag = 0;
+        for (int i : A)
+          for (int j : B) {
+            if (i == j) {
+              diag += src(i, j);
+              ++ndiag;
+            } else {
+              off += src(i, j);
+              ++noff;
+            }
+          }
+        for (int i : A)
+          for (int j : B) m(i, j) = i == j ? diag / ndiag : off / noff;
+      }
+  }
+  for (const auto& A : members) {
+    double c = 0.0;
+    for (int i : A) c += out.c_raw[i];
+    for (int i : A) out.c_raw[i] = c / A.size();
+  }
+}
+
 StrategyAssignment solve_strategy(const CollaborationSpec& spec, const SolveOptions& opts) {
   require_valid(spec);
   const int n = spec.size();
@@ -403,6 +469,7 @@ StrategyAssignment solve_strategy(const CollaborationSpec& spec, const SolveOpti
   }
   out.xi = x(cp.xi()) * s.xi_scale;
   out.lp_iterations = static_cast<int>(solver.iterations());
+  symmetrize(spec, out);
 
   // fractions_i = min_{j in R} g_ij / sum_k min_{j in R} g_kj;
   // if every reducer misses some recipient, fall back to outbound mass

@@ -296,3 +296,30 @@ def test_measured_fractions_per_algorithm():
     assert fractions_for(sj, "allreduce") == [0.25] * 4
     assert fractions_for(sj, "parameter_server") == [0.0, 0.0, 0.0, 1.0]
     np.testing.assert_allclose(fractions_for(sj, "adaptive"), [1 / 22] * 3 + [19 / 22], atol=1e-9)
+
+
+@pytest.mark.parametrize("n", [2, 3, 5, 6])
+def test_symmetric_fleets_get_symmetric_fractions(n):
+    # the LP optimum of a homogeneous fleet is not unique for every n (two
+    # peers: [1, 0] and [0.5, 0.5] tie); solve_strategy returns the average
+    # over interchangeable peers, which keeps every stage optimal
+    spec = homogeneous(n, 1.0, 1000.0, 4096.0, 17847474)
+    s = sp.solve_strategy(_sj(spec))
+    np.testing.assert_allclose(s["fractions"], [1.0 / n] * n, rtol=1e-12)
+    check_assignment(spec, s)
+
+
+@pytest.mark.parametrize("name", ["table1_c", "daynight", "table1_d", "aux_server"])
+def test_symmetrized_assignment_feasible(name):
+    spec = json.loads(spec_json(name))
+    s = sp.solve_strategy(spec_json(name))
+    check_assignment(spec, s)
+    assert s["steps_per_sec"] == pytest.approx(XI_GOLDEN[name], rel=1e-9)
+    # interchangeable peers (same spec and duty cycle) get equal fractions
+    groups = {}
+    for p, f, c in zip(spec["peers"], s["fractions"], s["duty_cycle"]):
+        key = (p["samples_per_sec"], p["download_mbps"], p["upload_mbps"],
+               p.get("can_compute", True), p.get("client_mode", False), round(c, 9))
+        groups.setdefault(key, []).append(f)
+    for fs in groups.values():
+        assert max(fs) - min(fs) <= 1e-12
