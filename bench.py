@@ -270,7 +270,16 @@ def rank_model(r, offsets, L, world, n, b, wire, shard, fused, fused_pack) -> di
 
 
 def round_roofline(models, n, peak) -> float:
-    """Seconds: sum over phases of the slowest rank's max(HBM, NVLink) time."""
+    """Seconds: HBM and NVLink phases serialized, each on its
+    critical-path rank: max_r HBM_r / peak + max_r NVL_r / NVLink."""
+    return (max(m["hbm"] for m in models) * n / (peak * 1e9)
+            + max(m["nvl"] for m in models) * n / (NVLINK_GBS * 1e9))
+
+
+def overlap_roofline(models, n, peak) -> float:
+    """Seconds, a tighter bound: within each barrier-separated phase (pack +
+    scatter, reduce, LAMB [+ parameter push]) HBM and NVLink traffic overlap,
+    so the phase costs the slowest rank's max(HBM time, NVLink time)."""
     t = 0.0
     for k in range(3):
         t += max(max(m["phases"][k][0] * n / (peak * 1e9), m["phases"][k][1] * n / (NVLINK_GBS * 1e9))
@@ -510,6 +519,7 @@ def main():
         hbm_round = max(x["hbm"] for x in models)
         nvl_round = max(x["nvl"] for x in models)
         t_roof = round_roofline(models, n, peak)
+        t_ovl = overlap_roofline(models, n, peak)
         lp_times = None
         try:
             lp_times = lp_solve_times()
@@ -566,12 +576,17 @@ def main():
                          "traffic": ncu_traffic(kname) if table == "albert-large" else None,
                          "algorithmic_bytes": alg[dom],
                          "peak_kind": peak_kind if bound == "hbm" else "measured peer copy per direction (B200_PROFILING.md)"},
-            "round_roofline": {"t_roof_us": round(t_roof * 1e6, 2),
-                               "frac": round(t_roof * 1e3 / ms_step, 4),
+            # primary: the overlap bound (a lower bound on the round time; the
+            # §8d serialized sum is not one: large N=4 rounds beat it)
+            "round_roofline": {"t_roof_us": round(t_ovl * 1e6, 2),
+                               "frac": round(t_ovl * 1e3 / ms_step, 4),
                                "hbm_B_per_param": round(hbm_round, 3),
                                "nvlink_B_per_param_dir": round(nvl_round, 3),
-                               "model": f"sum over phases (pack+scatter, reduce, LAMB[+param push]) of the "
-                                        f"slowest rank's max(HBM B/{peak:g} GB/s, NVLink B/{NVLINK_GBS:g} GB/s)"},
+                               "model": f"sum over barrier-separated phases (pack+scatter, reduce, "
+                                        f"LAMB[+param push]) of the slowest rank's max(HBM B/{peak:g}, "
+                                        f"NVLink B/{NVLINK_GBS:g} GB/s)",
+                               "t_roof_serialized_us": round(t_roof * 1e6, 2),
+                               "frac_serialized": round(t_roof * 1e3 / ms_step, 4)},
             "e2e": {"value": round(e2e_value, 3), "unit": "GB/s",
                     "round_us": round(e2e_step * 1e3, 2),
                     "h2d_bytes_per_step": 4 * n * L, "d2h_bytes_per_step": 4 * len(tsizes),

@@ -1279,11 +1279,8 @@ struct ParamPush {
 
 // Pass 2 of the owned chunks: p' = p - lr*trust*u, stored into every rank's
 // copy (the local one last, so the local read of p precedes the local write).
-template <int W>
-__global__ void __launch_bounds__(kLambThreads) k_lamb_update_push(LambArgs a, ParamPush d) {
-  const Chunk c = a.chunks[blockIdx.x];
-  const LambScalars s{a.hp[0], a.hp[1], a.hp[2]};
-  const float neg = -__ldcg(a.step_scale + c.tensor);
+__device__ __forceinline__ void lamb_push_chunk(const LambArgs& a, const LambScalars& s, const Chunk& c,
+                                                float neg, const ParamPush& d) {
   const ChunkSplit sp = split_chunk(c);
   const int t = threadIdx.x;
   int64_t si = -1;
@@ -1323,6 +1320,189 @@ __global__ void __launch_bounds__(kLambThreads) k_lamb_update_push(LambArgs a, P
     const int4 o = make_int4(__float_as_int(q.x), __float_as_int(q.y), __float_as_int(q.z),
                              __float_as_int(q.w));
     for (int j = 0; j < d.ndst; ++j) st_v4(d.dst[j] + i, o);
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(kLambThreads) k_lamb_update_push(LambArgs a, ParamPush d) {
+  const Chunk c = a.chunks[blockIdx.x];
+  const LambScalars s{a.hp[0], a.hp[1], a.hp[2]};
+  lamb_push_chunk(a, s, c, -__ldcg(a.step_scale + c.tensor), d);
+}
+
+// ------------------------------------------- sharded LAMB, one kernel (N1)
+// The chain above (pass 1 -> norms -> barrier -> trust -> pass 2 + push)
+// as one persistent kernel over a work queue of this rank's chunks:
+//   pass-1 item: moments + chunk partial; the CTA finishing the tensor's
+//     last chunk sums the partials in fp64 (k_shard_norms' order), stores the
+//     pair into slot [rank][t] of every rank's norm table and release-stores
+//     the round's epoch into flag [rank][t] of every rank;
+//   pass-2 item: waits for the world flags of its tensor, forms the trust
+//     ratio from the world slots in rank order (k_shard_trust's arithmetic),
+//     updates the chunk and stores p' into every rank's parameter vector.
+// Pass-2 items of tensor t are queued `lag` items after its last pass-1
+// item, so the NVLink push of early tensors can overlap the HBM-bound pass 1
+// of later ones. Measured (4x B200, profiles/r01/shard_fused.txt): no faster
+// than the chain at 268M elements and 1.4-2.5x slower at ALBERT-large size
+// (pass-2 items wait on the slowest chunk of their tensor on every rank, and
+// the push needs every CTA to keep NVLink busy), so it is opt-in
+// (SP_SHARD_FUSED=1) and kept bit-exact by the tests. Items only wait on earlier items of this rank's queue and
+// on other GPUs' pass 1, which progresses independently: no deadlock. The
+// last CTA out waits for every flag, writes trust / step_scale for all
+// tensors (what read_trust() returns) and resets the queue; flags carry
+// the epoch, so nothing needs clearing between graph replays.
+struct ShardFused {
+  const int* items;                         // >= 0 pass-1 chunk, < 0 ~chunk (pass 2 + push)
+  int nitems;
+  int* work;
+  int* exited;
+  int* done;                                // per tensor: pass-1 chunks finished
+  const int2* tchunks;                      // this rank's chunks of tensor t
+  double2* table[SP_MAX_RANKS];             // norm table of rank (rank + 1 + k) % world
+  unsigned long long* flags[SP_MAX_RANKS];  // norm flags of the same ranks
+  const double2* my_table;                  // [world][T]
+  const unsigned long long* my_flags;       // [world][T]
+  unsigned long long* epoch;                // local round counter
+  float* trust;
+  float* step_scale;
+  ParamPush push;
+  int rank, world, T;
+  int* err;
+  unsigned long long timeout_ns;
+};
+
+__device__ __forceinline__ bool wait_norms(const ShardFused& f, int t, unsigned long long e) {
+  const unsigned long long t0 = globaltimer();
+  for (int k = 0; k < f.world; ++k)
+    while (ld_acquire_sys(f.my_flags + (size_t)k * f.T + t) < e) {
+      if (globaltimer() - t0 > f.timeout_ns) {
+        atomicExch_system(f.err, 1);
+        return false;
+      }
+      __nanosleep(256);  // hundreds of CTAs may poll: keep them off the memory system
+    }
+  return true;
+}
+
+__device__ __forceinline__ float shard_trust(const ShardFused& f, int t) {
+  double x = 0.0, y = 0.0;
+  for (int k = 0; k < f.world; ++k) {
+    const double2 v = __ldcg(f.my_table + (size_t)k * f.T + t);
+    x += v.x;
+    y += v.y;
+  }
+  const double r1 = sqrt(x), r2 = sqrt(y);
+  return (r1 > 0.0 && r2 > 0.0) ? (float)(r1 / r2) : 1.0f;
+}
+
+// thread 0..world-1 store the pair, then thread 0 publishes the epoch
+__device__ __forceinline__ void publish_norms(const ShardFused& f, int t, double x, double y,
+                                              unsigned long long e) {
+  if (threadIdx.x < f.world) {
+    f.table[threadIdx.x][(size_t)f.rank * f.T + t] = make_double2(x, y);
+    __threadfence_system();
+  }
+  __syncthreads();
+  if (threadIdx.x < f.world) st_release_sys(f.flags[threadIdx.x] + (size_t)f.rank * f.T + t, e);
+}
+
+template <int W>
+__global__ void __launch_bounds__(kLambThreads, 4) k_shard_lamb_fused(LambArgs a,
+                                                                                     ShardFused f) {
+  __shared__ int s_item, s_last;
+  __shared__ float s_neg;
+  __shared__ unsigned long long s_epoch;
+  __shared__ float red_p[kLambThreads / 32], red_u[kLambThreads / 32];
+  __shared__ double dred_p[kLambThreads], dred_u[kLambThreads];
+  const LambScalars s{a.hp[0], a.hp[1], a.hp[2]};
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) s_epoch = *f.epoch + 1;
+  __syncthreads();
+  const unsigned long long e = s_epoch;
+  // tensors with no chunk on this rank contribute a zero pair
+  for (int t = blockIdx.x; t < f.T; t += gridDim.x) {
+    const int2 r = f.tchunks[t];
+    if (r.y <= r.x) publish_norms(f, t, 0.0, 0.0, e);
+    __syncthreads();
+  }
+  int next = 0;
+  if (tid == 0) next = atomicAdd(f.work, 1);
+  for (;;) {
+    if (tid == 0) s_item = next;
+    __syncthreads();
+    const int it = s_item;
+    __syncthreads();
+    if (it >= f.nitems) break;
+    if (tid == 0) next = atomicAdd(f.work, 1);
+    const int code = f.items[it];
+    if (code >= 0) {
+      const Chunk c = a.chunks[code];
+      float pp = 0.0f, uu = 0.0f;
+      lamb_pass1<W>(a, s, c, pp, uu);
+      pp = warp_sum(pp);
+      uu = warp_sum(uu);
+      if (lane == 0) {
+        red_p[wid] = pp;
+        red_u[wid] = uu;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        float sp_ = 0.0f, su = 0.0f;
+#pragma unroll
+        for (int w = 0; w < kLambThreads / 32; ++w) {
+          sp_ += red_p[w];
+          su += red_u[w];
+        }
+        a.partial[code] = make_float2(sp_, su);
+        __threadfence();
+        const int2 r = f.tchunks[c.tensor];
+        s_last = atomicAdd(f.done + c.tensor, 1) == r.y - r.x - 1;
+      }
+      __syncthreads();
+      if (s_last) {  // this rank's partials of the tensor are all in
+        __threadfence();
+        const int2 r = f.tchunks[c.tensor];
+        double dp = 0.0, du = 0.0;
+        for (int q = r.x + tid; q < r.y; q += kLambThreads) {
+          const float2 v = __ldcg(a.partial + q);
+          dp += (double)v.x;
+          du += (double)v.y;
+        }
+        dred_p[tid] = dp;
+        dred_u[tid] = du;
+        __syncthreads();
+        for (int h = kLambThreads / 2; h > 0; h >>= 1) {
+          if (tid < h) {
+            dred_p[tid] += dred_p[tid + h];
+            dred_u[tid] += dred_u[tid + h];
+          }
+          __syncthreads();
+        }
+        if (tid == 0) f.done[c.tensor] = 0;
+        publish_norms(f, c.tensor, dred_p[0], dred_u[0], e);
+      }
+    } else {
+      const Chunk c = a.chunks[~code];
+      if (tid == 0) {
+        s_neg = wait_norms(f, c.tensor, e) ? -__fmul_rn(s.lr, shard_trust(f, c.tensor)) : 0.0f;
+      }
+      __syncthreads();
+      lamb_push_chunk(a, s, c, s_neg, f.push);
+    }
+  }
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(f.exited, 1) == (int)gridDim.x - 1) {  // last CTA out
+      for (int t = 0; t < f.T; ++t) {
+        const float tr = wait_norms(f, t, e) ? shard_trust(f, t) : 1.0f;
+        f.trust[t] = tr;
+        f.step_scale[t] = __fmul_rn(s.lr, tr);
+      }
+      *f.work = 0;
+      *f.exited = 0;
+      *f.epoch = e;
+      __threadfence();
+    }
   }
 }
 

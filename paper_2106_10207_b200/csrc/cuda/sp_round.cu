@@ -126,7 +126,15 @@ struct sp_round {
   int sm_count = 148;
   // sharded LAMB (cfg.shard_lamb): flat parameter vector + per-rank norm table
   bool shard = false;
-  size_t param_off = 0, norms_off = 0;
+  size_t param_off = 0, norms_off = 0, nflags_off = 0;
+  // one-kernel sharded LAMB (k_shard_lamb_fused): its own work list, grid,
+  // epoch, and the norm flags in the shared allocation
+  bool shard_fused = false;  // opt-in (SP_SHARD_FUSED=1): measured slower than the chain
+  int shard_lag = 0;      // pass-2 items of tensor t queued this many items after its pass 1
+  int shard_grid = 0;
+  int* d_sitems = nullptr;
+  int nsitems = 0;
+  unsigned long long* d_sepoch = nullptr;
   // hybrid split: tensors [0, shard_t0) (elements [0, shard_cut)) keep the
   // replicated LAMB on a second stream, tensors [shard_t0, T) are sharded
   int shard_t0 = 0;
@@ -136,6 +144,9 @@ struct sp_round {
 
   float* param(int rank) const { return reinterpret_cast<float*>(base[rank] + param_off); }
   double2* norms(int rank) const { return reinterpret_cast<double2*>(base[rank] + norms_off); }
+  unsigned long long* nflags(int rank) const {
+    return reinterpret_cast<unsigned long long*>(base[rank] + nflags_off);
+  }
   char* wire(int rank, int g) const {
     return base[rank] + flags_bytes + ctr_bytes + (size_t)g * buf_bytes;
   }
@@ -333,6 +344,32 @@ int build_lamb_tables(sp_round* r, bool with_cuts) {
   }
   r->nchunks = (int)chunks.size();
   r->nitems = (int)items.size();
+  if (r->shard && r->d_sitems) {
+    // one-kernel sharded LAMB (used when nothing is replicated): pass-1
+    // items in chunk order, pass 2 of tensor t `shard_lag` items after its
+    // last pass-1 chunk
+    std::vector<int> si;
+    std::vector<std::pair<int, size_t>> pend;
+    size_t head = 0;
+    const size_t lag = (size_t)std::max(0, r->shard_lag);
+    auto flush = [&](bool all) {
+      while (head < pend.size() && (all || pend[head].second + lag <= si.size())) {
+        const int2 rg = tch[(size_t)pend[head].first];
+        for (int c = rg.x; c < rg.y; ++c) si.push_back(~c);
+        ++head;
+      }
+    };
+    for (size_t c = 0; c < chunks.size(); ++c) {
+      si.push_back((int)c);
+      if ((int)c == tch[(size_t)chunks[c].tensor].y - 1) pend.push_back({chunks[c].tensor, si.size()});
+      flush(false);
+    }
+    flush(true);
+    r->nsitems = (int)si.size();
+    SP_CUDA(cudaSetDevice(r->cfg.device));
+    if (!si.empty())
+      SP_CUDA(cudaMemcpy(r->d_sitems, si.data(), si.size() * sizeof(int), cudaMemcpyHostToDevice));
+  }
   r->h_chunks = chunks;
   SP_CUDA(cudaSetDevice(r->cfg.device));
   SP_CUDA(cudaMemcpy(r->d_chunks, chunks.data(), chunks.size() * sizeof(Chunk), cudaMemcpyHostToDevice));
@@ -589,6 +626,53 @@ int enqueue_shard_lamb(sp_round* r, const LambArgs& la, const BarrierArgs& ba, c
   LambArgs ls = la;  // the sharded chunks follow the replicated ones in the table
   ls.chunks = r->d_chunks + nR;
   ls.partial = r->d_partial + nR;
+  ParamPush pp{};
+  pp.ndst = c.world;
+  for (int k = 0; k < c.world; ++k) pp.dst[k] = r->param((c.rank + 1 + k) % c.world);
+  // (the choice must not depend on this rank's item count: a rank that owns
+  // nothing still publishes zero norms through the same protocol)
+  if (t0 < T && nR == 0 && r->shard_fused) {
+    // the whole sharded step as one persistent kernel (k_shard_lamb_fused)
+    ShardFused f{};
+    f.items = r->d_sitems;
+    f.nitems = r->nsitems;
+    f.work = r->d_qstate;
+    f.exited = r->d_qstate + 1;
+    f.done = r->d_qstate + 2;
+    f.tchunks = r->d_tchunks;
+    for (int k = 0; k < c.world; ++k) {
+      f.table[k] = r->norms((c.rank + 1 + k) % c.world);
+      f.flags[k] = r->nflags((c.rank + 1 + k) % c.world);
+    }
+    f.my_table = r->norms(c.rank);
+    f.my_flags = r->nflags(c.rank);
+    f.epoch = r->d_sepoch;
+    f.trust = r->d_trust;
+    f.step_scale = r->d_step_scale;
+    f.push = pp;
+    f.rank = c.rank;
+    f.world = c.world;
+    f.T = T;
+    f.err = r->d_err;
+    f.timeout_ns = (unsigned long long)((c.barrier_timeout_s > 0 ? c.barrier_timeout_s : 20.0) * 1e9);
+    const int g = std::max(1, std::min(r->shard_grid, r->nsitems));
+    switch (c.wire) {
+      case SP_WIRE_FP32: k_shard_lamb_fused<SP_WIRE_FP32><<<g, kLambThreads, 0, st>>>(ls, f); break;
+      case SP_WIRE_FP16: k_shard_lamb_fused<SP_WIRE_FP16><<<g, kLambThreads, 0, st>>>(ls, f); break;
+      default: k_shard_lamb_fused<SP_WIRE_Q8><<<g, kLambThreads, 0, st>>>(ls, f); break;
+    }
+    SP_CUDA(cudaGetLastError());
+    if (ev) {
+      SP_CUDA(cudaEventRecord(ev[5], st));
+      SP_CUDA(cudaEventRecord(ev[6], st));
+    }
+    if (c.world > 1) {  // every owner's parameters have landed everywhere
+      k_barrier<<<1, 32, 0, st>>>(ba);
+      SP_CUDA(cudaGetLastError());
+    }
+    if (ev) SP_CUDA(cudaEventRecord(ev[7], st));
+    return SP_OK;
+  }
   if (t0 < T) {
     if (nS > 0) {
       switch (c.wire) {
@@ -617,10 +701,6 @@ int enqueue_shard_lamb(sp_round* r, const LambArgs& la, const BarrierArgs& ba, c
                                                         r->d_trust, r->d_step_scale);
     SP_CUDA(cudaGetLastError());
     if (ev) SP_CUDA(cudaEventRecord(ev[6], st));
-    ParamPush pp{};
-    pp.ndst = c.world;
-    for (int k = 0; k < c.world; ++k) pp.dst[k] = r->param((c.rank + 1 + k) % c.world);
-
     if (nS > 0) {
       switch (c.wire) {
         case SP_WIRE_FP32: k_lamb_update_push<SP_WIRE_FP32><<<nS, kLambThreads, 0, st>>>(ls, pp); break;
@@ -995,7 +1075,8 @@ int sp_round_create(const sp_round_cfg* cfg, sp_round** out) {
     r->fused_round = false;
     r->param_off = r->shared_bytes;
     r->norms_off = r->param_off + round_up(r->npad * 4, 256);
-    r->shared_bytes = r->norms_off + round_up((int64_t)cfg->world * cfg->num_tensors * 16, 256);
+    r->nflags_off = r->norms_off + round_up((int64_t)cfg->world * cfg->num_tensors * 16, 256);
+    r->shared_bytes = r->nflags_off + round_up((int64_t)cfg->world * cfg->num_tensors * 8, 256);
   }
   int dev_sms = 0;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, cfg->device);
@@ -1038,6 +1119,23 @@ int sp_round_create(const sp_round_cfg* cfg, sp_round** out) {
       (e = cudaMalloc(&r->d_items, 2 * (size_t)r->nchunks_cap * sizeof(int))) != cudaSuccess ||
       (e = cudaMalloc(&r->epoch, sizeof(unsigned long long))) != cudaSuccess)
     return cleanup(fail(SP_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e)));
+  if (r->shard) {
+    if (const char* e2 = std::getenv("SP_SHARD_FUSED")) r->shard_fused = e2[0] == '1';
+    if (const char* e2 = std::getenv("SP_SHARD_LAG")) r->shard_lag = std::max(0, std::atoi(e2));
+    int per_sm = 0;
+    cudaError_t oe;
+    switch (cfg->wire) {
+      case SP_WIRE_FP32: oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_shard_lamb_fused<SP_WIRE_FP32>, kLambThreads, 0); break;
+      case SP_WIRE_FP16: oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_shard_lamb_fused<SP_WIRE_FP16>, kLambThreads, 0); break;
+      default: oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_shard_lamb_fused<SP_WIRE_Q8>, kLambThreads, 0); break;
+    }
+    if (oe != cudaSuccess || per_sm < 1) return cleanup(fail(SP_ERR_CUDA, "occupancy query failed for the sharded LAMB kernel"));
+    r->shard_grid = per_sm * r->sm_count;
+    if ((e = cudaMalloc(&r->d_sitems, 2 * (size_t)r->nchunks_cap * sizeof(int))) != cudaSuccess ||
+        (e = cudaMalloc(&r->d_sepoch, sizeof(unsigned long long))) != cudaSuccess)
+      return cleanup(fail(SP_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e)));
+    cudaMemset(r->d_sepoch, 0, sizeof(unsigned long long));
+  }
   if (int rc2 = build_lamb_tables(r, false)) return cleanup(rc2);
   {
     const char* env = std::getenv("SP_LAMB_UNFUSED");
@@ -1120,6 +1218,8 @@ int sp_round_destroy(sp_round* r) {
   cudaFree(r->d_step_scale);
   cudaFree(r->d_hp);
   cudaFree(r->d_items);
+  cudaFree(r->d_sitems);
+  cudaFree(r->d_sepoch);
   cudaFree(r->d_qstate);
   for (int b = 0; b < 2; ++b)
     for (int l = 0; l < SP_MAX_LOCAL; ++l) cudaFree(r->acc[b][l]);

@@ -11,13 +11,13 @@ import bench  # noqa: E402
 
 
 def main(paths):
-    print("| N | params | wire | LAMB | round (us) | GB/s | T_roof (us) | frac |")
-    print("|---|---|---|---|---|---|---|---|")
+    print("| N | params | wire | LAMB | round (us) | GB/s | T_roof (us) | frac | T serialized §8d (us) | frac |")
+    print("|---|---|---|---|---|---|---|---|---|---|")
     for path in paths:
         for line in open(path):
             d = json.loads(line)
             if "error" in d:
-                print(f"| {d['n_gpus']} | {d['params']} | {d['wire']} | | error | | | |")
+                print(f"| {d['n_gpus']} | {d['params']} | {d['wire']} | | error | | | | | |")
                 continue
             c = d["config"]
             n, world, L, wire = c["params"], d["n_gpus"], c["peers_per_gpu"], c["wire"]
@@ -32,10 +32,12 @@ def main(paths):
             ms = [bench.rank_model(r, offs, L, world, n, b, wire, shard, fused,
                                    world == 1 and L == 1 and wire != "q8" and fused)
                   for r in range(world)]
-            t = bench.round_roofline(ms, n, d["roofline"]["peak"] if d["roofline"]["bound"] == "hbm"
-                                     else bench.peak_hbm()[0]) * 1e6
+            peak = 6524.0
+            t = bench.round_roofline(ms, n, peak) * 1e6
+            t2 = bench.overlap_roofline(ms, n, peak) * 1e6
             print(f"| {world} | {n:,} | {wire} | {'sharded' if shard else 'replicated'} | "
-                  f"{d['round_us']:.1f} | {d['value']:.0f} | {t:.1f} | {t / d['round_us']:.3f} |")
+                  f"{d['round_us']:.1f} | {d['value']:.0f} | {t2:.1f} | {t2 / d['round_us']:.3f} | "
+                  f"{t:.1f} | {t / d['round_us']:.3f} |")
 
 
 if __name__ == "__main__":

@@ -101,3 +101,17 @@ def test_sharded_lamb_hybrid_split():
     # opt-in split: replicated LAMB for the leading tensors on a second stream
     # beside the sharded chain (measured slower; kept bit-exact)
     _launch(NGPU, "--wire", "fp16", "--shard-lamb", env={"SP_SHARD_FRACTION": "0.5"})
+
+
+@pytest.mark.parametrize("env", [
+    {"SP_SHARD_FUSED": "1", "SP_SHARD_LAG": "0", "SP_LAMB_CHUNK": "1024"},  # many items per tensor, pass 2 interleaved
+    {"SP_SHARD_FUSED": "1", "SP_SHARD_LAG": "37", "SP_LAMB_CHUNK": "2048"},
+    {"SP_SHARD_FUSED": "1"},  # one kernel, default lag
+])
+def test_sharded_lamb_one_kernel_schedules(env):
+    # k_shard_lamb_fused: per-tensor norm flags over NVLink inside one
+    # persistent kernel; every schedule must give the same bits
+    _launch(NGPU, "--wire", "fp16", "--shard-lamb", "--steps", "4", env=env)
+    fr = [0.0] * NGPU
+    fr[-1], fr[0] = 0.7, 0.3
+    _launch(NGPU, "--wire", "q8", "--shard-lamb", "--fractions", ",".join(map(str, fr)), env=env)

@@ -126,6 +126,18 @@ def test_round_parity_lp_planned(fleet, wire):
     _run_case(wire, plan["fractions"], plan["weights"], RAGGED, offsets=plan["offsets"])
 
 
+@pytest.mark.parametrize("env", [{"SP_SHARD_FUSED": "1", "SP_SHARD_LAG": "0", "SP_LAMB_CHUNK": "1024"},
+                                 {"SP_SHARD_FUSED": "1", "SP_SHARD_LAG": "11", "SP_LAMB_CHUNK": "2048"},
+                                 {"SP_SHARD_FUSED": "1"}])
+def test_sharded_lamb_schedules_one_rank(env, monkeypatch):
+    # one-kernel sharded LAMB (k_shard_lamb_fused) with interleaved pass-2
+    # items, and the kernel chain, against the oracle
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _run_case("fp16", [0.25, 0.25, 0.25, 0.25], [5.0, 0.0, 3.0, 8.0], RAGGED, steps=3, warm=True,
+              shard=True)
+
+
 @pytest.mark.parametrize("wire", ["fp32", "fp16", "q8"])
 def test_round_parity_sharded_lamb_one_rank(wire):
     # shard_lamb on one rank: the owned range is the whole vector; exercises
