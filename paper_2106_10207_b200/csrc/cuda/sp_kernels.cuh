@@ -1253,6 +1253,83 @@ __global__ void __launch_bounds__(256) k_shard_norms(ShardNormArgs a) {
   if (threadIdx.x < a.ndst) a.table[threadIdx.x][(size_t)a.rank * a.T + t] = make_double2(sx[0], sy[0]);
 }
 
+// k_lamb_moments with k_shard_norms folded in (the default sharded chain
+// when every tensor is sharded): the CTA finishing a tensor's last owned
+// chunk sums the chunk partials in fp64 in k_shard_norms' order and stores
+// the pair into slot [rank][t] of every rank's table. Tensors this rank has
+// no chunk of get a zero pair. `nchunks` may be 0 (grid 1: zeros only).
+template <int W>
+__global__ void __launch_bounds__(kLambThreads) k_lamb_moments_shard(LambArgs a, ShardNormArgs na,
+                                                                    int* __restrict__ done,
+                                                                    int nchunks) {
+  __shared__ float red_p[kLambThreads / 32], red_u[kLambThreads / 32];
+  __shared__ double dred_p[kLambThreads], dred_u[kLambThreads];
+  __shared__ int s_last;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int t = na.t0 + blockIdx.x; t < na.T; t += gridDim.x) {
+    const int2 r = na.tchunks[t];
+    if (r.y <= r.x && tid < na.ndst) na.table[tid][(size_t)na.rank * na.T + t] = make_double2(0.0, 0.0);
+  }
+  if ((int)blockIdx.x >= nchunks) return;
+  const Chunk c = a.chunks[blockIdx.x];
+  const LambScalars s{a.hp[0], a.hp[1], a.hp[2]};
+  float pp = 0.0f, uu = 0.0f;
+  lamb_pass1<W>(a, s, c, pp, uu);
+  pp = warp_sum(pp);
+  uu = warp_sum(uu);
+  if (lane == 0) {
+    red_p[wid] = pp;
+    red_u[wid] = uu;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    float sp_ = 0.0f, su = 0.0f;
+#pragma unroll
+    for (int w = 0; w < kLambThreads / 32; ++w) {
+      sp_ += red_p[w];
+      su += red_u[w];
+    }
+    a.partial[blockIdx.x] = make_float2(sp_, su);
+    __threadfence();
+    const int2 r = na.tchunks[c.tensor];
+    s_last = atomicAdd(done + c.tensor, 1) == r.y - r.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int2 r = na.tchunks[c.tensor];
+  double x = 0.0, y = 0.0;
+  for (int q = r.x + tid; q < r.y; q += kLambThreads) {
+    const float2 v = __ldcg(a.partial + q);
+    x += (double)v.x;
+    y += (double)v.y;
+  }
+  dred_p[tid] = x;
+  dred_u[tid] = y;
+  __syncthreads();
+  for (int h = kLambThreads / 2; h > 0; h >>= 1) {
+    if (tid < h) {
+      dred_p[tid] += dred_p[tid + h];
+      dred_u[tid] += dred_u[tid + h];
+    }
+    __syncthreads();
+  }
+  if (tid < na.ndst) na.table[tid][(size_t)na.rank * na.T + c.tensor] = make_double2(dred_p[0], dred_u[0]);
+  if (tid == 0) done[c.tensor] = 0;
+}
+
+__device__ __forceinline__ float trust_from_table(const double2* __restrict__ table, int world, int T,
+                                                  int t) {
+  double x = 0.0, y = 0.0;
+  for (int k = 0; k < world; ++k) {
+    const double2 v = __ldcg(table + (size_t)k * T + t);
+    x += v.x;
+    y += v.y;
+  }
+  const double r1 = sqrt(x), r2 = sqrt(y);
+  return (r1 > 0.0 && r2 > 0.0) ? (float)(r1 / r2) : 1.0f;
+}
+
 // trust[t] = sqrt(sum_k pp[k][t]) / sqrt(sum_k uu[k][t]) over ranks in order
 // (1 if either is 0); step_scale[t] = lr * trust[t].
 __global__ void k_shard_trust(const double2* __restrict__ table, int world, int T, int t0,
@@ -1328,6 +1405,30 @@ __global__ void __launch_bounds__(kLambThreads) k_lamb_update_push(LambArgs a, P
   const Chunk c = a.chunks[blockIdx.x];
   const LambScalars s{a.hp[0], a.hp[1], a.hp[2]};
   lamb_push_chunk(a, s, c, -__ldcg(a.step_scale + c.tensor), d);
+}
+
+// k_lamb_update_push with k_shard_trust folded in: every CTA forms its
+// tensor's trust ratio from the norm table (k_shard_trust's arithmetic), and
+// CTAs b, b + grid, ... also write trust / step_scale of tensor b (what
+// read_trust() returns). `nchunks` may be 0 (grid 1: trust only).
+template <int W>
+__global__ void __launch_bounds__(kLambThreads) k_lamb_update_push_trust(
+    LambArgs a, ParamPush d, const double2* __restrict__ table, int world, int T, int t0,
+    float* __restrict__ trust, float* __restrict__ step_scale, int nchunks) {
+  __shared__ float s_neg;
+  const LambScalars s{a.hp[0], a.hp[1], a.hp[2]};
+  if (threadIdx.x == 0) {
+    for (int t = t0 + blockIdx.x; t < T; t += gridDim.x) {
+      const float tr = trust_from_table(table, world, T, t);
+      trust[t] = tr;
+      step_scale[t] = __fmul_rn(s.lr, tr);
+    }
+    if ((int)blockIdx.x < nchunks)
+      s_neg = -__fmul_rn(s.lr, trust_from_table(table, world, T, a.chunks[blockIdx.x].tensor));
+  }
+  __syncthreads();
+  if ((int)blockIdx.x >= nchunks) return;
+  lamb_push_chunk(a, s, a.chunks[blockIdx.x], s_neg, d);
 }
 
 // ------------------------------------------- sharded LAMB, one kernel (N1)

@@ -673,6 +673,43 @@ int enqueue_shard_lamb(sp_round* r, const LambArgs& la, const BarrierArgs& ba, c
     if (ev) SP_CUDA(cudaEventRecord(ev[7], st));
     return SP_OK;
   }
+  if (t0 < T && nR == 0) {
+    // default chain, every tensor sharded: pass 1 with the norm publication
+    // folded in -> barrier -> pass 2 + push with the trust folded in -> barrier
+    ShardNormArgs na{};
+    na.tchunks = r->d_tchunks;
+    na.ndst = c.world;
+    for (int k = 0; k < c.world; ++k) na.table[k] = r->norms((c.rank + 1 + k) % c.world);
+    na.rank = c.rank;
+    na.T = T;
+    na.t0 = 0;
+    const int g = std::max(1, nS);
+    switch (c.wire) {
+      case SP_WIRE_FP32: k_lamb_moments_shard<SP_WIRE_FP32><<<g, kLambThreads, 0, st>>>(ls, na, r->d_qstate + 2, nS); break;
+      case SP_WIRE_FP16: k_lamb_moments_shard<SP_WIRE_FP16><<<g, kLambThreads, 0, st>>>(ls, na, r->d_qstate + 2, nS); break;
+      default: k_lamb_moments_shard<SP_WIRE_Q8><<<g, kLambThreads, 0, st>>>(ls, na, r->d_qstate + 2, nS); break;
+    }
+    SP_CUDA(cudaGetLastError());
+    if (ev) SP_CUDA(cudaEventRecord(ev[5], st));
+    if (c.world > 1) {
+      k_barrier<<<1, 32, 0, st>>>(ba);
+      SP_CUDA(cudaGetLastError());
+    }
+    if (ev) SP_CUDA(cudaEventRecord(ev[6], st));
+    const double2* tab = r->norms(c.rank);
+    switch (c.wire) {
+      case SP_WIRE_FP32: k_lamb_update_push_trust<SP_WIRE_FP32><<<g, kLambThreads, 0, st>>>(ls, pp, tab, c.world, T, 0, r->d_trust, r->d_step_scale, nS); break;
+      case SP_WIRE_FP16: k_lamb_update_push_trust<SP_WIRE_FP16><<<g, kLambThreads, 0, st>>>(ls, pp, tab, c.world, T, 0, r->d_trust, r->d_step_scale, nS); break;
+      default: k_lamb_update_push_trust<SP_WIRE_Q8><<<g, kLambThreads, 0, st>>>(ls, pp, tab, c.world, T, 0, r->d_trust, r->d_step_scale, nS); break;
+    }
+    SP_CUDA(cudaGetLastError());
+    if (c.world > 1) {
+      k_barrier<<<1, 32, 0, st>>>(ba);
+      SP_CUDA(cudaGetLastError());
+    }
+    if (ev) SP_CUDA(cudaEventRecord(ev[7], st));
+    return SP_OK;
+  }
   if (t0 < T) {
     if (nS > 0) {
       switch (c.wire) {
@@ -892,7 +929,12 @@ int enqueue_round(sp_round* r, const float* const* grads, float* p, float* m, fl
       }
     }
     if (ev && s == 0) SP_CUDA(cudaEventRecord(ev[3], st));
-    if (c.world > 1) {
+    // the averages must have landed everywhere before LAMB reads them; with
+    // every tensor sharded they stay with their owner, so no barrier (the
+    // next round's pack cannot start before the round's last barrier, which
+    // every rank enters after its reduce)
+    const bool all_local = r->shard && r->nchunks_rep == 0 && K == 1;
+    if (c.world > 1 && !all_local) {
       k_barrier<<<1, 32, 0, st>>>(ba);
       SP_CUDA(cudaGetLastError());
     }
