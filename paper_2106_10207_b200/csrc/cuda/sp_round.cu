@@ -81,6 +81,7 @@ struct sp_round {
   int segments = 1;
   int seg_lamb_grid = 1 << 30;  // CTA cap of a segment's pass-1 launch
   int xchg_per_sm = 8;          // CTAs per SM of the exchange kernels
+  double pack_local_weight = 1.0;  // CTA share of the local range in the pack (vs remote)
   std::vector<int> p1_off;   // K+1 offsets of the per-segment pass-1 item lists
   int p2_off = 0;            // pass-2 items
   cudaStream_t aux = nullptr;
@@ -850,12 +851,18 @@ int enqueue_round(sp_round* r, const float* const* grads, float* p, float* m, fl
       const int want = c.wire == SP_WIRE_Q8
                            ? (int)std::min<int64_t>(units, (int64_t)r->sm_count * 16)
                            : grid_for(units, 256, r->sm_count, r->xchg_per_sm);
-      // split the CTAs over the ranges in proportion to their lengths (>= 1 each)
+      // split the CTAs over the ranges in proportion to their lengths (>= 1
+      // each); the local range (HBM stores) weighted by pack_local_weight
+      // against the remote ones (NVLink stores, the slower side)
       int total = 0;
       a.cta0[0] = 0;
+      double wsum_r = 0.0;
+      for (int j = 0; j < a.nr; ++j)
+        wsum_r += (double)(a.pref[j + 1] - a.pref[j]) * (a.owner[j] == c.rank ? r->pack_local_weight : 1.0);
       for (int j = 0; j < a.nr; ++j) {
         const int64_t len = a.pref[j + 1] - a.pref[j];
-        int nct = (int)std::max<int64_t>(1, (int64_t)((double)want * len / units + 0.5));
+        const double wj = (double)len * (a.owner[j] == c.rank ? r->pack_local_weight : 1.0);
+        int nct = (int)std::max<int64_t>(1, (int64_t)((double)want * wj / wsum_r + 0.5));
         nct = (int)std::min<int64_t>(nct, (len + per_cta - 1) / per_cta);
         total += std::max(1, nct);
         a.cta0[j + 1] = total;
@@ -1142,6 +1149,7 @@ int sp_round_create(const sp_round_cfg* cfg, sp_round** out) {
     const bool unfused = unf && unf[0] == '1';
     if (const char* g = std::getenv("SP_SEG_LAMB_GRID")) r->seg_lamb_grid = std::max(1, std::atoi(g));
     if (const char* x = std::getenv("SP_XCHG_PER_SM")) r->xchg_per_sm = std::max(1, std::atoi(x));
+    if (const char* x = std::getenv("SP_PACK_LOCAL_WEIGHT")) r->pack_local_weight = std::max(0.01, std::atof(x));
     r->segments = (cfg->world > 1 && !unfused && !r->fused_round && !r->shard)
                       ? std::max(1, std::min(8, seg_env ? std::atoi(seg_env) : 1))
                       : 1;
