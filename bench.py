@@ -30,11 +30,6 @@ sys.path.insert(0, ROOT)
 METRIC = "averaging round time + GB/s (grad avg + LAMB step), ALBERT-large, 1/2/4/8 B200"
 HP = dict(lr=1.76e-3, beta1=0.9, beta2=0.999, eps=1e-6, weight_decay=0.01, bias_correction=1)
 SIGMA = 1e-3 * 3 ** 0.5
-# NVLink roofline denominator: the measured B200 peer copy per direction per
-# GPU (/opt/skills/guides/B200_PROFILING.md; 900 nominal). Our own all-to-all
-# push microbenchmark sustains ~660 at 4 GPUs (profiles/r01/p2p_bw.txt) and
-# large sweeps reach ~770 (profiles/r01/sweep).
-NVLINK_GBS = 770.0
 L2_BYTES = 126e6
 
 WORKLOADS = {
@@ -225,66 +220,8 @@ def lp_solve_times() -> dict:
     return out
 
 
-def rank_model(r, offsets, L, world, n, b, wire, shard, fused, fused_pack) -> dict:
-    """Algorithmic bytes per element for rank r given the
-    part fraction f it owns: per-kernel launch bytes (`alg`) and, for each
-    phase of the round (pack+scatter, reduce(+push), LAMB(+parameter push)),
-    the HBM bytes it must move and the NVLink bytes per direction (the larger
-    of out and in). Phases are separated by cross-rank barriers, so the
-    round's roofline is the sum over phases of the slowest rank's
-    max(HBM time, NVLink time)."""
-    G = L * world
-    f = (offsets[(r + 1) * L] - offsets[r * L]) / n
-    f_l = f if shard else 1.0  # fraction of the vector this rank's LAMB steps
-    alg = {
-        "pack_ms": 0.0 if fused_pack else (L * n * (4 + b)),
-        "reduce_ms": (G + (1 if shard else world)) * f * n * b,
-        # fused kernel: pass 1 reads g,p,m,v writes m,v; pass 2 reads p,m,v writes p
-        "moments_ms": f_l * n * (20 + b + (4 + b if fused_pack else 0.0)) + (n * 16.0 if fused else 0.0),
-        "update_ms": 0.0 if fused else f_l * n * 16.0,
-    }
-    multi = world > 1
-    # pack: read the fp32 gradients (4 L), write the wire of the owned range
-    # (L f b from local peers, (G - L) f b arriving from the other ranks; the
-    # rest of the local wire lands in the owners' HBM). fp32 on one GPU: the
-    # wire is the gradient itself (zero-copy).
-    pack_hbm = (4 * L + G * f * b) if (wire != "fp32" or multi) else 0.0
-    pack_nvl = max(L * (1 - f) * b, (G - L) * f * b) if multi else 0.0
-    # reduce: read G inbox slots of the owned range, write the average
-    # (replicated: pushed to every rank, (1 - f) b arrives from the others).
-    # G = 1: the average of one peer is its wire values, no reduce pass.
-    if G > 1:
-        # sharded: the average stays local (f b); replicated: f b written
-        # here and pushed out, (1 - f) b of the others' averages lands here
-        red_hbm = G * f * b + (f * b if shard else b)
-        red_nvl = 0.0 if (shard or not multi) else max((world - 1) * f * b, (1 - f) * b)
-    else:
-        red_hbm = red_nvl = 0.0
-    # LAMB, one-pass ideal: read wire grad + p, m, v, write p, m, v; sharded:
-    # the fp32 parameters of the owned range go to every other rank
-    lamb_hbm = f_l * (24 + b) + ((1 - f) * 4.0 if shard and multi else 0.0)
-    lamb_nvl = max((world - 1) * f * 4.0, (1 - f) * 4.0) if (shard and multi) else 0.0
-    phases = [(pack_hbm, pack_nvl), (red_hbm, red_nvl), (lamb_hbm, lamb_nvl)]
-    return {"f": f, "alg": alg, "phases": phases,
-            "hbm": sum(h for h, _ in phases), "nvl": sum(x for _, x in phases)}
-
-
-def round_roofline(models, n, peak) -> float:
-    """Seconds: HBM and NVLink phases serialized, each on its
-    critical-path rank: max_r HBM_r / peak + max_r NVL_r / NVLink."""
-    return (max(m["hbm"] for m in models) * n / (peak * 1e9)
-            + max(m["nvl"] for m in models) * n / (NVLINK_GBS * 1e9))
-
-
-def overlap_roofline(models, n, peak) -> float:
-    """Seconds, a tighter bound: within each barrier-separated phase (pack +
-    scatter, reduce, LAMB [+ parameter push]) HBM and NVLink traffic overlap,
-    so the phase costs the slowest rank's max(HBM time, NVLink time)."""
-    t = 0.0
-    for k in range(3):
-        t += max(max(m["phases"][k][0] * n / (peak * 1e9), m["phases"][k][1] * n / (NVLINK_GBS * 1e9))
-                 for m in models)
-    return t
+from paper_2106_10207_b200.roofline import (NVLINK_GBS, overlap_roofline, rank_model,  # noqa: E402,F401
+                                            round_roofline)
 
 
 # ------------------------------------------------------------------ main
@@ -300,9 +237,10 @@ def main():
     ap.add_argument("--phased-steps", type=int, default=20)
     ap.add_argument("--lamb", choices=["auto", "replicated", "sharded"], default="auto",
                     help="replicated: every GPU steps the all-gathered average; sharded: ZeRO-1 "
-                         "style, owners step their range and push fp32 parameters (faster at "
-                         "N > 1 for every wire, profiles/r01/overlap_experiments.txt); auto: "
-                         "sharded when N > 1")
+                         "style, owners step their range and push fp32 parameters; auto: at N > 1 "
+                         "the mode with the lower round bound for the LP plan "
+                         "(roofline.choose_shard_lamb: sharded for uniform splits, replicated "
+                         "when one owner dominates)")
     ap.add_argument("--shard-lamb", action="store_true", help="alias of --lamb sharded")
     ap.add_argument("--params", type=int, default=0, help="--workload sweep: vector length")
     ap.add_argument("--wire", choices=["fp32", "fp16", "q8"], default=None,
@@ -315,7 +253,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.shard_lamb:
         args.lamb = "sharded"
-    args.shard_lamb = args.lamb == "sharded" or (args.lamb == "auto" and world > 1)
+    args.shard_lamb = args.lamb == "sharded"  # auto: decided from the plan below
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         log(f"note: WORLD_SIZE={world} but --gpus={args.gpus}; using WORLD_SIZE")
@@ -347,6 +285,10 @@ def main():
     wsum = sum(plan["weights"])
     weights = [w * TARGET_BATCH / wsum for w in plan["weights"]]  # sample counts, sum = batch
     b = wire_bytes(wire, block)
+    if args.lamb == "auto":
+        from paper_2106_10207_b200.roofline import choose_shard_lamb
+
+        args.shard_lamb = choose_shard_lamb(offsets, L, world, n, b, wire)
 
     if args.impl == "reference":
         return run_reference(args, rank, world, tsizes, wire, block, G, weights, b)
