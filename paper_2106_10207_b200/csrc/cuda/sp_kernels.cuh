@@ -1270,52 +1270,57 @@ __global__ void __launch_bounds__(kLambThreads) k_lamb_moments_shard(LambArgs a,
     const int2 r = na.tchunks[t];
     if (r.y <= r.x && tid < na.ndst) na.table[tid][(size_t)na.rank * na.T + t] = make_double2(0.0, 0.0);
   }
-  if ((int)blockIdx.x >= nchunks) return;
-  const Chunk c = a.chunks[blockIdx.x];
   const LambScalars s{a.hp[0], a.hp[1], a.hp[2]};
-  float pp = 0.0f, uu = 0.0f;
-  lamb_pass1<W>(a, s, c, pp, uu);
-  pp = warp_sum(pp);
-  uu = warp_sum(uu);
-  if (lane == 0) {
-    red_p[wid] = pp;
-    red_u[wid] = uu;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    float sp_ = 0.0f, su = 0.0f;
-#pragma unroll
-    for (int w = 0; w < kLambThreads / 32; ++w) {
-      sp_ += red_p[w];
-      su += red_u[w];
-    }
-    a.partial[blockIdx.x] = make_float2(sp_, su);
-    __threadfence();
-    const int2 r = na.tchunks[c.tensor];
-    s_last = atomicAdd(done + c.tensor, 1) == r.y - r.x - 1;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const int2 r = na.tchunks[c.tensor];
-  double x = 0.0, y = 0.0;
-  for (int q = r.x + tid; q < r.y; q += kLambThreads) {
-    const float2 v = __ldcg(a.partial + q);
-    x += (double)v.x;
-    y += (double)v.y;
-  }
-  dred_p[tid] = x;
-  dred_u[tid] = y;
-  __syncthreads();
-  for (int h = kLambThreads / 2; h > 0; h >>= 1) {
-    if (tid < h) {
-      dred_p[tid] += dred_p[tid + h];
-      dred_u[tid] += dred_u[tid + h];
+  // grid-stride over the owned chunks (a grid of one resident wave)
+  for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x) {
+    const Chunk c = a.chunks[ci];
+    float pp = 0.0f, uu = 0.0f;
+    lamb_pass1<W>(a, s, c, pp, uu);
+    pp = warp_sum(pp);
+    uu = warp_sum(uu);
+    if (lane == 0) {
+      red_p[wid] = pp;
+      red_u[wid] = uu;
     }
     __syncthreads();
+    if (tid == 0) {
+      float sp_ = 0.0f, su = 0.0f;
+#pragma unroll
+      for (int w = 0; w < kLambThreads / 32; ++w) {
+        sp_ += red_p[w];
+        su += red_u[w];
+      }
+      a.partial[ci] = make_float2(sp_, su);
+      __threadfence();
+      const int2 r = na.tchunks[c.tensor];
+      s_last = atomicAdd(done + c.tensor, 1) == r.y - r.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      const int2 r = na.tchunks[c.tensor];
+      double x = 0.0, y = 0.0;
+      for (int q = r.x + tid; q < r.y; q += kLambThreads) {
+        const float2 v = __ldcg(a.partial + q);
+        x += (double)v.x;
+        y += (double)v.y;
+      }
+      dred_p[tid] = x;
+      dred_u[tid] = y;
+      __syncthreads();
+      for (int h = kLambThreads / 2; h > 0; h >>= 1) {
+        if (tid < h) {
+          dred_p[tid] += dred_p[tid + h];
+          dred_u[tid] += dred_u[tid + h];
+        }
+        __syncthreads();
+      }
+      if (tid < na.ndst)
+        na.table[tid][(size_t)na.rank * na.T + c.tensor] = make_double2(dred_p[0], dred_u[0]);
+      if (tid == 0) done[c.tensor] = 0;
+    }
+    __syncthreads();  // red_p / s_last reused by the next chunk
   }
-  if (tid < na.ndst) na.table[tid][(size_t)na.rank * na.T + c.tensor] = make_double2(dred_p[0], dred_u[0]);
-  if (tid == 0) done[c.tensor] = 0;
 }
 
 __device__ __forceinline__ float trust_from_table(const double2* __restrict__ table, int world, int T,
@@ -1423,12 +1428,14 @@ __global__ void __launch_bounds__(kLambThreads) k_lamb_update_push_trust(
       trust[t] = tr;
       step_scale[t] = __fmul_rn(s.lr, tr);
     }
-    if ((int)blockIdx.x < nchunks)
-      s_neg = -__fmul_rn(s.lr, trust_from_table(table, world, T, a.chunks[blockIdx.x].tensor));
   }
-  __syncthreads();
-  if ((int)blockIdx.x >= nchunks) return;
-  lamb_push_chunk(a, s, a.chunks[blockIdx.x], s_neg, d);
+  for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x) {  // grid-stride over owned chunks
+    const Chunk c = a.chunks[ci];
+    if (threadIdx.x == 0) s_neg = -__fmul_rn(s.lr, trust_from_table(table, world, T, c.tensor));
+    __syncthreads();
+    lamb_push_chunk(a, s, c, s_neg, d);
+    __syncthreads();
+  }
 }
 
 // ------------------------------------------- sharded LAMB, one kernel (N1)

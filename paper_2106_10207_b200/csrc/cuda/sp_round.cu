@@ -684,7 +684,8 @@ int enqueue_shard_lamb(sp_round* r, const LambArgs& la, const BarrierArgs& ba, c
     na.rank = c.rank;
     na.T = T;
     na.t0 = 0;
-    const int g = std::max(1, nS);
+    // one resident wave, grid-stride over the chunks (no partial second wave)
+    const int g = std::max(1, std::min(nS, r->lamb_grid));
     switch (c.wire) {
       case SP_WIRE_FP32: k_lamb_moments_shard<SP_WIRE_FP32><<<g, kLambThreads, 0, st>>>(ls, na, r->d_qstate + 2, nS); break;
       case SP_WIRE_FP16: k_lamb_moments_shard<SP_WIRE_FP16><<<g, kLambThreads, 0, st>>>(ls, na, r->d_qstate + 2, nS); break;
