@@ -504,10 +504,12 @@ def main():
                                f"counts scaled to batch {TARGET_BATCH:g}",
                        "l2": f"no flush: per-step working set {(n * (12 + 4 * L + 2 * b)) / 1e9:.2f} GB > 126 MB L2",
                        "parallelism": f"dp{world} (one process per GPU, {L} peer(s) each, CUDA IPC over NVLink)"},
-            # per round: pack + reduce + LAMB (1 fused / 3 unfused) + 2 barriers if N > 1
-            # (one rank with a single peer skips the reduce: identity average)
+            # replicated: pack (fused into LAMB on one GPU with one peer) + reduce
+            # + LAMB (1 fused / 3 unfused) + 2 barriers if N > 1
+            # sharded: pack, reduce, pass 1 (+norms), pass 2 + push (+trust),
+            # barriers after the pack, the norms and the push
             "gpu_launches": args.steps * (
-                (1 + (1 if G > 1 else 0) + 4 + (4 if world > 1 else 0)) if shard else
+                (1 + (1 if G > 1 else 0) + 2 + (3 if world > 1 else 0)) if shard else
                 ((0 if fused_pack else 1) + (1 if G > 1 else 0) + (1 if fused else 3)
                  + (2 if world > 1 else 0))),
             "kernel_ms": {k: round(v_, 5) for k, v_ in ph.items()},
