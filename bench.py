@@ -445,8 +445,10 @@ def main():
         dom = max(("pack_ms", "reduce_ms", "moments_ms", "update_ms"), key=lambda k: phc[k])
         widx = {"fp32": 0, "fp16": 1, "q8": 2}[wire]
         kname = {"pack_ms": f"k_pack_{wire}", "reduce_ms": f"k_reduce_{wire}",
-                 "moments_ms": f"k_lamb_fused<{widx}>" if fused else f"k_lamb_moments<{widx}>",
-                 "update_ms": f"k_lamb_update<{widx}>"}[dom]
+                 "moments_ms": (f"k_lamb_fused<{widx}>" if fused else
+                                f"k_lamb_moments_shard<{widx}>" if shard else f"k_lamb_moments<{widx}>"),
+                 "update_ms": (f"k_lamb_update_push_trust<{widx}>" if shard
+                               else f"k_lamb_update<{widx}>")}[dom]
         achieved = alg[dom] / (phc[dom] * 1e-3) / 1e9
         bound, pk, unit = "hbm", peak, "GB/s"
         if shard and dom == "update_ms" and world > 1:  # parameter push: (world-1) f 4 B out
@@ -517,7 +519,10 @@ def main():
             "roofline": {"bound": bound, "kernel": dom.replace("_ms", ""), "rank": rc,
                          "achieved": round(achieved, 1), "peak": pk, "unit": unit,
                          "frac": round(achieved / pk, 4),
-                         "traffic": ncu_traffic(kname) if table == "albert-large" else None,
+                         # committed captures are single-GPU ALBERT-large launches: only
+                         # comparable per launch to the same configuration
+                         "traffic": (ncu_traffic(kname) if table == "albert-large" and world == 1
+                                     and L == 1 else None),
                          "algorithmic_bytes": alg[dom],
                          "peak_kind": peak_kind if bound == "hbm" else "measured peer copy per direction (B200_PROFILING.md)"},
             # primary: the overlap bound (a lower bound on the round time; the
