@@ -80,7 +80,10 @@ typedef struct {
                         * partials are exchanged over NVLink, and the updated
                         * parameters (not the averaged gradient) are pushed to
                         * every rank. p must be sp_round_param_ptr(); m and v
-                        * stay full-length but only the owned range is kept. */
+                        * stay full-length but only the owned range is kept.
+                        * Pays off on uniform splits; with a dominant owner the
+                        * replicated mode is faster (the Python planner's
+                        * roofline.choose_shard_lamb picks per plan). */
 } sp_round_cfg;
 
 /* Per-kernel device times of the last sp_round_run_phased call (ms). */
@@ -88,10 +91,12 @@ typedef struct {
   float pack_ms;      /* K1: fp32 -> wire                                    */
   float barrier_a_ms; /* cross-rank barrier before the exchange (0 if N=1)   */
   float reduce_ms;    /* K2: fused reduce-scatter / average / all-gather     */
-  float barrier_b_ms; /* cross-rank barrier after the exchange               */
-  float moments_ms;   /* K3: LAMB moments + per-chunk norm partials          */
-  float trust_ms;     /* per-tensor trust ratios                             */
-  float update_ms;    /* K4: LAMB parameter update                           */
+  float barrier_b_ms; /* cross-rank barrier after the exchange (sharded: none) */
+  float moments_ms;   /* K3: LAMB moments + per-chunk norm partials (sharded:
+                         + norm publication; replicated, fused: whole LAMB)  */
+  float trust_ms;     /* per-tensor trust ratios (sharded: the norm barrier) */
+  float update_ms;    /* K4: LAMB parameter update (sharded: + parameter push
+                         + the closing barrier)                              */
   float total_ms;
 } sp_phase_times;
 
