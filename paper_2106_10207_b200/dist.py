@@ -61,3 +61,48 @@ def check_same_plan(offsets, weights, group=None) -> None:
     dist.all_gather_object(out, mine, group=group)
     if any(d != mine for d in out):
         raise RuntimeError("ranks disagree on the round assignment (offsets/weights)")
+
+
+def share_fd(fd: int | None, src: int = 0, group=None, tag: str = "sp") -> int:
+    """Give every rank of one node a file descriptor owned by rank `src`.
+
+    CUDA multicast objects and VMM allocations are shared between processes
+    as POSIX file descriptors (cuMemExportToShareableHandle), which cannot
+    travel through torch.distributed. Rank `src` listens on an abstract Unix
+    socket whose name it all-gathers; every other rank connects and receives
+    the descriptor with SCM_RIGHTS. Returns the local descriptor (`fd` itself
+    on `src`; the caller closes received ones)."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    names: list = [None] * world
+    name = f"\0{tag}-{os.getpid()}-{rank}" if rank == src else None
+    dist.all_gather_object(names, name, group=group)
+    path = names[src]
+    if rank == src:
+        if fd is None:
+            raise ValueError("the source rank must pass a descriptor")
+        srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        srv.bind(path)
+        srv.listen(world)
+        dist.barrier(group=group)  # listening before anyone connects
+        try:
+            for _ in range(world - 1):
+                conn, _ = srv.accept()
+                with conn:
+                    socket.send_fds(conn, [b"fd"], [fd])
+        finally:
+            srv.close()
+        dist.barrier(group=group)
+        return fd
+    dist.barrier(group=group)
+    with socket.socket(socket.AF_UNIX, socket.SOCK_STREAM) as c:
+        c.connect(path)
+        _, fds, _, _ = socket.recv_fds(c, 16, 1)
+    dist.barrier(group=group)
+    if len(fds) != 1:
+        raise RuntimeError("share_fd: no descriptor received")
+    return fds[0]

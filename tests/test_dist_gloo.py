@@ -79,3 +79,39 @@ def test_gloo_host_logic(world):
         want = [f * 17847474 for f in FRACTIONS_APPENDIX_A["het8c"]]
         assert sizes[6] == 0
         assert all(abs(s - w) <= 8 for s, w in zip(sizes, want))
+
+
+def _fd_worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2106_10207_b200 import dist as D
+
+    try:
+        fd = None
+        if rank == 1:  # the source need not be rank 0
+            fd = os.memfd_create("sp-test")
+            os.write(fd, b"multicast handle stand-in")
+        got = D.share_fd(fd, src=1)
+        q.put((rank, os.pread(got, 64, 0)))
+        os.close(got)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_share_fd_between_ranks(world):
+    # the POSIX-fd path CUDA multicast / VMM handles need between processes
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_fd_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [r for r, _ in res] == list(range(world))
+    assert all(b == b"multicast handle stand-in" for _, b in res)
