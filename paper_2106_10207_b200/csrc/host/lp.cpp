@@ -13,7 +13,10 @@
 //    as product-form eta columns. ftran/btran cost O(nnz(L+U) + etas*m).
 //  * Pricing: devex reference weights (symmetric fleets make whole column
 //    families tie; largest-coefficient pricing stalls on them), lowest index
-//    on ties, Bland's rule after a run of degenerate pivots.
+//    on ties, Bland's rule after a run of degenerate pivots. The pivot row
+//    is formed row-wise over the nonzeros of rho (about 1.3k multiply-adds
+//    per pivot instead of 7.6k column-wise on table1_c), and phase 2 updates
+//    the reduced costs from it instead of a second btran per iteration.
 //  * Ratio test: exact minimum ratio; near-ties go to the largest pivot,
 //    then to the lowest variable index. If roundoff pushes a basic variable
 //    out of bounds during phase 2, the solve returns to phase 1 to repair.
@@ -572,6 +575,33 @@ struct SimplexSolver::Impl {
     const double dtol = phase1 ? opt.opt_tol : opt.opt_tol * cmax;
     std::vector<double> cb(m), y, w, rc(m), rho, aq(m, 0.0);
     std::vector<double> ref(nv(), 1.0);
+    // Phase 2 keeps the reduced costs d_j = c_j - y'A_j across iterations and
+    // updates them from the pivot row the devex step already computes
+    // (d_j -= (d_q / alpha_q) alpha_j), which saves one btran and one pass
+    // over the columns per iteration. They are recomputed from a fresh btran
+    // after every refactorization, after a Bland pivot, and before optimality
+    // is declared.
+    std::vector<double> d(nv(), 0.0);
+    bool d_valid = false;
+    // Row-wise copy of the constraint matrix, so the devex pivot row
+    // alpha_j = rho'A_j visits only the rows where rho is nonzero (rho is
+    // usually sparse). Columns are stored in ascending row order, so each
+    // alpha_j accumulates its terms in the same order as col_dot.
+    std::vector<int> rbeg(m + 1, 0), rvar;
+    std::vector<double> rval, alpha(nv(), 0.0);
+    for (int j = 0; j < nv(); ++j)
+      for (const auto& rc_ : v[j].col) ++rbeg[rc_.first + 1];
+    for (int r = 0; r < m; ++r) rbeg[r + 1] += rbeg[r];
+    rvar.resize(rbeg[m]);
+    rval.resize(rbeg[m]);
+    {
+      std::vector<int> fill(rbeg.begin(), rbeg.end() - 1);
+      for (int j = 0; j < nv(); ++j)
+        for (const auto& [r, c] : v[j].col) {
+          rvar[fill[r]] = j;
+          rval[fill[r]++] = c;
+        }
+    }
     struct Cand {
       int p;
       double t, mag;
@@ -604,14 +634,21 @@ struct SimplexSolver::Impl {
         lost_feasibility = true;  // roundoff pushed a basic out of bounds: repair in phase 1
         return LpStatus::Optimal;
       }
-      btran(cb, y);
+      const bool incremental = !phase1 && d_valid;
+      if (!incremental) btran(cb, y);
 
       int q = -1, dir = 0;
       double best = 0.0;
       for (int j = 0; j < nv(); ++j) {
         const St s = st[j];
         if (s == St::Basic || v[j].lo == v[j].up) continue;
-        const double dj = (phase1 ? 0.0 : v[j].cost) - col_dot(j, y);
+        double dj;
+        if (incremental) {
+          dj = d[j];
+        } else {
+          dj = (phase1 ? 0.0 : v[j].cost) - col_dot(j, y);
+          d[j] = dj;
+        }
         int cd = 0;
         if ((s == St::Lower || s == St::Free) && dj > dtol)
           cd = 1;
@@ -630,7 +667,13 @@ struct SimplexSolver::Impl {
           dir = cd;
         }
       }
+      if (q < 0 && incremental) {  // confirm optimality on fresh reduced costs
+        d_valid = false;
+        --iters;
+        continue;
+      }
       if (q < 0) return phase1 ? LpStatus::Infeasible : LpStatus::Optimal;
+      if (!phase1 && !bland) d_valid = true;
 
       std::fill(aq.begin(), aq.end(), 0.0);
       for (const auto& [r, c] : v[q].col) aq[r] = c;
@@ -708,18 +751,30 @@ struct SimplexSolver::Impl {
         rc[leave] = 1.0;
         btran(rc, rho);
         const double wq = ref[q];
+        const double td = d[q] / ap;  // dual step (phase 2 reduced-cost update)
         double rmax = 0.0;
+        std::fill(alpha.begin(), alpha.end(), 0.0);
+        for (int r = 0; r < m; ++r) {
+          const double rr = rho[r];
+          if (rr == 0.0) continue;
+          for (int t = rbeg[r]; t < rbeg[r + 1]; ++t) alpha[rvar[t]] += rval[t] * rr;
+        }
         for (int j = 0; j < nv(); ++j) {
           if (st[j] == St::Basic || j == q || v[j].lo == v[j].up) continue;
-          const double al = col_dot(j, rho);
+          const double al = alpha[j];
           if (al == 0.0) continue;
+          d[j] -= td * al;
           const double cand = (al / ap) * (al / ap) * wq;
           if (cand > ref[j]) ref[j] = cand;
           rmax = std::max(rmax, ref[j]);
         }
         ref[basis[leave]] = std::max(wq / (ap * ap), 1.0);
+        d[basis[leave]] = -td;
+        d[q] = 0.0;
         if (rmax > 1e7) std::fill(ref.begin(), ref.end(), 1.0);
       }
+
+      if (leave >= 0 && bland) d_valid = false;
 
       // move
       if (theta != 0.0) {
@@ -756,6 +811,7 @@ struct SimplexSolver::Impl {
         if (static_cast<int>(etas.size()) >= kEtaLimit || std::fabs(w[leave]) < 1e-8) {
           refactor();
           recompute_basics();
+          d_valid = false;
         }
       }
       if (theta <= 1e-12) {
