@@ -35,7 +35,7 @@
 #include <cmath>
 #include <cstdint>
 #include <limits>
-#include <cstdint>
+#include <set>
 #include <sstream>
 
 #include "swarmplan/log.hpp"
@@ -305,6 +305,19 @@ struct SimplexSolver::Impl {
           row[row_k[r]].push_back(c);
         }
     std::vector<char> rdone(k, 0), cdone(k, 0);
+    // active columns bucketed by entry count, each bucket ordered by index:
+    // the pivot column is the lowest-index one with <= 1 entries, else the
+    // lowest-index one of the smallest count (O(log k) instead of a scan)
+    std::vector<std::set<int>> bucket(k + 1);
+    for (int c = 0; c < k; ++c) bucket[col[c].size()].insert(c);
+    std::size_t min_count = 0;
+    auto resize_col = [&](int c, std::size_t from) {
+      bucket[from].erase(c);
+      const std::size_t to = col[c].size();
+      if (to >= bucket.size()) bucket.resize(to + 1);
+      bucket[to].insert(c);
+      min_count = std::min(min_count, to);
+    };
     prow.assign(k, -1);
     pcol.assign(k, -1);
     piv.assign(k, 0.0);
@@ -318,13 +331,15 @@ struct SimplexSolver::Impl {
     std::vector<int> urowc;
     for (int t = 0; t < k; ++t) {
       int q = -1;
-      std::size_t best = SIZE_MAX;
-      for (int c = 0; c < k; ++c)
-        if (!cdone[c] && col[c].size() < best) {
-          best = col[c].size();
-          q = c;
-          if (best <= 1) break;
-        }
+      if (!bucket[0].empty() || (bucket.size() > 1 && !bucket[1].empty())) {
+        const int c0 = bucket[0].empty() ? k : *bucket[0].begin();
+        const int c1 = bucket.size() > 1 && !bucket[1].empty() ? *bucket[1].begin() : k;
+        q = std::min(c0, c1);
+      } else {
+        while (bucket[min_count].empty()) ++min_count;
+        q = *bucket[min_count].begin();
+      }
+      bucket[col[q].size()].erase(q);
       double cmax = 0.0;
       for (const auto& e : col[q]) cmax = std::max(cmax, std::fabs(e.second));
       if (cmax < kSingular) {
@@ -385,6 +400,7 @@ struct SimplexSolver::Impl {
           if (!found) {  // fill-in
             cc.emplace_back(r, -mult * urowv[u]);
             row[r].push_back(urowc[u]);
+            resize_col(urowc[u], cc.size() - 1);
           }
         }
       }
@@ -399,6 +415,7 @@ struct SimplexSolver::Impl {
           if (cc[e].first == p) {
             cc[e] = cc.back();
             cc.pop_back();
+            resize_col(c, cc.size() + 1);
             break;
           }
       }
