@@ -579,12 +579,6 @@ struct SimplexSolver::Impl {
     return worst;
   }
 
-  double col_dot(int j, const std::vector<double>& y) const {
-    double s = 0.0;
-    for (const auto& [r, c] : v[j].col) s += c * y[r];
-    return s;
-  }
-
   // ------------------------------------------------------------- phases
   LpStatus run_phase(bool phase1) {
     const double ftol = opt.feas_tol;
@@ -605,7 +599,8 @@ struct SimplexSolver::Impl {
     // Row-wise copy of the constraint matrix, so the devex pivot row
     // alpha_j = rho'A_j visits only the rows where rho is nonzero (rho is
     // usually sparse). Columns are stored in ascending row order, so each
-    // alpha_j accumulates its terms in the same order as col_dot.
+    // alpha_j accumulates its terms in ascending row order, as a
+    // column-wise dot product would.
     std::vector<int> rbeg(m + 1, 0), rvar;
     std::vector<double> rval, alpha(nv(), 0.0);
     for (int j = 0; j < nv(); ++j)
@@ -657,7 +652,7 @@ struct SimplexSolver::Impl {
       if (!incremental) {
         btran(cb, y);
         // y'A_j for every column, row-wise over the nonzeros of y (same
-        // per-column summation order as col_dot)
+        // per-column summation order as a column-wise dot product)
         std::fill(alpha.begin(), alpha.end(), 0.0);
         for (int r = 0; r < m; ++r) {
           const double yr = y[r];
