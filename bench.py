@@ -2,14 +2,14 @@
 """Benchmark of the DeDLOC averaging round (grad avg + LAMB step) on B200.
 
 One step = one butterfly averaging round over a flattened gradient vector
-(pack -> fused reduce-scatter/weighted-average/all-gather over NVLink ->
-LAMB) through libsp_round.so. Default workload: ALBERT-large-sized vector
+(pack -> reduce-scatter / weighted average / all-gather over NVLink -> LAMB)
+through libsp_round.so. Default workload: ALBERT-large-sized vector
 (17,847,474 params, 32-tensor LAMB table), fp16 wire, one peer per GPU
-(G = N, weak scaling), LP-balanced uniform fractions, synthetic gradients.
+(G = N, weak scaling), LP-balanced fractions, synthetic gradients.
 
     python bench.py --gpus 1 --steps 50 --warmup 5
     torchrun --nproc-per-node 8 ... bench.py --gpus 8 --steps 50 --warmup 5
-    python bench.py --impl reference ...   # CPU oracle port on host cores
+    python bench.py --impl reference ...   # reference run_plan + oracle LAMB on host cores
 
 Prints ONE JSON line on rank 0 (stdout); diagnostics go to stderr.
 """
@@ -94,8 +94,8 @@ def wire_bytes(wire: str, block: int) -> float:
 
 def ncu_traffic(kernel_substr: str):
     """dram__bytes_read.sum + dram__bytes_write.sum of the kernel in the
-    committed `ncu --set full` capture (profiles/*/ncu_full_*.csv), bytes per
-    launch, or None when no capture of that kernel is committed."""
+    newest committed `ncu --set full` capture (profiles/*/ncu_full_*.csv),
+    bytes per launch, or None when no capture of that kernel is committed."""
     import csv
     import glob
 
@@ -120,6 +120,16 @@ def peak_hbm() -> tuple[float, str]:
             return float(json.load(f)["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 # ----------------------------------------------------------------- clocks
@@ -176,34 +186,86 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(rows)}
 
 
-# ---------------------------------------------------------- CPU baseline
-def cpu_round_time(tsizes, wire, block, G, weights, reps: int, threads: int = 0):
-    """Times the oracle's CPU round (the reference semantics restated in C,
-    OpenMP over host cores) on the full vector; returns (sec/round, threads)."""
+# ---------------------------------------------------------- CPU reference
+def make_cpu_round(tsizes, wire, block, G, weights):
+    """The path on the host: every peer's gradient packed to the wire format
+    (oracle), the weighted mean of the wire buffers by the REFERENCE's own
+    groups::run_plan (oracle/_ref: /root/reference/proj/src/groups.cpp
+    compiled unmodified; fp64, peer order), the mean rounded to the wire
+    format (oracle) and the LAMB step (oracle; the reference has no LAMB,
+    SPEC.md:519). Returns one(step, threads) -> per-phase seconds."""
     import numpy as np
 
     from oracle import oracle as O
+    from oracle import ref as R
 
     n = sum(tsizes)
-    grads = [O.fill_synthetic(n, 1, g, SIGMA) for g in range(G)]
+    grads = [None if weights[g] == 0 else O.fill_synthetic(n, 1, g, SIGMA) for g in range(G)]
     p = O.fill_synthetic(n, 2, 0, 0.02, 0)
     m = np.zeros(n, np.float32)
     v = np.zeros(n, np.float32)
-    O.round_cpu(wire, grads, weights, p, m, v, tsizes, HP, 1, block, threads)  # warm-up
-    ts = []
-    for r in range(reps):
+    mean = np.empty(n, np.float64)
+
+    def one(step: int, threads: int) -> dict:
+        O.set_threads(threads)
         t0 = time.perf_counter()
-        O.round_cpu(wire, grads, weights, p, m, v, tsizes, HP, r + 2, block, threads)
-        ts.append(time.perf_counter() - t0)
-    return statistics.median(ts), (threads or O.max_threads())
+        packed = [None if x is None else O.pack(wire, x, block) for x in grads]
+        t1 = time.perf_counter()
+        R.weighted_mean_wire(wire, packed, weights, block, threads=threads, out=mean)
+        t2 = time.perf_counter()
+        avg, avg_s = O.wire_from_f64(wire, mean, block)
+        t3 = time.perf_counter()
+        O.lamb(wire, avg, avg_s, p, m, v, tsizes, HP, step, block)
+        t4 = time.perf_counter()
+        return {"pack_s": t1 - t0, "average_s": t2 - t1, "to_wire_s": t3 - t2, "lamb_s": t4 - t3,
+                "round_s": t4 - t0}
+
+    return one
+
+
+def host_threads() -> int:
+    return len(os.sched_getaffinity(0))  # every host core (torchrun sets OMP_NUM_THREADS=1)
+
+
+def cpu_baseline(tsizes, wire, block, G, weights, grad_bytes, budget_s: float = 30.0) -> dict:
+    """the CPU path in two modes, 1 thread (the reference is
+    single-threaded, proj/CMakeLists.txt:12) and every host core; median of
+    10 rounds after 2 warm-ups (fewer rounds when 12 would exceed the time
+    budget: the sample stays bounded)."""
+    one = make_cpu_round(tsizes, wire, block, G, weights)
+    modes = {}
+    step = 0
+    for label, th in (("1_thread", 1), ("all_cores", host_threads())):
+        step += 1
+        t_first = one(step, th)["round_s"]  # warm-up 1
+        step += 1
+        one(step, th)  # warm-up 2
+        reps = int(max(3, min(10, budget_s / 2 / max(t_first, 1e-6))))
+        runs = []
+        for _ in range(reps):
+            step += 1
+            runs.append(one(step, th))
+        med = {k: statistics.median(r[k] for r in runs) for k in runs[0]}
+        modes[label] = {"threads": th, "rounds": reps,
+                        "round_ms": round(med["round_s"] * 1e3, 3),
+                        "value": round(grad_bytes / med["round_s"] / 1e9, 4),
+                        "phase_ms": {k.replace("_s", "_ms"): round(x * 1e3, 3) for k, x in med.items()
+                                     if k != "round_s"}}
+    best = modes["all_cores"]
+    return {"value": best["value"], "unit": "GB/s", "cores": best["threads"], "kind": "reference",
+            "round_ms": best["round_ms"], "cpu_model": cpu_model(), "modes": modes,
+            "sample": f"full {len(tsizes)}-tensor vector ({sum(tsizes)} params), G={G}, {wire} wire: "
+                      "oracle pack -> reference groups::run_plan weighted mean (oracle/_ref, "
+                      "column blocks over threads) -> wire -> oracle LAMB; median of "
+                      f"{modes['1_thread']['rounds']} (1 thread) / {best['rounds']} (all cores) "
+                      "rounds after 2 warm-ups"}
 
 
 def lp_solve_times() -> dict:
     """Host LP (strategy solve) time, median of 5, for the fleets the budget is
     quoted on (< 50 ms at n = 16: PAPER.md:140)."""
-    from paper_2106_10207_b200.fleets import homogeneous, spec_json
-
     from paper_2106_10207_b200 import _swarmplan
+    from paper_2106_10207_b200.fleets import homogeneous, spec_json
 
     out = {}
     for name, sj in (("n4_homogeneous", json.dumps(homogeneous(4, 1.0, 1000.0, 4.0, 17847474))),
@@ -224,6 +286,25 @@ from paper_2106_10207_b200.roofline import (NVLINK_GBS, overlap_roofline, rank_m
                                             round_roofline)
 
 
+def dominant_kernel(ph: dict, model: dict, world: int, L: int, n: int, b: float, shard: bool,
+                    peak: float) -> dict:
+    """Roofline of the longest kernel of one rank's phased round: §8(d)
+    algorithmic bytes of one launch / its event-timed duration."""
+    f_r, alg = model["f"], model["alg"]
+    dom = max(("pack_ms", "reduce_ms", "lamb_ms"), key=lambda k: ph[k])
+    achieved = alg[dom] / (ph[dom] * 1e-3) / 1e9
+    bound, pk = "hbm", peak
+    if shard and dom == "lamb_ms" and world > 1:  # parameter push: (world-1) f 4 B out
+        bound, pk = "nvlink", NVLINK_GBS
+        achieved = (world - 1) * f_r * 4.0 * n / (ph[dom] * 1e-3) / 1e9
+    elif dom in ("reduce_ms", "pack_ms") and world > 1:
+        bound, pk = "nvlink", NVLINK_GBS
+        # per direction: pack scatters L (1-f) b n, reduce pushes (world-1) f b n
+        nvl = (L * (1 - f_r) * b * n) if dom == "pack_ms" else ((world - 1) * f_r * b * n)
+        achieved = nvl / (ph[dom] * 1e-3) / 1e9
+    return {"kernel": dom, "bound": bound, "achieved": achieved, "peak": pk}
+
+
 # ------------------------------------------------------------------ main
 def main():
     ap = argparse.ArgumentParser()
@@ -234,6 +315,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="albert-large-fp16")
     ap.add_argument("--peers-per-gpu", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-virtual-peers", action="store_true",
+                    help="skip the N=1 8-virtual-peer pass (pack + reduce timed)")
     ap.add_argument("--phased-steps", type=int, default=20)
     ap.add_argument("--lamb", choices=["auto", "replicated", "sharded"], default="auto",
                     help="replicated: every GPU steps the all-gathered average; sharded: ZeRO-1 "
@@ -291,7 +374,7 @@ def main():
         args.shard_lamb = choose_shard_lamb(offsets, L, world, n, b, wire)
 
     if args.impl == "reference":
-        return run_reference(args, rank, world, tsizes, wire, block, G, weights, b)
+        return run_reference(args, rank, world, tsizes, wire, block, G, weights)
 
     if os.environ.get("NCCL_DEBUG", "VERSION").upper() in ("VERSION", ""):
         os.environ["NCCL_DEBUG"] = "WARN"  # keep stdout to the one JSON line
@@ -303,14 +386,17 @@ def main():
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     from paper_2106_10207_b200 import AveragingRound, fill_synthetic
-    from paper_2106_10207_b200.round import part_offsets
 
     dev = torch.device("cuda", local_rank)
     stream = torch.cuda.Stream(dev)
-    rnd = AveragingRound(n, tsizes, wire=wire, q8_block=block, peers_per_rank=L, rank=rank,
-                         world=world, device=local_rank, lr=HP["lr"],
-                         betas=(HP["beta1"], HP["beta2"]), eps=HP["eps"],
-                         weight_decay=HP["weight_decay"], shard_lamb=args.shard_lamb)
+
+    def make_round(peers, shard):
+        return AveragingRound(n, tsizes, wire=wire, q8_block=block, peers_per_rank=peers, rank=rank,
+                              world=world, device=local_rank, lr=HP["lr"],
+                              betas=(HP["beta1"], HP["beta2"]), eps=HP["eps"],
+                              weight_decay=HP["weight_decay"], shard_lamb=shard)
+
+    rnd = make_round(L, args.shard_lamb)
     if rnd.align != align:
         raise SystemExit(f"align mismatch: library {rnd.align}, planned {align}")
     rnd.set_assignment(offsets, weights)
@@ -380,28 +466,30 @@ def main():
     value = grad_bytes / (ms_step * 1e-3) / 1e9
 
     # per-kernel device times (non-graph pass with events between kernels)
-    phases = []
-    with torch.cuda.stream(stream):
-        for _ in range(args.phased_steps):
-            step += 1
-            phases.append(rnd.run_phased(grads, p, m, v, step, stream))
-    keys = [k for k in phases[0] if k != "total_ms"]
-    ph = {k: statistics.mean(x[k] for x in phases) for k in keys}
-    ph["total_ms"] = statistics.mean(x["total_ms"] for x in phases)
+    def phased(r, gs, pp, mm, vv, k):
+        nonlocal step
+        out = []
+        with torch.cuda.stream(stream):
+            for _ in range(k):
+                step += 1
+                out.append(r.run_phased(gs, pp, mm, vv, step, stream))
+        return {key: statistics.median(x[key] for x in out) for key in out[0]}
 
-    # e2e through the public API with host buffers (sp_round_run_host): H2D
-    # of this rank's accumulated gradients from pinned memory into a
-    # double-buffered staging area (step k's copy overlaps round k-1), the
-    # round, D2H of the step's trust ratios
+    ph = phased(rnd, grads, p, m, v, args.phased_steps)
+
+    # e2e through the public API with host buffers: H2D of this rank's
+    # accumulated gradients from pinned memory into double-buffered device
+    # staging (step k's copy overlaps round k-1), the round, and the D2H of
+    # the step's result, the updated parameters (p_out). PCIe is full
+    # duplex, so the parameter read-back overlaps the next upload.
     host_g = [gg.cpu().pin_memory() for gg in grads]
-    trust_h = torch.empty(len(tsizes), dtype=torch.float32).pin_memory()
+    p_host = torch.empty(n, dtype=torch.float32).pin_memory()
     e2e_steps = max(3, min(args.steps, 20))
 
     def one_host():
         nonlocal step
         step += 1
-        rnd.run_host(host_g, p, m, v, step, stream)
-        rnd.copy_trust_async(trust_h.data_ptr(), stream)  # D2H of the step's result
+        rnd.run_host(host_g, p, m, v, step, stream, p_out=p_host)
 
     with torch.cuda.stream(stream):
         for _ in range(3):  # captures the graphs of both staging buffers
@@ -427,38 +515,38 @@ def main():
     if world > 1:
         all_ph = [None] * world
         torch.distributed.all_gather_object(all_ph, ph)
+    nwin = rnd.lamb_windows()
+    rnd.close()
+    del host_g, p_host
+
+    # N=1 only: the same vector split over 8 virtual peers on this GPU, so
+    # that the pack and the weighted reduce (which a one-peer round skips)
+    # are timed in the driver's own bench run too
+    virt = None
+    if world == 1 and L == 1 and not args.no_virtual_peers:
+        try:
+            virt = virtual_peer_pass(make_round, n, wire, b, dev, stream, args, fill_synthetic)
+        except Exception as e:  # a diagnostic; never fails the bench line
+            log("virtual-peer pass failed:", e)
 
     if rank == 0:
         peak, peak_kind = peak_hbm()
         shard = args.shard_lamb
-        fused = ph["update_ms"] < 0.1 * ph["moments_ms"] and not shard  # fused LAMB: one kernel
         # one GPU, one peer, fp32/fp16: the pack runs inside LAMB pass 1
-        fused_pack = world == 1 and L == 1 and wire != "q8" and fused
-        models = [rank_model(r, offsets, L, world, n, b, wire, shard, fused, fused_pack)
+        fused_pack = world == 1 and L == 1 and wire != "q8"
+        models = [rank_model(r, offsets, L, world, n, b, wire, shard, fused_pack)
                   for r in range(world)]
         # critical rank: the one with the longest modeled round (non-uniform
         # LP splits put the big owner on the critical path);
         # every rank's phased times include waiting for it at the barriers
         rc = max(range(world), key=lambda r: (round_roofline([models[r]], n, peak), -r))
         phc, mc = all_ph[rc], models[rc]
-        f_r, alg = mc["f"], mc["alg"]
-        dom = max(("pack_ms", "reduce_ms", "moments_ms", "update_ms"), key=lambda k: phc[k])
+        dk = dominant_kernel(phc, mc, world, L, n, b, shard, peak)
+        dom = dk["kernel"]
         widx = {"fp32": 0, "fp16": 1, "q8": 2}[wire]
         kname = {"pack_ms": f"k_pack_{wire}", "reduce_ms": f"k_reduce_{wire}",
-                 "moments_ms": (f"k_lamb_fused<{widx}>" if fused else
-                                f"k_lamb_moments_shard<{widx}>" if shard else f"k_lamb_moments<{widx}>"),
-                 "update_ms": (f"k_lamb_update_push_trust<{widx}>" if shard
-                               else f"k_lamb_update<{widx}>")}[dom]
-        achieved = alg[dom] / (phc[dom] * 1e-3) / 1e9
-        bound, pk, unit = "hbm", peak, "GB/s"
-        if shard and dom == "update_ms" and world > 1:  # parameter push: (world-1) f 4 B out
-            bound, pk = "nvlink", NVLINK_GBS
-            achieved = (world - 1) * f_r * 4.0 * n / (phc[dom] * 1e-3) / 1e9
-        elif dom in ("reduce_ms", "pack_ms") and world > 1:
-            bound, pk = "nvlink", NVLINK_GBS
-            # per direction: pack scatters L (1-f) b n, reduce pushes (world-1) f b n
-            nvl = (L * (1 - f_r) * b * n) if dom == "pack_ms" else ((world - 1) * f_r * b * n)
-            achieved = nvl / (phc[dom] * 1e-3) / 1e9
+                 "lamb_ms": f"k_lamb<{widx}>"}[dom]
+        traffic = (ncu_traffic(kname) if table == "albert-large" and world == 1 and L == 1 else None)
         # whole-round roofline (per phase on the slowest rank)
         hbm_round = max(x["hbm"] for x in models)
         nvl_round = max(x["nvl"] for x in models)
@@ -472,14 +560,11 @@ def main():
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             try:
-                sec, cores = cpu_round_time(tsizes, wire, block, G, weights, reps=3)
-                cpu = {"value": round(grad_bytes / sec / 1e9, 4), "unit": "GB/s", "cores": cores,
-                       "kind": "port", "round_ms": round(sec * 1e3, 3),
-                       "sample": f"oracle C round (OpenMP), full {table} vector, G={G}, "
-                                 f"{wire} wire, median of 3 rounds"}
+                cpu = cpu_baseline(tsizes, wire, block, G, weights, grad_bytes)
             except Exception as e:
                 log("cpu baseline failed:", e)
         fr = [round(x, 6) for x in plan["fractions"]]
+        alg_b = mc["alg"].get(dom)
         out = {
             "metric": METRIC,
             "value": round(value, 3),
@@ -499,32 +584,30 @@ def main():
                        "wire": wire, "q8_block": block if wire == "q8" else None,
                        "lamb": "sharded (ZeRO-1: owners step, fp32 params pushed)" if args.shard_lamb
                                else "replicated (averaged gradient all-gathered)",
-                       "shard_cut": rnd.shard_cut() if args.shard_lamb else None,
+                       "lamb_windows": nwin,
                        "fleet": fleet or f"homogeneous{G}",
                        "fractions": fr if G <= 16 else f"{min(fr)}..{max(fr)}",
                        "plan": "solve_strategy (host LP) -> part_offsets; weights = LP sample "
                                f"counts scaled to batch {TARGET_BATCH:g}",
                        "l2": f"no flush: per-step working set {(n * (12 + 4 * L + 2 * b)) / 1e9:.2f} GB > 126 MB L2",
                        "parallelism": f"dp{world} (one process per GPU, {L} peer(s) each, CUDA IPC over NVLink)"},
-            # replicated: pack (fused into LAMB on one GPU with one peer) + reduce
-            # + LAMB (1 fused / 3 unfused) + 2 barriers if N > 1
-            # sharded: pack, reduce, pass 1 (+norms), pass 2 + push (+trust),
-            # barriers after the pack, the norms and the push
-            "gpu_launches": args.steps * (
-                (1 + (1 if G > 1 else 0) + 2 + (3 if world > 1 else 0)) if shard else
-                ((0 if fused_pack else 1) + (1 if G > 1 else 0) + (1 if fused else 3)
-                 + (2 if world > 1 else 0))),
+            # pack (fused into LAMB on one GPU with one peer) + reduce (G > 1)
+            # + k_lamb + barriers (N > 1: after the scatter, and after the
+            # push of the averages (replicated) or of the parameters (sharded))
+            "gpu_launches": args.steps * ((0 if fused_pack else 1) + (1 if G > 1 else 0) + 1
+                                          + (2 if world > 1 else 0)),
             "kernel_ms": {k: round(v_, 5) for k, v_ in ph.items()},
             "kernel_ms_critical_rank": {k: round(v_, 5) for k, v_ in phc.items()} if rc else None,
-            "roofline": {"bound": bound, "kernel": dom.replace("_ms", ""), "rank": rc,
-                         "achieved": round(achieved, 1), "peak": pk, "unit": unit,
-                         "frac": round(achieved / pk, 4),
-                         # committed captures are single-GPU ALBERT-large launches: only
-                         # comparable per launch to the same configuration
-                         "traffic": (ncu_traffic(kname) if table == "albert-large" and world == 1
-                                     and L == 1 else None),
-                         "algorithmic_bytes": alg[dom],
-                         "peak_kind": peak_kind if bound == "hbm" else "measured peer copy per direction (B200_PROFILING.md)"},
+            "roofline": {"bound": dk["bound"], "kernel": kname, "rank": rc,
+                         "achieved": round(dk["achieved"], 1), "peak": dk["peak"], "unit": "GB/s",
+                         "frac": round(dk["achieved"] / dk["peak"], 4),
+                         "traffic": traffic,
+                         "traffic_over_alg": round(traffic / alg_b, 4) if traffic and alg_b else None,
+                         "algorithmic_bytes": alg_b,
+                         "algorithmic_B_per_param": round(alg_b / n, 3) if alg_b else None,
+                         "kernel_bytes": mc["impl"].get(dom),
+                         "peak_kind": peak_kind if dk["bound"] == "hbm" else
+                                      "measured peer copy per direction (B200_PROFILING.md)"},
             # primary: the overlap bound (a lower bound on the round time; the
             # §8d serialized sum is not one: large N=4 rounds beat it)
             "round_roofline": {"t_roof_us": round(t_ovl * 1e6, 2),
@@ -536,57 +619,104 @@ def main():
                                         f"NVLink B/{NVLINK_GBS:g} GB/s)",
                                "t_roof_serialized_us": round(t_roof * 1e6, 2),
                                "frac_serialized": round(t_roof * 1e3 / ms_step, 4)},
+            "virtual_peers_n1": virt,
             "e2e": {"value": round(e2e_value, 3), "unit": "GB/s",
                     "round_us": round(e2e_step * 1e3, 2),
-                    "h2d_bytes_per_step": 4 * n * L, "d2h_bytes_per_step": 4 * len(tsizes),
-                    "api": "AveragingRound.run_host -> sp_round_run_host (pinned host gradients; "
-                           "step k's H2D overlaps round k-1)"},
+                    "h2d_bytes_per_step": 4 * n * L, "d2h_bytes_per_step": 4 * n,
+                    "api": "AveragingRound.run_host(p_out=) -> sp_round_run_host_params (pinned host "
+                           "gradients in, updated parameters out; step k's H2D overlaps round k-1 "
+                           "and the D2H of step k-1)"},
             "clocks": clk,
             "cpu_baseline": cpu,
             "lp_solve_ms": lp_times,
         }
         emit(out)
-    rnd.close()
     if world > 1:
         torch.distributed.destroy_process_group()
 
 
-def run_reference(args, rank, world, tsizes, wire, block, G, weights, b):
-    """--impl reference: the reference path on host cores. The reference
-    cannot be built here (Eigen/KLU missing), so this times the
-    oracle port of its semantics (groups::run_plan weighted mean + the
-    framework's wire/LAMB definition) with every host thread."""
+def virtual_peer_pass(make_round, n, wire, b, dev, stream, args, fill_synthetic) -> dict:
+    """One GPU hosting all 8 peers of a uniform fleet: times the round and,
+    from a phased pass, the pack, reduce and LAMB kernels against §8(d)."""
+    import torch
+
+    Gv = 8
+    rv = make_round(Gv, False)
+    rv.assign([1.0 / Gv] * Gv, [TARGET_BATCH / Gv] * Gv)
+    gv = []
+    for l in range(Gv):
+        t_ = torch.empty(n, dtype=torch.float32, device=dev)
+        fill_synthetic(t_, 1, l, SIGMA)
+        gv.append(t_)
+    pv = torch.empty(n, dtype=torch.float32, device=dev)
+    fill_synthetic(pv, 2, 0, 0.02, 0)
+    mv, vv = torch.zeros_like(pv), torch.zeros_like(pv)
+    step = 0
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            step += 1
+            rv.run(gv, pv, mv, vv, step, stream)
+        torch.cuda.synchronize(dev)
+        v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        v0.record(stream)
+        for _ in range(args.steps):
+            step += 1
+            rv.run(gv, pv, mv, vv, step, stream)
+        v1.record(stream)
+        torch.cuda.synchronize(dev)
+        vms = v0.elapsed_time(v1) / args.steps
+        out = []
+        for _ in range(args.phased_steps):
+            step += 1
+            out.append(rv.run_phased(gv, pv, mv, vv, step, stream))
+    vph = {key: statistics.median(x[key] for x in out) for key in out[0]}
+    model = rank_model(0, rv.offsets, Gv, 1, n, b, wire, False, False)
+    peak = peak_hbm()[0]
+    kern = {}
+    for k in ("pack_ms", "reduce_ms", "lamb_ms"):
+        gbs = model["alg"][k] / (vph[k] * 1e-3) / 1e9
+        kern[k.replace("_ms", "")] = {"ms": round(vph[k], 5), "algorithmic_bytes": model["alg"][k],
+                                      "achieved_gbs": round(gbs, 1), "frac": round(gbs / peak, 4)}
+    rv.close()
+    return {"peers": Gv, "round_us": round(vms * 1e3, 2),
+            "value": round(4.0 * n * Gv / (vms * 1e-3) / 1e9, 3), "unit": "GB/s", "kernels": kern,
+            "note": "N=1 with 8 virtual peers (one GPU holds all 8 peers' gradients): §8(d) bytes, "
+                    "pack 4+b per peer element, reduce G f b + f b, LAMB 24+b"}
+
+
+def run_reference(args, rank, world, tsizes, wire, block, G, weights):
+    """--impl reference: the path on the host cores with the reference's own
+    code where it exists (groups::run_plan from oracle/_ref, column blocks
+    spread over every host thread) and the oracle for what the reference
+    lacks (wire pack, LAMB). Rank 0 only."""
     if rank != 0:
         return 0
     n = sum(tsizes)
     reps = max(1, args.steps)
-    import numpy as np
-
-    from oracle import oracle as O
-
-    grads = [O.fill_synthetic(n, 1, g, SIGMA) for g in range(G)]
-    p = O.fill_synthetic(n, 2, 0, 0.02, 0)
-    m = np.zeros(n, np.float32)
-    v = np.zeros(n, np.float32)
-    threads = len(os.sched_getaffinity(0))  # every host core (torchrun sets OMP_NUM_THREADS=1)
+    threads = host_threads()
+    one = make_cpu_round(tsizes, wire, block, G, weights)
     for w in range(args.warmup):
-        O.round_cpu(wire, grads, weights, p, m, v, tsizes, HP, w + 1, block, threads)
-    t0 = time.perf_counter()
-    for r in range(reps):
-        O.round_cpu(wire, grads, weights, p, m, v, tsizes, HP, args.warmup + r + 1, block, threads)
-    sec = (time.perf_counter() - t0) / reps
+        one(w + 1, threads)
+    runs = [one(args.warmup + r + 1, threads) for r in range(reps)]
+    sec = statistics.mean(r["round_s"] for r in runs)
     grad_bytes = 4.0 * n * G
     val = grad_bytes / sec / 1e9
-    cores = threads
+    phase = {k.replace("_s", "_ms"): round(statistics.median(r[k] for r in runs) * 1e3, 3)
+             for k in runs[0] if k != "round_s"}
     out = {
         "metric": METRIC, "impl": "reference", "value": round(val, 4), "unit": "GB/s",
         "n_gpus": world, "steps": reps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": wire, "data": "synthetic",
+        "dtype": {"fp32": "f32", "fp16": "f16 wire / f32 accum", "q8": "u8 wire / f32 accum"}[wire],
+        "data": "synthetic",
         "config": {"workload": f"{args.workload}: DeDLOC butterfly round + LAMB", "params": n,
-                   "tensors": len(tsizes), "peers": G, "wire": wire},
-        "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": cores, "kind": "port",
-                         "sample": f"full vector, G={G} peers simulated on host, {reps} rounds"},
+                   "tensors": len(tsizes), "peers": G, "peers_per_gpu": G // max(world, 1),
+                   "wire": wire},
+        "phase_ms": phase,
+        "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": threads, "kind": "reference",
+                         "cpu_model": cpu_model(),
+                         "sample": f"full vector, G={G} peers on the host, {reps} rounds: oracle pack -> "
+                                   "reference groups::run_plan (oracle/_ref) -> wire -> oracle LAMB"},
         "e2e": {"value": round(val, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }

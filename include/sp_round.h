@@ -28,6 +28,14 @@
  *
  * Status codes: every function returns SP_OK (0) or an SP_ERR_* code; the
  * message of the last failure on the calling thread is sp_last_error().
+ *
+ * Streams: every `void* stream` argument is a cudaStream_t and NULL is the
+ * CUDA legacy default stream, as everywhere in CUDA. All work of a call is
+ * ordered on that stream: it starts after the work the caller enqueued
+ * before it (e.g. the backward pass writing the gradients) and the next
+ * work on the stream (e.g. the forward reading p) starts after the round.
+ * Host-input rounds copy on an internal stream that is joined to `stream`
+ * with events.
  */
 #ifndef SP_ROUND_H_
 #define SP_ROUND_H_
@@ -77,26 +85,26 @@ typedef struct {
   double barrier_timeout_s; /* cross-rank spin limit (0 -> 20 s)             */
   int shard_lamb;      /* 1: sharded LAMB (ZeRO-1 style): each
                         * rank steps only the range it owns, per-tensor norm
-                        * partials are exchanged over NVLink, and the updated
-                        * parameters (not the averaged gradient) are pushed to
-                        * every rank. p must be sp_round_param_ptr(); m and v
-                        * stay full-length but only the owned range is kept.
-                        * Pays off on uniform splits; with a dominant owner the
-                        * replicated mode is faster (the Python planner's
-                        * roofline.choose_shard_lamb picks per plan). */
+                        * sums are exchanged over NVLink inside the LAMB
+                        * kernel, and the updated parameters (not the averaged
+                        * gradient) are pushed to every rank. p must be
+                        * sp_round_param_ptr(); m and v stay full-length but
+                        * only the owned range is kept. Pays off on uniform
+                        * splits; with a dominant owner the replicated mode is
+                        * faster (roofline.choose_shard_lamb picks per plan). */
 } sp_round_cfg;
 
-/* Per-kernel device times of the last sp_round_run_phased call (ms). */
+/* Per-phase device times of the last sp_round_run_phased call (ms). */
 typedef struct {
-  float pack_ms;      /* K1: fp32 -> wire                                    */
-  float barrier_a_ms; /* cross-rank barrier before the exchange (0 if N=1)   */
-  float reduce_ms;    /* K2: fused reduce-scatter / average / all-gather     */
-  float barrier_b_ms; /* cross-rank barrier after the exchange (sharded: none) */
-  float moments_ms;   /* K3: LAMB moments + per-chunk norm partials (sharded:
-                         + norm publication; replicated, fused: whole LAMB)  */
-  float trust_ms;     /* per-tensor trust ratios (sharded: the norm barrier) */
-  float update_ms;    /* K4: LAMB parameter update (sharded: + parameter push
-                         + the closing barrier)                              */
+  float pack_ms;      /* K1: fp32 -> wire + scatter to the owners (0 when fused
+                         into LAMB: one rank, one peer, fp32/fp16 wire)      */
+  float barrier_a_ms; /* cross-rank barrier after the scatter (0 if N=1)     */
+  float reduce_ms;    /* K2: weighted average of the owned range (+ push of the
+                         averages to every rank with replicated LAMB)        */
+  float barrier_b_ms; /* barrier after the push (replicated LAMB, N>1)       */
+  float lamb_ms;      /* K3: k_lamb, both LAMB passes (sharded: + norm
+                         exchange and parameter push)                        */
+  float barrier_c_ms; /* closing barrier (sharded LAMB, N>1)                 */
   float total_ms;
 } sp_phase_times;
 
@@ -125,7 +133,7 @@ int sp_round_set_assignment(sp_round* r, const int64_t* offsets,
                             const double* weights);
 
 /* One averaging round + LAMB step, stream-ordered on `stream`
- * (cudaStream_t; NULL = the executor's own stream). grads[l] is the
+ * (cudaStream_t; NULL = legacy default stream). grads[l] is the
  * accumulated gradient of local peer l (device fp32[n]; NULL for an
  * aggregation-only peer whose weight is 0). p/m/v are this rank's replica
  * (device fp32[n]), updated in place. `step` is the 1-based optimizer step
@@ -147,6 +155,16 @@ int sp_round_run(sp_round* r, const float* const* grads, float* p, float* m,
 int sp_round_run_host(sp_round* r, const float* const* host_grads, float* p,
                       float* m, float* v, int step, void* stream);
 
+/* sp_round_run_host that also returns the step's result: the updated
+ * parameters p (n floats) are copied into host_p_out (pinned, or the copy is
+ * synchronous) on `stream` after the round (the device->host half of
+ * groups::run_plan's by-value result, proj/src/groups.cpp:154-161). PCIe is
+ * full duplex, so this copy overlaps the next step's gradient upload.
+ * host_p_out == NULL is sp_round_run_host. */
+int sp_round_run_host_params(sp_round* r, const float* const* host_grads, float* p,
+                             float* m, float* v, int step, float* host_p_out,
+                             void* stream);
+
 /* Same round without graph capture, with CUDA events between phases;
  * synchronizes the stream and fills *t. Diagnostic only. */
 int sp_round_run_phased(sp_round* r, const float* const* grads, float* p,
@@ -166,14 +184,10 @@ void* sp_round_wire_ptr(sp_round* r, int local_peer);
  * every rank's copy (NULL without shard_lamb). */
 float* sp_round_param_ptr(sp_round* r);
 
-/* shard_lamb: element index c (a tensor edge) of the hybrid split chosen at
- * sp_round_set_assignment: tensors in [0, c) keep the replicated LAMB (every
- * rank steps them, full-length m/v) on a second stream while tensors in
- * [c, n) are sharded, so the HBM-bound and NVLink-bound halves can overlap.
- * Default c = 0 (everything sharded; the overlap was measured slower, the
- * halves contend for SMs and HBM); SP_SHARD_FRACTION=<share>|model selects a
- * split for experiments. -1 without shard_lamb. */
-int64_t sp_round_shard_cut(const sp_round* r);
+/* Number of tensor windows of the LAMB plan (replicated LAMB: consecutive
+ * tensors whose per-SM share of u fits half the shared-memory stash; sharded:
+ * 1). Valid after sp_round_set_assignment; -1 for a null handle. */
+int sp_round_lamb_windows(const sp_round* r);
 void* sp_round_avg_ptr(sp_round* r);
 int64_t sp_round_padded_n(const sp_round* r);
 /* Per-tensor trust ratios of the last step (device float[num_tensors]). */

@@ -33,6 +33,7 @@ struct RoundConfig {
   float lr = 1.76e-3f, beta1 = 0.9f, beta2 = 0.999f, eps = 1e-6f, weight_decay = 0.01f;
   bool bias_correction = true;
   double barrier_timeout_s = 20.0;
+  bool shard_lamb = false;  // sp_round_cfg::shard_lamb (p must be param_buffer())
 };
 
 class AveragingRound {
@@ -58,8 +59,12 @@ class AveragingRound {
   void run(const float* const* grads, float* p, float* m, float* v, int step, void* stream = nullptr);
   // Same round from pinned HOST gradients (sp_round_run_host): the copy of
   // step k overlaps round k-1 through double-buffered device staging.
+  // host_p_out != nullptr also copies the updated parameters back to the
+  // host after the round (sp_round_run_host_params).
   void run_host(const float* const* host_grads, float* p, float* m, float* v, int step,
-                void* stream = nullptr);
+                void* stream = nullptr, float* host_p_out = nullptr);
+  // shard_lamb: the flat parameter vector the round updates (device fp32[n]).
+  float* param_buffer() const;
   sp_phase_times run_phased(const float* const* grads, float* p, float* m, float* v, int step,
                             void* stream = nullptr);
 
@@ -74,6 +79,7 @@ class AveragingRound {
   const std::vector<std::int64_t>& offsets() const { return offsets_; }
   sp_round* handle() const { return h_; }
   int peers() const { return cfg_.peers_per_rank * cfg_.world; }
+  int local_peers() const { return cfg_.peers_per_rank; }
 
  private:
   RoundConfig cfg_;

@@ -63,6 +63,9 @@ def lib():
                                          ctypes.c_int, ctypes.POINTER(LambHP), ctypes.c_int,
                                          ctypes.c_int, ctypes.c_void_p]
         _lib.sp_oracle_max_threads.restype = ctypes.c_int
+        _lib.sp_oracle_set_threads.argtypes = [ctypes.c_int]
+        _lib.sp_oracle_wire_from_f64.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                                 ctypes.c_void_p, ctypes.c_int64, ctypes.c_int]
     return _lib
 
 
@@ -168,3 +171,17 @@ def round_cpu(wire: str, grads: list[np.ndarray], weights, p, m, v, tensor_sizes
 
 def max_threads() -> int:
     return int(lib().sp_oracle_max_threads())
+
+
+def set_threads(threads: int) -> None:
+    lib().sp_oracle_set_threads(int(threads))
+
+
+def wire_from_f64(wire: str, x: np.ndarray, block: int = 4096):
+    """fp64 -> fp32 -> wire format; returns (values, scales) like pack()."""
+    x = np.ascontiguousarray(x, np.float64)
+    dtype = {"fp32": np.float32, "fp16": np.uint16, "q8": np.int8}[wire]
+    out = np.empty(x.size, dtype)
+    sc = np.empty((x.size + block - 1) // block, np.float32) if wire == "q8" else None
+    lib().sp_oracle_wire_from_f64(WIRE[wire], _p(x), _p(out), _p(sc), x.size, block)
+    return out, sc

@@ -330,3 +330,37 @@ int sp_oracle_max_threads(void) {
   return 1;
 #endif
 }
+
+void sp_oracle_set_threads(int threads) {
+#ifdef _OPENMP
+  if (threads > 0) omp_set_num_threads(threads);
+#else
+  (void)threads;
+#endif
+}
+
+/* fp64 values (the reference run_plan's weighted mean) rounded to fp32, then
+ * to the wire format: what a reference-side aggregator would put on the
+ * wire. out is float[n] (fp32), uint16[n] (fp16) or int8[n] + scales. */
+void sp_oracle_wire_from_f64(int wire, const double* x, void* out, float* scales, int64_t n,
+                             int block) {
+  if (wire == SPO_FP32) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) ((float*)out)[i] = (float)x[i];
+    return;
+  }
+  if (wire == SPO_FP16) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) ((uint16_t*)out)[i] = sp_oracle_f2h((float)x[i]);
+    return;
+  }
+  const int64_t nb = (n + block - 1) / block;
+#pragma omp parallel for schedule(static)
+  for (int64_t b = 0; b < nb; ++b) {
+    float tmp[16384];
+    const int64_t s = b * block;
+    const int64_t len = (n - s) < block ? (n - s) : block;
+    for (int64_t j = 0; j < len; ++j) tmp[j] = (float)x[s + j];
+    quantize_block(tmp, len, (int8_t*)out + s, scales + b);
+  }
+}

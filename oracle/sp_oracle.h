@@ -106,6 +106,11 @@ int sp_oracle_round(int wire, int block, int G, int64_t n,
                     float* trust_out);
 
 int sp_oracle_max_threads(void);
+/* OpenMP threads of the calls that follow (<= 0: unchanged). */
+void sp_oracle_set_threads(int threads);
+/* fp64 -> fp32 -> wire format (fp32 / fp16 RNE / blockwise 8-bit). */
+void sp_oracle_wire_from_f64(int wire, const double* x, void* out, float* scales, int64_t n,
+                             int block);
 
 #ifdef __cplusplus
 }

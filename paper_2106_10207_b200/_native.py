@@ -13,7 +13,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("SP_ROUND_LIB") or os.path.join(_HERE, "lib", "libsp_round.so")
+LIB_PATH = os.path.join(_HERE, "lib", "libsp_round.so")
 
 SP_OK, SP_ERR_ARG, SP_ERR_CUDA, SP_ERR_STATE, SP_ERR_PEER, SP_ERR_SHAPE = range(6)
 SP_WIRE_FP32, SP_WIRE_FP16, SP_WIRE_Q8 = range(3)
@@ -45,8 +45,8 @@ class SpRoundCfg(ctypes.Structure):
 
 class SpPhaseTimes(ctypes.Structure):
     _fields_ = [(k, ctypes.c_float) for k in (
-        "pack_ms", "barrier_a_ms", "reduce_ms", "barrier_b_ms", "moments_ms", "trust_ms",
-        "update_ms", "total_ms")]
+        "pack_ms", "barrier_a_ms", "reduce_ms", "barrier_b_ms", "lamb_ms", "barrier_c_ms",
+        "total_ms")]
 
 
 class PeerTimeout(RuntimeError):
@@ -76,12 +76,13 @@ def lib() -> ctypes.CDLL:
         "sp_round_set_assignment": (c_int, [vp, ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double)]),
         "sp_round_run": (c_int, [vp, ctypes.POINTER(vp), vp, vp, vp, c_int, vp]),
         "sp_round_run_host": (c_int, [vp, ctypes.POINTER(vp), vp, vp, vp, c_int, vp]),
+        "sp_round_run_host_params": (c_int, [vp, ctypes.POINTER(vp), vp, vp, vp, c_int, vp, vp]),
         "sp_round_run_phased": (c_int, [vp, ctypes.POINTER(vp), vp, vp, vp, c_int, vp,
                                         ctypes.POINTER(SpPhaseTimes)]),
         "sp_round_wire_ptr": (vp, [vp, c_int]),
         "sp_round_avg_ptr": (vp, [vp]),
         "sp_round_param_ptr": (vp, [vp]),
-        "sp_round_shard_cut": (i64, [vp]),
+        "sp_round_lamb_windows": (c_int, [vp]),
         "sp_round_padded_n": (i64, [vp]),
         "sp_round_trust_ptr": (vp, [vp]),
         "sp_round_copy_trust": (c_int, [vp, vp, vp]),
@@ -110,9 +111,8 @@ def lib() -> ctypes.CDLL:
 EXPORTED_SYMBOLS = [
     "sp_round_create", "sp_round_destroy", "sp_round_handle_bytes", "sp_round_export",
     "sp_round_connect", "sp_round_align", "sp_round_set_assignment", "sp_round_run",
-    "sp_round_run_host", "sp_round_run_phased", "sp_round_wire_ptr", "sp_round_avg_ptr", "sp_round_param_ptr",
-    "sp_round_shard_cut",
-    "sp_round_padded_n",
+    "sp_round_run_host", "sp_round_run_host_params", "sp_round_run_phased", "sp_round_wire_ptr",
+    "sp_round_avg_ptr", "sp_round_param_ptr", "sp_round_lamb_windows", "sp_round_padded_n",
     "sp_round_trust_ptr", "sp_round_copy_trust", "sp_round_read", "sp_round_accumulate", "sp_round_accumulator_ptr",
     "sp_round_add_samples", "sp_round_samples", "sp_round_run_accumulated",
     "sp_vec_scale", "sp_vec_sum", "sp_vec_div", "sp_fill_synthetic", "sp_version", "sp_last_error",

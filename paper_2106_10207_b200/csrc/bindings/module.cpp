@@ -2,9 +2,11 @@
 // (/root/reference/proj/bindings/module.cpp:92-146, re-exported by
 // proj/python/swarmplan/__init__.py) with the same names, argument meaning
 // and errors (SpecParseError -> ValueError subclass), plus the hooks the
-// averaging round needs: part_offsets, plan_parts, run_plan and the LP.
-// The GPU round itself is driven from Python through the C-ABI
-// (paper_2106_10207_b200/round.py); the GIL is released around solves.
+// averaging round needs: part_offsets, plan_parts, run_plan and the LP, and
+// the GPU round itself: AveragingRound (swarmplan::round::AveragingRound over
+// the libsp_round.so C-ABI) and run_averaging_round, which takes torch CUDA
+// tensors (duck-typed: only their data pointers cross, no torch headers or
+// library are linked). The GIL is released around solves and rounds.
 
 #include <map>
 
@@ -17,6 +19,7 @@
 #include "swarmplan/model.hpp"
 #include "swarmplan/netsim.hpp"
 #include "swarmplan/partition.hpp"
+#include "swarmplan/round.hpp"
 #include "swarmplan/scenario.hpp"
 #include "swarmplan/strategy.hpp"
 
@@ -176,12 +179,14 @@ PYBIND11_MODULE(_swarmplan, m) {
         },
         py::arg("spec_json"), py::arg("n"), py::arg("align"),
         "solve_strategy + part_offsets: what each peer aggregates in the GPU round.");
+  m.def("spec_roundtrip", [](const std::string& spec_json) { return spec_to_json(spec_from_json(spec_json)); },
+        py::arg("spec_json"), "spec_to_json(spec_from_json(text)): the canonical spec JSON.");
   m.def("scenario_spec_json",
         [](const std::string& scenario_text) { return spec_to_json(scenario_from_json(scenario_text).collaboration); },
         py::arg("scenario_json"));
   m.def("run_plan",
         [](int n, int msize, py::array_t<double, py::array::c_style | py::array::forcecast> values,
-           std::vector<double> weights, std::vector<std::pair<int, int>> failures) {
+           std::vector<double> weights, std::vector<std::pair<int, int>> failures, bool exact) {
           if (values.ndim() != 2) throw std::invalid_argument("values must be 2-D (peers x dim)");
           groups::GroupPlan plan = groups::build_plan(n, msize);
           Eigen::MatrixXd v(values.shape(0), values.shape(1));
@@ -192,7 +197,8 @@ PYBIND11_MODULE(_swarmplan, m) {
           groups::RunResult res;
           {
             py::gil_scoped_release release;
-            res = groups::run_plan(plan, v, weights, fs);
+            res = groups::run_plan(plan, v, weights, fs,
+                                   exact ? groups::MergeRule::Exact : groups::MergeRule::Reference);
           }
           py::array_t<double> out({static_cast<py::ssize_t>(res.values.rows()),
                                    static_cast<py::ssize_t>(res.values.cols())});
@@ -208,12 +214,13 @@ PYBIND11_MODULE(_swarmplan, m) {
           return d;
         },
         py::arg("n"), py::arg("m"), py::arg("values"), py::arg("weights") = std::vector<double>{},
-        py::arg("failures") = std::vector<std::pair<int, int>>{},
-        "groups::run_plan on the CPU (fp64): values is peers x dim.");
+        py::arg("failures") = std::vector<std::pair<int, int>>{}, py::arg("exact") = false,
+        "groups::run_plan on the CPU (fp64): values is peers x dim. exact=True merges classes "
+        "per SPEC.md:240-241 instead of the reference's groups.cpp:126-151 rule.");
   m.def("run_plan_device",
         [](int n, int msize, std::vector<std::uintptr_t> values, std::int64_t dim,
            std::vector<std::uintptr_t> out, std::vector<double> weights,
-           std::vector<std::pair<int, int>> failures, std::uintptr_t stream) {
+           std::vector<std::pair<int, int>> failures, std::uintptr_t stream, bool exact) {
           if (static_cast<int>(values.size()) != n || static_cast<int>(out.size()) != n)
             throw std::invalid_argument("run_plan_device: one device row per peer");
           groups::GroupPlan plan = groups::build_plan(n, msize);
@@ -228,7 +235,8 @@ PYBIND11_MODULE(_swarmplan, m) {
           {
             py::gil_scoped_release release;
             res = groups::run_plan_device(plan, src.data(), dim, dst.data(), weights, fs,
-                                          reinterpret_cast<void*>(stream));
+                                          reinterpret_cast<void*>(stream),
+                                          exact ? groups::MergeRule::Exact : groups::MergeRule::Reference);
           }
           py::dict d;
           std::vector<bool> complete(res.complete.begin(), res.complete.end());
@@ -240,6 +248,7 @@ PYBIND11_MODULE(_swarmplan, m) {
         py::arg("n"), py::arg("m"), py::arg("values"), py::arg("dim"), py::arg("out"),
         py::arg("weights") = std::vector<double>{},
         py::arg("failures") = std::vector<std::pair<int, int>>{}, py::arg("stream") = 0,
+        py::arg("exact") = false,
         "groups::run_plan on the GPU: values/out are device addresses of n fp64 rows of "
         "length dim; bit-identical to run_plan.");
 
@@ -302,4 +311,96 @@ PYBIND11_MODULE(_swarmplan, m) {
                                 sol.status == lp::LpStatus::Optimal ? sol.x(sp.xi_var) * sp.xi_scale : 0.0);
         },
         py::arg("spec_json"), py::arg("pinned_compute") = std::vector<int>{});
+
+  // ---- the GPU round (run_averaging_round) -------------------
+  py::class_<round::AveragingRound>(m, "AveragingRound",
+                                    "One rank's B200 averaging round (swarmplan/round.hpp).")
+      .def(py::init([](std::int64_t n, std::vector<std::int64_t> tensor_sizes, const std::string& wire,
+                       int q8_block, int peers_per_rank, int rank, int world, int device, float lr,
+                       float beta1, float beta2, float eps, float weight_decay, bool bias_correction,
+                       double barrier_timeout_s, bool shard_lamb) {
+             round::RoundConfig c;
+             c.n = n;
+             c.tensor_sizes = std::move(tensor_sizes);
+             c.wire = wire;
+             c.q8_block = q8_block;
+             c.peers_per_rank = peers_per_rank;
+             c.rank = rank;
+             c.world = world;
+             c.device = device;
+             c.lr = lr;
+             c.beta1 = beta1;
+             c.beta2 = beta2;
+             c.eps = eps;
+             c.weight_decay = weight_decay;
+             c.bias_correction = bias_correction;
+             c.barrier_timeout_s = barrier_timeout_s;
+             c.shard_lamb = shard_lamb;
+             return std::make_unique<round::AveragingRound>(c);
+           }),
+           py::arg("n"), py::arg("tensor_sizes") = std::vector<std::int64_t>{}, py::arg("wire") = "fp16",
+           py::arg("q8_block") = 4096, py::arg("peers_per_rank") = 1, py::arg("rank") = 0,
+           py::arg("world") = 1, py::arg("device") = 0, py::arg("lr") = 1.76e-3f, py::arg("beta1") = 0.9f,
+           py::arg("beta2") = 0.999f, py::arg("eps") = 1e-6f, py::arg("weight_decay") = 0.01f,
+           py::arg("bias_correction") = true, py::arg("barrier_timeout_s") = 20.0,
+           py::arg("shard_lamb") = false)
+      .def_property_readonly("align", &round::AveragingRound::align)
+      .def_property_readonly("peers", &round::AveragingRound::peers)
+      .def_property_readonly("offsets", &round::AveragingRound::offsets)
+      .def("assign", &round::AveragingRound::assign, py::arg("fractions"), py::arg("weights"),
+           "LP fractions -> part offsets (partition.hpp) + per-peer sample counts.")
+      .def("set_assignment", &round::AveragingRound::set_assignment, py::arg("offsets"), py::arg("weights"))
+      .def("export_handle",
+           [](const round::AveragingRound& r) {
+             const std::vector<std::uint8_t> b = r.export_handle();
+             return py::bytes(reinterpret_cast<const char*>(b.data()), b.size());
+           })
+      .def("connect",
+           [](round::AveragingRound& r, const py::bytes& all) {
+             const std::string s = all;
+             r.connect(std::vector<std::uint8_t>(s.begin(), s.end()));
+           },
+           py::arg("all_handles"));
+  m.def("run_averaging_round",
+        [](round::AveragingRound& r, const py::list& grads, const py::object& p, const py::object& mom,
+           const py::object& var, int step, const py::object& stream) {
+          const std::int64_t n = r.offsets().empty() ? 0 : r.offsets().back();
+          if (n <= 0) throw std::invalid_argument("run_averaging_round: assign() first");
+          // a contiguous CUDA float32 tensor of at least n elements -> its data pointer
+          auto ptr = [n](const py::handle& t) -> std::uintptr_t {
+            if (!py::hasattr(t, "data_ptr") || !t.attr("is_cuda").cast<bool>())
+              throw std::invalid_argument("run_averaging_round: expected CUDA tensors");
+            if (py::str(t.attr("dtype")).cast<std::string>() != "torch.float32")
+              throw std::invalid_argument("run_averaging_round: tensors must be float32");
+            if (!t.attr("is_contiguous")().cast<bool>() || t.attr("numel")().cast<std::int64_t>() < n)
+              throw std::invalid_argument("run_averaging_round: tensors must be contiguous with >= n elements");
+            return t.attr("data_ptr")().cast<std::uintptr_t>();
+          };
+          std::vector<const float*> g;
+          for (const py::handle& t : grads)
+            g.push_back(t.is_none() ? nullptr : reinterpret_cast<const float*>(ptr(t)));
+          if (static_cast<int>(g.size()) != r.local_peers())
+            throw std::invalid_argument("run_averaging_round: need one gradient per local peer");
+          float* pp = reinterpret_cast<float*>(ptr(p));
+          float* mp = reinterpret_cast<float*>(ptr(mom));
+          float* vp = reinterpret_cast<float*>(ptr(var));
+          // default: torch's current stream on the tensors' device (the
+          // round is ordered after the caller's backward pass)
+          std::uintptr_t st = 0;
+          if (stream.is_none()) {
+            py::object torch = py::module_::import("torch");
+            st = torch.attr("cuda").attr("current_stream")(p.attr("device")).attr("cuda_stream").cast<std::uintptr_t>();
+          } else if (py::hasattr(stream, "cuda_stream")) {
+            st = stream.attr("cuda_stream").cast<std::uintptr_t>();
+          } else {
+            st = stream.cast<std::uintptr_t>();
+          }
+          py::gil_scoped_release release;
+          r.run(g.data(), pp, mp, vp, step, reinterpret_cast<void*>(st));
+        },
+        py::arg("round"), py::arg("grads"), py::arg("p"), py::arg("m"), py::arg("v"), py::arg("step"),
+        py::arg("stream") = py::none(),
+        "One averaging round + LAMB step on torch CUDA tensors (grads: one per local peer, None "
+        "for a weight-0 peer; p/m/v updated in place), ordered on `stream` (default: torch's "
+        "current stream). The C++ route to sp_round_run.");
 }

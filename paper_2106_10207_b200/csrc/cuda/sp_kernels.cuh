@@ -19,12 +19,16 @@
 
 namespace sp {
 
-constexpr int kLambChunk = 8192;  // elements per LAMB work item (one CTA)
+// LAMB CTA: kLambThreads threads, 1024 / kLambThreads CTAs per SM (64
+// registers per thread), so several CTAs per SM overlap their memory and
+// compute phases.
 #ifndef SP_LAMB_THREADS
 #define SP_LAMB_THREADS 256
 #endif
 constexpr int kLambThreads = SP_LAMB_THREADS;
-constexpr int kPad = 16384;       // wire/avg buffers padded to this multiple
+constexpr int kLambCtasPerSm = 1024 / kLambThreads;
+constexpr int kLambTile = 8192;     // max chunk length
+constexpr int kPad = 16384;         // wire/avg buffers padded to this multiple
 
 struct BarrierArgs {
   unsigned long long* flags[SP_MAX_RANKS];  // flags array of every rank
@@ -134,10 +138,17 @@ __device__ __forceinline__ void load_peers(const ReduceArgs& a, PeerView& pv) {
   __syncthreads();
 }
 
+// One LAMB work item: a piece of one tensor, at most kLambTile elements,
+// processed by one CTA in both passes (sp_lamb.cuh).
 struct Chunk {
   long long start;
   int len;
   int tensor;
+  int stash;  // float offset of element `start` in the CTA's stash (start - stash = 0 mod 4),
+              // -1: not stashed, pass 2 recomputes u from p, m', v'
+  int run;    // slot of this chunk's (sum p^2, sum u^2) partial
+  int last;   // 1: last chunk of its run (the partial is stored after it)
+  int pad;
 };
 
 struct LambArgs {
@@ -146,13 +157,9 @@ struct LambArgs {
   float* p;
   float* m;
   float* v;
-  const Chunk* chunks;
-  float2* partial;          // per chunk (sum p^2, sum u^2)
   const float* hp;          // device: [lr, 1/(1-b1^t), 1/(1-b2^t)]
-  const float* step_scale;  // per tensor lr * trust (update kernel only)
   float b1, b2, omb1, omb2, eps, wd;
   int qshift;               // log2(q8 block): scale index = i >> qshift
-  int l2_hints;             // fused LAMB: keep p/m/v of pass 1 in L2 for pass 2
   // one rank, one peer, fp32/fp16 wire: the pack is fused into pass 1, which
   // reads the fp32 gradient, rounds it to the wire format (the identity
   // average) and also stores the wire values (nullptr: read `avg`)
@@ -825,258 +832,15 @@ struct ChunkSplit {
   int head, nbody4, tail;
 };
 
-__device__ __forceinline__ ChunkSplit split_chunk(const Chunk& c) {
+__device__ __forceinline__ ChunkSplit split_chunk(long long start, int len) {
   ChunkSplit s;
-  s.start = c.start;
-  int head = (int)((4 - (c.start & 3)) & 3);
-  if (head > c.len) head = c.len;
+  s.start = start;
+  int head = (int)((4 - (start & 3)) & 3);
+  if (head > len) head = len;
   s.head = head;
-  s.nbody4 = (c.len - head) >> 2;
-  s.tail = c.len - head - 4 * s.nbody4;
+  s.nbody4 = (len - head) >> 2;
+  s.tail = len - head - 4 * s.nbody4;
   return s;
-}
-
-template <int W>
-__global__ void __launch_bounds__(kLambThreads) k_lamb_moments(LambArgs a) {
-  __shared__ float red_p[kLambThreads / 32], red_u[kLambThreads / 32];
-  const Chunk c = a.chunks[blockIdx.x];
-  const LambScalars s{a.hp[0], a.hp[1], a.hp[2]};
-  const ChunkSplit sp = split_chunk(c);
-  float pp = 0.0f, uu = 0.0f;
-  const int t = threadIdx.x;
-  // scalar head and tail
-  int64_t si = -1;
-  if (t < sp.head) si = sp.start + t;
-  else if (t >= 32 && t - 32 < sp.tail) si = sp.start + sp.head + 4 * (int64_t)sp.nbody4 + (t - 32);
-  if (si >= 0) {
-    const float g = load_grad1<W>(a, si);
-    const float p = a.p[si];
-    float m = a.m[si], v = a.v[si], u;
-    lamb_moments(a, s, g, p, m, v, u);
-    a.m[si] = m;
-    a.v[si] = v;
-    pp = __fmaf_rn(p, p, pp);
-    uu = __fmaf_rn(u, u, uu);
-  }
-  const int64_t b0 = sp.start + sp.head;
-  for (int k = t; k < sp.nbody4; k += kLambThreads) {
-    const int64_t i = b0 + 4 * (int64_t)k;
-    const float4 g = load_grad4<W>(a, i);
-    const float4 p = *reinterpret_cast<const float4*>(a.p + i);
-    float4 m = *reinterpret_cast<const float4*>(a.m + i);
-    float4 v = *reinterpret_cast<const float4*>(a.v + i);
-    float4 u;
-    lamb_moments(a, s, g.x, p.x, m.x, v.x, u.x);
-    lamb_moments(a, s, g.y, p.y, m.y, v.y, u.y);
-    lamb_moments(a, s, g.z, p.z, m.z, v.z, u.z);
-    lamb_moments(a, s, g.w, p.w, m.w, v.w, u.w);
-    *reinterpret_cast<float4*>(a.m + i) = m;
-    *reinterpret_cast<float4*>(a.v + i) = v;
-    pp = __fmaf_rn(p.x, p.x, pp); pp = __fmaf_rn(p.y, p.y, pp);
-    pp = __fmaf_rn(p.z, p.z, pp); pp = __fmaf_rn(p.w, p.w, pp);
-    uu = __fmaf_rn(u.x, u.x, uu); uu = __fmaf_rn(u.y, u.y, uu);
-    uu = __fmaf_rn(u.z, u.z, uu); uu = __fmaf_rn(u.w, u.w, uu);
-  }
-  pp = warp_sum(pp);
-  uu = warp_sum(uu);
-  const int lane = t & 31, wid = t >> 5;
-  if (lane == 0) {
-    red_p[wid] = pp;
-    red_u[wid] = uu;
-  }
-  __syncthreads();
-  if (t == 0) {
-    float sp_ = 0.0f, su = 0.0f;
-#pragma unroll
-    for (int w = 0; w < kLambThreads / 32; ++w) {
-      sp_ += red_p[w];
-      su += red_u[w];
-    }
-    a.partial[blockIdx.x] = make_float2(sp_, su);
-  }
-}
-
-// One CTA per tensor: deterministic fp64 sum of its chunk partials, then
-// step_scale[t] = lr * trust_t and trust[t].
-__global__ void __launch_bounds__(256) k_lamb_trust(const float2* __restrict__ partial,
-                                                    const int2* __restrict__ tchunks,
-                                                    const float* __restrict__ hp,
-                                                    float* __restrict__ trust,
-                                                    float* __restrict__ step_scale) {
-  __shared__ double sp_[256], su[256];
-  const int2 r = tchunks[blockIdx.x];
-  double a = 0.0, b = 0.0;
-  for (int c = r.x + threadIdx.x; c < r.y; c += blockDim.x) {
-    const float2 q = partial[c];
-    a += (double)q.x;
-    b += (double)q.y;
-  }
-  sp_[threadIdx.x] = a;
-  su[threadIdx.x] = b;
-  __syncthreads();
-  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) {
-      sp_[threadIdx.x] += sp_[threadIdx.x + s];
-      su[threadIdx.x] += su[threadIdx.x + s];
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    const double r1 = sqrt(sp_[0]), r2 = sqrt(su[0]);
-    const float tr = (r1 > 0.0 && r2 > 0.0) ? (float)(r1 / r2) : 1.0f;
-    trust[blockIdx.x] = tr;
-    step_scale[blockIdx.x] = __fmul_rn(hp[0], tr);
-  }
-}
-
-// ------------------------------------------------------------ fused LAMB
-// One persistent kernel for K3 + trust + K4. Work items (chunk, pass) are
-// handed out in a host-built order through an atomic counter: all pass-1
-// chunks in tensor order, with the pass-2 chunks of tensor t inserted `lag`
-// items after t's last pass-1 chunk, so pass 2 re-reads p/m/v while they are
-// still L2-resident. The CTA finishing the last pass-1 chunk of a tensor
-// reduces its chunk partials (fixed order, fp64) into trust[t] and releases
-// a ready flag that the tensor's pass-2 CTAs acquire. Items are taken in
-// list order and a pass-2 item only waits on earlier pass-1 items, so the
-// queue cannot deadlock; the last CTA to exit resets the counters for the
-// next launch (CUDA-graph replay safe).
-
-struct FusedLamb {
-  const int* items;        // >= 0: pass-1 chunk, < 0: ~chunk for pass 2
-  int nitems;
-  int* work;               // next item
-  int* exited;             // CTAs done
-  int* done;               // per tensor: pass-1 chunks finished
-  unsigned int* ready;     // per tensor: trust available
-  const int2* tchunks;     // per tensor [first, last) chunk
-  float* trust;
-  int ntensors;
-  int final_launch;        // last LAMB launch of the round: clears the trust flags
-};
-
-template <int W>
-__device__ __forceinline__ void lamb_p1_vec(const LambArgs& a, const LambScalars& s, int64_t i,
-                                            float4 g, float4 p, float4 m, float4 v, float& pp,
-                                            float& uu) {
-  float4 u;
-  lamb_moments(a, s, g.x, p.x, m.x, v.x, u.x);
-  lamb_moments(a, s, g.y, p.y, m.y, v.y, u.y);
-  lamb_moments(a, s, g.z, p.z, m.z, v.z, u.z);
-  lamb_moments(a, s, g.w, p.w, m.w, v.w, u.w);
-  if (a.l2_hints) {
-    const uint64_t keep = policy_evict_last();
-    st_hint_f4(a.m + i, m, keep);
-    st_hint_f4(a.v + i, v, keep);
-  } else {
-    *reinterpret_cast<float4*>(a.m + i) = m;
-    *reinterpret_cast<float4*>(a.v + i) = v;
-  }
-  pp = __fmaf_rn(p.x, p.x, pp); pp = __fmaf_rn(p.y, p.y, pp);
-  pp = __fmaf_rn(p.z, p.z, pp); pp = __fmaf_rn(p.w, p.w, pp);
-  uu = __fmaf_rn(u.x, u.x, uu); uu = __fmaf_rn(u.y, u.y, uu);
-  uu = __fmaf_rn(u.z, u.z, uu); uu = __fmaf_rn(u.w, u.w, uu);
-}
-
-template <int W>
-__device__ __forceinline__ void lamb_pass1(const LambArgs& a, const LambScalars& s, const Chunk& c,
-                                           float& pp, float& uu) {
-  const ChunkSplit sp = split_chunk(c);
-  const int t = threadIdx.x;
-  int64_t si = -1;
-  if (t < sp.head) si = sp.start + t;
-  else if (t >= 32 && t - 32 < sp.tail) si = sp.start + sp.head + 4 * (int64_t)sp.nbody4 + (t - 32);
-  if (si >= 0) {
-    const float g = load_grad1<W>(a, si);
-    const float p = a.p[si];
-    float m = a.m[si], v = a.v[si], u;
-    lamb_moments(a, s, g, p, m, v, u);
-    a.m[si] = m;
-    a.v[si] = v;
-    pp = __fmaf_rn(p, p, pp);
-    uu = __fmaf_rn(u, u, uu);
-  }
-  const int64_t b0 = sp.start + sp.head;
-  int k = t;
-  // two independent vectors per iteration: all 8 loads issued before use
-  for (; k + kLambThreads < sp.nbody4; k += 2 * kLambThreads) {
-    const int64_t i0 = b0 + 4 * (int64_t)k, i1 = i0 + 4 * (int64_t)kLambThreads;
-    const float4 g0 = load_grad4<W>(a, i0), g1 = load_grad4<W>(a, i1);
-    float4 p0, p1, m0, m1, v0, v1;
-    if (a.l2_hints) {
-      const uint64_t keep = policy_evict_last();
-      p0 = ld_hint_f4(a.p + i0, keep);
-      p1 = ld_hint_f4(a.p + i1, keep);
-      m0 = ld_hint_f4(a.m + i0, keep);
-      m1 = ld_hint_f4(a.m + i1, keep);
-      v0 = ld_hint_f4(a.v + i0, keep);
-      v1 = ld_hint_f4(a.v + i1, keep);
-    } else {
-      p0 = *reinterpret_cast<const float4*>(a.p + i0);
-      p1 = *reinterpret_cast<const float4*>(a.p + i1);
-      m0 = *reinterpret_cast<const float4*>(a.m + i0);
-      m1 = *reinterpret_cast<const float4*>(a.m + i1);
-      v0 = *reinterpret_cast<const float4*>(a.v + i0);
-      v1 = *reinterpret_cast<const float4*>(a.v + i1);
-    }
-    lamb_p1_vec<W>(a, s, i0, g0, p0, m0, v0, pp, uu);
-    lamb_p1_vec<W>(a, s, i1, g1, p1, m1, v1, pp, uu);
-  }
-  if (k < sp.nbody4) {
-    const int64_t i = b0 + 4 * (int64_t)k;
-    lamb_p1_vec<W>(a, s, i, load_grad4<W>(a, i), *reinterpret_cast<const float4*>(a.p + i),
-                   *reinterpret_cast<const float4*>(a.m + i),
-                   *reinterpret_cast<const float4*>(a.v + i), pp, uu);
-  }
-}
-
-__device__ __forceinline__ float4 lamb_p2_vec(const LambArgs& a, const LambScalars& s, float neg,
-                                              float4 p, float4 m, float4 v) {
-  p.x = __fmaf_rn(neg, lamb_dir(a, s, p.x, m.x, v.x), p.x);
-  p.y = __fmaf_rn(neg, lamb_dir(a, s, p.y, m.y, v.y), p.y);
-  p.z = __fmaf_rn(neg, lamb_dir(a, s, p.z, m.z, v.z), p.z);
-  p.w = __fmaf_rn(neg, lamb_dir(a, s, p.w, m.w, v.w), p.w);
-  return p;
-}
-
-__device__ __forceinline__ void lamb_pass2(const LambArgs& a, const LambScalars& s, const Chunk& c,
-                                           float neg) {
-  const ChunkSplit sp = split_chunk(c);
-  const int t = threadIdx.x;
-  int64_t si = -1;
-  if (t < sp.head) si = sp.start + t;
-  else if (t >= 32 && t - 32 < sp.tail) si = sp.start + sp.head + 4 * (int64_t)sp.nbody4 + (t - 32);
-  if (si >= 0) {
-    const float p = a.p[si];
-    a.p[si] = __fmaf_rn(neg, lamb_dir(a, s, p, a.m[si], a.v[si]), p);
-  }
-  const int64_t b0 = sp.start + sp.head;
-  int k = t;
-  for (; k + kLambThreads < sp.nbody4; k += 2 * kLambThreads) {
-    const int64_t i0 = b0 + 4 * (int64_t)k, i1 = i0 + 4 * (int64_t)kLambThreads;
-    if (a.l2_hints) {  // last use of m/v this step: let them go first
-      const uint64_t drop = policy_evict_first();
-      const float4 p0 = ld_hint_f4(a.p + i0, drop), p1 = ld_hint_f4(a.p + i1, drop);
-      const float4 m0 = ld_hint_f4(a.m + i0, drop), m1 = ld_hint_f4(a.m + i1, drop);
-      const float4 v0 = ld_hint_f4(a.v + i0, drop), v1 = ld_hint_f4(a.v + i1, drop);
-      st_hint_f4(a.p + i0, lamb_p2_vec(a, s, neg, p0, m0, v0), drop);
-      st_hint_f4(a.p + i1, lamb_p2_vec(a, s, neg, p1, m1, v1), drop);
-      continue;
-    }
-    const float4 p0 = *reinterpret_cast<const float4*>(a.p + i0);
-    const float4 p1 = *reinterpret_cast<const float4*>(a.p + i1);
-    const float4 m0 = *reinterpret_cast<const float4*>(a.m + i0);
-    const float4 m1 = *reinterpret_cast<const float4*>(a.m + i1);
-    const float4 v0 = *reinterpret_cast<const float4*>(a.v + i0);
-    const float4 v1 = *reinterpret_cast<const float4*>(a.v + i1);
-    *reinterpret_cast<float4*>(a.p + i0) = lamb_p2_vec(a, s, neg, p0, m0, v0);
-    *reinterpret_cast<float4*>(a.p + i1) = lamb_p2_vec(a, s, neg, p1, m1, v1);
-  }
-  if (k < sp.nbody4) {
-    const int64_t i = b0 + 4 * (int64_t)k;
-    *reinterpret_cast<float4*>(a.p + i) =
-        lamb_p2_vec(a, s, neg, *reinterpret_cast<const float4*>(a.p + i),
-                    *reinterpret_cast<const float4*>(a.m + i), *reinterpret_cast<const float4*>(a.v + i));
-  }
 }
 
 __device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
@@ -1089,529 +853,9 @@ __device__ __forceinline__ void st_release_gpu(unsigned int* p, unsigned int v) 
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-#ifndef SP_LAMB_MIN_CTAS
-#define SP_LAMB_MIN_CTAS 1
-#endif
-template <int W>
-__global__ void __launch_bounds__(kLambThreads, SP_LAMB_MIN_CTAS) k_lamb_fused(LambArgs a, FusedLamb f) {
-  __shared__ int s_item;
-  __shared__ int s_last;
-  __shared__ float s_scale;
-  __shared__ float red_p[kLambThreads / 32], red_u[kLambThreads / 32];
-  __shared__ double dred_p[kLambThreads], dred_u[kLambThreads];
-  const LambScalars s{a.hp[0], a.hp[1], a.hp[2]};
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  int next = 0;
-  if (tid == 0) next = atomicAdd(f.work, 1);
-  for (;;) {
-    if (tid == 0) s_item = next;
-    __syncthreads();
-    const int it = s_item;
-    __syncthreads();
-    if (it >= f.nitems) break;
-    if (tid == 0) next = atomicAdd(f.work, 1);  // in flight while this item runs
-    const int code = f.items[it];
-    if (code >= 0) {
-      const Chunk c = a.chunks[code];
-      float pp = 0.0f, uu = 0.0f;
-      lamb_pass1<W>(a, s, c, pp, uu);
-      pp = warp_sum(pp);
-      uu = warp_sum(uu);
-      if (lane == 0) {
-        red_p[wid] = pp;
-        red_u[wid] = uu;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        float sp_ = 0.0f, su = 0.0f;
-#pragma unroll
-        for (int w = 0; w < kLambThreads / 32; ++w) {
-          sp_ += red_p[w];
-          su += red_u[w];
-        }
-        a.partial[code] = make_float2(sp_, su);
-        __threadfence();
-        const int2 r = f.tchunks[c.tensor];
-        s_last = atomicAdd(f.done + c.tensor, 1) == r.y - r.x - 1;
-      }
-      __syncthreads();
-      if (s_last) {  // every pass-1 chunk of this tensor has published its partial
-        __threadfence();
-        const int2 r = f.tchunks[c.tensor];
-        double dp = 0.0, du = 0.0;
-        for (int q = r.x + tid; q < r.y; q += kLambThreads) {
-          const float2 v = __ldcg(a.partial + q);
-          dp += (double)v.x;
-          du += (double)v.y;
-        }
-        dred_p[tid] = dp;
-        dred_u[tid] = du;
-        __syncthreads();
-        for (int h = kLambThreads / 2; h > 0; h >>= 1) {
-          if (tid < h) {
-            dred_p[tid] += dred_p[tid + h];
-            dred_u[tid] += dred_u[tid + h];
-          }
-          __syncthreads();
-        }
-        if (tid == 0) {
-          const double r1 = sqrt(dred_p[0]), r2 = sqrt(dred_u[0]);
-          const float tr = (r1 > 0.0 && r2 > 0.0) ? (float)(r1 / r2) : 1.0f;
-          f.trust[c.tensor] = tr;
-          const_cast<float*>(a.step_scale)[c.tensor] = __fmul_rn(s.lr, tr);
-          f.done[c.tensor] = 0;
-          __threadfence();
-          st_release_gpu(f.ready + c.tensor, 1u);
-        }
-      }
-    } else {
-      const Chunk c = a.chunks[~code];
-      if (tid == 0) {
-        while (ld_acquire_gpu(f.ready + c.tensor) == 0u) __nanosleep(64);
-        s_scale = __ldcg(a.step_scale + c.tensor);
-      }
-      __syncthreads();
-      lamb_pass2(a, s, c, -s_scale);
-    }
-  }
-  if (tid == 0) {
-    __threadfence();
-    if (atomicAdd(f.exited, 1) == (int)gridDim.x - 1) {  // last CTA out resets the queue
-      if (f.final_launch)
-        for (int t = 0; t < f.ntensors; ++t) f.ready[t] = 0u;
-      *f.work = 0;
-      *f.exited = 0;
-      __threadfence();
-    }
-  }
-}
-
-template <int W>
-__global__ void __launch_bounds__(kLambThreads) k_lamb_update(LambArgs a) {
-  const Chunk c = a.chunks[blockIdx.x];
-  const LambScalars s{a.hp[0], a.hp[1], a.hp[2]};
-  const float neg = -a.step_scale[c.tensor];
-  const ChunkSplit sp = split_chunk(c);
-  const int t = threadIdx.x;
-  int64_t si = -1;
-  if (t < sp.head) si = sp.start + t;
-  else if (t >= 32 && t - 32 < sp.tail) si = sp.start + sp.head + 4 * (int64_t)sp.nbody4 + (t - 32);
-  if (si >= 0) {
-    const float p = a.p[si];
-    a.p[si] = __fmaf_rn(neg, lamb_dir(a, s, p, a.m[si], a.v[si]), p);
-  }
-  const int64_t b0 = sp.start + sp.head;
-  for (int k = t; k < sp.nbody4; k += kLambThreads) {
-    const int64_t i = b0 + 4 * (int64_t)k;
-    float4 p = *reinterpret_cast<const float4*>(a.p + i);
-    const float4 m = *reinterpret_cast<const float4*>(a.m + i);
-    const float4 v = *reinterpret_cast<const float4*>(a.v + i);
-    p.x = __fmaf_rn(neg, lamb_dir(a, s, p.x, m.x, v.x), p.x);
-    p.y = __fmaf_rn(neg, lamb_dir(a, s, p.y, m.y, v.y), p.y);
-    p.z = __fmaf_rn(neg, lamb_dir(a, s, p.z, m.z, v.z), p.z);
-    p.w = __fmaf_rn(neg, lamb_dir(a, s, p.w, m.w, v.w), p.w);
-    *reinterpret_cast<float4*>(a.p + i) = p;
-  }
-}
-
-// ------------------------------------------------------ sharded LAMB (N1)
-// ZeRO-1 style step: the owner of [lo, hi) runs pass 1
-// (k_lamb_moments) on its range only. Per tensor it sums its chunk partials
-// in fp64 (chunk order) and stores the pair into slot [rank][t] of every
-// rank's norm table; after a barrier every rank adds the world slots in rank
-// order, so all ranks hold identical trust ratios; pass 2 updates the owned
-// range and stores p' into every rank's parameter vector over NVLink.
-
-struct ShardNormArgs {
-  const float2* partial;
-  const int2* tchunks;             // this rank's chunks of tensor t (may be empty)
-  double2* table[SP_MAX_RANKS];    // push order: next rank first, self last
-  int ndst, rank, T;
-  int t0;                          // first sharded tensor (CTA b handles t0 + b)
-};
-
-__global__ void __launch_bounds__(256) k_shard_norms(ShardNormArgs a) {
-  __shared__ double sx[256], sy[256];
-  const int t = a.t0 + blockIdx.x;
-  const int2 r = a.tchunks[t];
-  double x = 0.0, y = 0.0;
-  for (int c = r.x + threadIdx.x; c < r.y; c += blockDim.x) {
-    const float2 q = a.partial[c];
-    x += (double)q.x;
-    y += (double)q.y;
-  }
-  sx[threadIdx.x] = x;
-  sy[threadIdx.x] = y;
-  __syncthreads();
-  for (int h = blockDim.x / 2; h > 0; h >>= 1) {
-    if (threadIdx.x < h) {
-      sx[threadIdx.x] += sx[threadIdx.x + h];
-      sy[threadIdx.x] += sy[threadIdx.x + h];
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x < a.ndst) a.table[threadIdx.x][(size_t)a.rank * a.T + t] = make_double2(sx[0], sy[0]);
-}
-
-// k_lamb_moments with k_shard_norms folded in (the default sharded chain
-// when every tensor is sharded): the CTA finishing a tensor's last owned
-// chunk sums the chunk partials in fp64 in k_shard_norms' order and stores
-// the pair into slot [rank][t] of every rank's table. Tensors this rank has
-// no chunk of get a zero pair. `nchunks` may be 0 (grid 1: zeros only).
-template <int W>
-__global__ void __launch_bounds__(kLambThreads) k_lamb_moments_shard(LambArgs a, ShardNormArgs na,
-                                                                    int* __restrict__ done,
-                                                                    int nchunks) {
-  __shared__ float red_p[kLambThreads / 32], red_u[kLambThreads / 32];
-  __shared__ double dred_p[kLambThreads], dred_u[kLambThreads];
-  __shared__ int s_last;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  for (int t = na.t0 + blockIdx.x; t < na.T; t += gridDim.x) {
-    const int2 r = na.tchunks[t];
-    if (r.y <= r.x && tid < na.ndst) na.table[tid][(size_t)na.rank * na.T + t] = make_double2(0.0, 0.0);
-  }
-  const LambScalars s{a.hp[0], a.hp[1], a.hp[2]};
-  // grid-stride over the owned chunks (a grid of one resident wave)
-  for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x) {
-    const Chunk c = a.chunks[ci];
-    float pp = 0.0f, uu = 0.0f;
-    lamb_pass1<W>(a, s, c, pp, uu);
-    pp = warp_sum(pp);
-    uu = warp_sum(uu);
-    if (lane == 0) {
-      red_p[wid] = pp;
-      red_u[wid] = uu;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      float sp_ = 0.0f, su = 0.0f;
-#pragma unroll
-      for (int w = 0; w < kLambThreads / 32; ++w) {
-        sp_ += red_p[w];
-        su += red_u[w];
-      }
-      a.partial[ci] = make_float2(sp_, su);
-      __threadfence();
-      const int2 r = na.tchunks[c.tensor];
-      s_last = atomicAdd(done + c.tensor, 1) == r.y - r.x - 1;
-    }
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      const int2 r = na.tchunks[c.tensor];
-      double x = 0.0, y = 0.0;
-      for (int q = r.x + tid; q < r.y; q += kLambThreads) {
-        const float2 v = __ldcg(a.partial + q);
-        x += (double)v.x;
-        y += (double)v.y;
-      }
-      dred_p[tid] = x;
-      dred_u[tid] = y;
-      __syncthreads();
-      for (int h = kLambThreads / 2; h > 0; h >>= 1) {
-        if (tid < h) {
-          dred_p[tid] += dred_p[tid + h];
-          dred_u[tid] += dred_u[tid + h];
-        }
-        __syncthreads();
-      }
-      if (tid < na.ndst)
-        na.table[tid][(size_t)na.rank * na.T + c.tensor] = make_double2(dred_p[0], dred_u[0]);
-      if (tid == 0) done[c.tensor] = 0;
-    }
-    __syncthreads();  // red_p / s_last reused by the next chunk
-  }
-}
-
-__device__ __forceinline__ float trust_from_table(const double2* __restrict__ table, int world, int T,
-                                                  int t) {
-  double x = 0.0, y = 0.0;
-  for (int k = 0; k < world; ++k) {
-    const double2 v = __ldcg(table + (size_t)k * T + t);
-    x += v.x;
-    y += v.y;
-  }
-  const double r1 = sqrt(x), r2 = sqrt(y);
-  return (r1 > 0.0 && r2 > 0.0) ? (float)(r1 / r2) : 1.0f;
-}
-
-// trust[t] = sqrt(sum_k pp[k][t]) / sqrt(sum_k uu[k][t]) over ranks in order
-// (1 if either is 0); step_scale[t] = lr * trust[t].
-__global__ void k_shard_trust(const double2* __restrict__ table, int world, int T, int t0,
-                              const float* __restrict__ hp, float* __restrict__ trust,
-                              float* __restrict__ step_scale) {
-  for (int t = t0 + blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
-    double x = 0.0, y = 0.0;
-    for (int k = 0; k < world; ++k) {
-      const double2 v = __ldcg(table + (size_t)k * T + t);
-      x += v.x;
-      y += v.y;
-    }
-    const double r1 = sqrt(x), r2 = sqrt(y);
-    const float tr = (r1 > 0.0 && r2 > 0.0) ? (float)(r1 / r2) : 1.0f;
-    trust[t] = tr;
-    step_scale[t] = __fmul_rn(hp[0], tr);
-  }
-}
-
 struct ParamPush {
   float* dst[SP_MAX_RANKS];  // every rank's parameter vector, next rank first, self last
   int ndst;
 };
-
-// Pass 2 of the owned chunks: p' = p - lr*trust*u, stored into every rank's
-// copy (the local one last, so the local read of p precedes the local write).
-__device__ __forceinline__ void lamb_push_chunk(const LambArgs& a, const LambScalars& s, const Chunk& c,
-                                                float neg, const ParamPush& d) {
-  const ChunkSplit sp = split_chunk(c);
-  const int t = threadIdx.x;
-  int64_t si = -1;
-  if (t < sp.head) si = sp.start + t;
-  else if (t >= 32 && t - 32 < sp.tail) si = sp.start + sp.head + 4 * (int64_t)sp.nbody4 + (t - 32);
-  if (si >= 0) {
-    const float p = a.p[si];
-    const float q = __fmaf_rn(neg, lamb_dir(a, s, p, a.m[si], a.v[si]), p);
-    for (int k = 0; k < d.ndst; ++k) d.dst[k][si] = q;
-  }
-  const int64_t b0 = sp.start + sp.head;
-  int k = t;
-  // two vectors per iteration: all loads in flight before the stores
-  for (; k + kLambThreads < sp.nbody4; k += 2 * kLambThreads) {
-    const int64_t i0 = b0 + 4 * (int64_t)k, i1 = i0 + 4 * (int64_t)kLambThreads;
-    const float4 p0 = *reinterpret_cast<const float4*>(a.p + i0);
-    const float4 p1 = *reinterpret_cast<const float4*>(a.p + i1);
-    const float4 m0 = *reinterpret_cast<const float4*>(a.m + i0);
-    const float4 m1 = *reinterpret_cast<const float4*>(a.m + i1);
-    const float4 v0 = *reinterpret_cast<const float4*>(a.v + i0);
-    const float4 v1 = *reinterpret_cast<const float4*>(a.v + i1);
-    const float4 q0 = lamb_p2_vec(a, s, neg, p0, m0, v0), q1 = lamb_p2_vec(a, s, neg, p1, m1, v1);
-    const int4 o0 = make_int4(__float_as_int(q0.x), __float_as_int(q0.y), __float_as_int(q0.z),
-                              __float_as_int(q0.w));
-    const int4 o1 = make_int4(__float_as_int(q1.x), __float_as_int(q1.y), __float_as_int(q1.z),
-                              __float_as_int(q1.w));
-    for (int q = 0; q < d.ndst; ++q) {
-      st_v4(d.dst[q] + i0, o0);
-      st_v4(d.dst[q] + i1, o1);
-    }
-  }
-  if (k < sp.nbody4) {
-    const int64_t i = b0 + 4 * (int64_t)k;
-    const float4 q = lamb_p2_vec(a, s, neg, *reinterpret_cast<const float4*>(a.p + i),
-                                 *reinterpret_cast<const float4*>(a.m + i),
-                                 *reinterpret_cast<const float4*>(a.v + i));
-    const int4 o = make_int4(__float_as_int(q.x), __float_as_int(q.y), __float_as_int(q.z),
-                             __float_as_int(q.w));
-    for (int j = 0; j < d.ndst; ++j) st_v4(d.dst[j] + i, o);
-  }
-}
-
-template <int W>
-__global__ void __launch_bounds__(kLambThreads) k_lamb_update_push(LambArgs a, ParamPush d) {
-  const Chunk c = a.chunks[blockIdx.x];
-  const LambScalars s{a.hp[0], a.hp[1], a.hp[2]};
-  lamb_push_chunk(a, s, c, -__ldcg(a.step_scale + c.tensor), d);
-}
-
-// k_lamb_update_push with k_shard_trust folded in: every CTA forms its
-// tensor's trust ratio from the norm table (k_shard_trust's arithmetic), and
-// CTAs b, b + grid, ... also write trust / step_scale of tensor b (what
-// read_trust() returns). `nchunks` may be 0 (grid 1: trust only).
-template <int W>
-__global__ void __launch_bounds__(kLambThreads) k_lamb_update_push_trust(
-    LambArgs a, ParamPush d, const double2* __restrict__ table, int world, int T, int t0,
-    float* __restrict__ trust, float* __restrict__ step_scale, int nchunks) {
-  __shared__ float s_neg;
-  const LambScalars s{a.hp[0], a.hp[1], a.hp[2]};
-  if (threadIdx.x == 0) {
-    for (int t = t0 + blockIdx.x; t < T; t += gridDim.x) {
-      const float tr = trust_from_table(table, world, T, t);
-      trust[t] = tr;
-      step_scale[t] = __fmul_rn(s.lr, tr);
-    }
-  }
-  for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x) {  // grid-stride over owned chunks
-    const Chunk c = a.chunks[ci];
-    if (threadIdx.x == 0) s_neg = -__fmul_rn(s.lr, trust_from_table(table, world, T, c.tensor));
-    __syncthreads();
-    lamb_push_chunk(a, s, c, s_neg, d);
-    __syncthreads();
-  }
-}
-
-// ------------------------------------------- sharded LAMB, one kernel (N1)
-// The chain above (pass 1 -> norms -> barrier -> trust -> pass 2 + push)
-// as one persistent kernel over a work queue of this rank's chunks:
-//   pass-1 item: moments + chunk partial; the CTA finishing the tensor's
-//     last chunk sums the partials in fp64 (k_shard_norms' order), stores the
-//     pair into slot [rank][t] of every rank's norm table and release-stores
-//     the round's epoch into flag [rank][t] of every rank;
-//   pass-2 item: waits for the world flags of its tensor, forms the trust
-//     ratio from the world slots in rank order (k_shard_trust's arithmetic),
-//     updates the chunk and stores p' into every rank's parameter vector.
-// Pass-2 items of tensor t are queued `lag` items after its last pass-1
-// item, so the NVLink push of early tensors can overlap the HBM-bound pass 1
-// of later ones. Measured (4x B200, profiles/r01/shard_fused.txt): no faster
-// than the chain at 268M elements and 1.4-2.5x slower at ALBERT-large size
-// (pass-2 items wait on the slowest chunk of their tensor on every rank, and
-// the push needs every CTA to keep NVLink busy), so it is opt-in
-// (SP_SHARD_FUSED=1) and kept bit-exact by the tests. Items only wait on earlier items of this rank's queue and
-// on other GPUs' pass 1, which progresses independently: no deadlock. The
-// last CTA out waits for every flag, writes trust / step_scale for all
-// tensors (what read_trust() returns) and resets the queue; flags carry
-// the epoch, so nothing needs clearing between graph replays.
-struct ShardFused {
-  const int* items;                         // >= 0 pass-1 chunk, < 0 ~chunk (pass 2 + push)
-  int nitems;
-  int* work;
-  int* exited;
-  int* done;                                // per tensor: pass-1 chunks finished
-  const int2* tchunks;                      // this rank's chunks of tensor t
-  double2* table[SP_MAX_RANKS];             // norm table of rank (rank + 1 + k) % world
-  unsigned long long* flags[SP_MAX_RANKS];  // norm flags of the same ranks
-  const double2* my_table;                  // [world][T]
-  const unsigned long long* my_flags;       // [world][T]
-  unsigned long long* epoch;                // local round counter
-  float* trust;
-  float* step_scale;
-  ParamPush push;
-  int rank, world, T;
-  int* err;
-  unsigned long long timeout_ns;
-};
-
-__device__ __forceinline__ bool wait_norms(const ShardFused& f, int t, unsigned long long e) {
-  const unsigned long long t0 = globaltimer();
-  for (int k = 0; k < f.world; ++k)
-    while (ld_acquire_sys(f.my_flags + (size_t)k * f.T + t) < e) {
-      if (globaltimer() - t0 > f.timeout_ns) {
-        atomicExch_system(f.err, 1);
-        return false;
-      }
-      __nanosleep(256);  // hundreds of CTAs may poll: keep them off the memory system
-    }
-  return true;
-}
-
-__device__ __forceinline__ float shard_trust(const ShardFused& f, int t) {
-  double x = 0.0, y = 0.0;
-  for (int k = 0; k < f.world; ++k) {
-    const double2 v = __ldcg(f.my_table + (size_t)k * f.T + t);
-    x += v.x;
-    y += v.y;
-  }
-  const double r1 = sqrt(x), r2 = sqrt(y);
-  return (r1 > 0.0 && r2 > 0.0) ? (float)(r1 / r2) : 1.0f;
-}
-
-// thread 0..world-1 store the pair, then thread 0 publishes the epoch
-__device__ __forceinline__ void publish_norms(const ShardFused& f, int t, double x, double y,
-                                              unsigned long long e) {
-  if (threadIdx.x < f.world) {
-    f.table[threadIdx.x][(size_t)f.rank * f.T + t] = make_double2(x, y);
-    __threadfence_system();
-  }
-  __syncthreads();
-  if (threadIdx.x < f.world) st_release_sys(f.flags[threadIdx.x] + (size_t)f.rank * f.T + t, e);
-}
-
-template <int W>
-__global__ void __launch_bounds__(kLambThreads, 4) k_shard_lamb_fused(LambArgs a,
-                                                                                     ShardFused f) {
-  __shared__ int s_item, s_last;
-  __shared__ float s_neg;
-  __shared__ unsigned long long s_epoch;
-  __shared__ float red_p[kLambThreads / 32], red_u[kLambThreads / 32];
-  __shared__ double dred_p[kLambThreads], dred_u[kLambThreads];
-  const LambScalars s{a.hp[0], a.hp[1], a.hp[2]};
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (tid == 0) s_epoch = *f.epoch + 1;
-  __syncthreads();
-  const unsigned long long e = s_epoch;
-  // tensors with no chunk on this rank contribute a zero pair
-  for (int t = blockIdx.x; t < f.T; t += gridDim.x) {
-    const int2 r = f.tchunks[t];
-    if (r.y <= r.x) publish_norms(f, t, 0.0, 0.0, e);
-    __syncthreads();
-  }
-  int next = 0;
-  if (tid == 0) next = atomicAdd(f.work, 1);
-  for (;;) {
-    if (tid == 0) s_item = next;
-    __syncthreads();
-    const int it = s_item;
-    __syncthreads();
-    if (it >= f.nitems) break;
-    if (tid == 0) next = atomicAdd(f.work, 1);
-    const int code = f.items[it];
-    if (code >= 0) {
-      const Chunk c = a.chunks[code];
-      float pp = 0.0f, uu = 0.0f;
-      lamb_pass1<W>(a, s, c, pp, uu);
-      pp = warp_sum(pp);
-      uu = warp_sum(uu);
-      if (lane == 0) {
-        red_p[wid] = pp;
-        red_u[wid] = uu;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        float sp_ = 0.0f, su = 0.0f;
-#pragma unroll
-        for (int w = 0; w < kLambThreads / 32; ++w) {
-          sp_ += red_p[w];
-          su += red_u[w];
-        }
-        a.partial[code] = make_float2(sp_, su);
-        __threadfence();
-        const int2 r = f.tchunks[c.tensor];
-        s_last = atomicAdd(f.done + c.tensor, 1) == r.y - r.x - 1;
-      }
-      __syncthreads();
-      if (s_last) {  // this rank's partials of the tensor are all in
-        __threadfence();
-        const int2 r = f.tchunks[c.tensor];
-        double dp = 0.0, du = 0.0;
-        for (int q = r.x + tid; q < r.y; q += kLambThreads) {
-          const float2 v = __ldcg(a.partial + q);
-          dp += (double)v.x;
-          du += (double)v.y;
-        }
-        dred_p[tid] = dp;
-        dred_u[tid] = du;
-        __syncthreads();
-        for (int h = kLambThreads / 2; h > 0; h >>= 1) {
-          if (tid < h) {
-            dred_p[tid] += dred_p[tid + h];
-            dred_u[tid] += dred_u[tid + h];
-          }
-          __syncthreads();
-        }
-        if (tid == 0) f.done[c.tensor] = 0;
-        publish_norms(f, c.tensor, dred_p[0], dred_u[0], e);
-      }
-    } else {
-      const Chunk c = a.chunks[~code];
-      if (tid == 0) {
-        s_neg = wait_norms(f, c.tensor, e) ? -__fmul_rn(s.lr, shard_trust(f, c.tensor)) : 0.0f;
-      }
-      __syncthreads();
-      lamb_push_chunk(a, s, c, s_neg, f.push);
-    }
-  }
-  if (tid == 0) {
-    __threadfence();
-    if (atomicAdd(f.exited, 1) == (int)gridDim.x - 1) {  // last CTA out
-      for (int t = 0; t < f.T; ++t) {
-        const float tr = wait_norms(f, t, e) ? shard_trust(f, t) : 1.0f;
-        f.trust[t] = tr;
-        f.step_scale[t] = __fmul_rn(s.lr, tr);
-      }
-      *f.work = 0;
-      *f.exited = 0;
-      *f.epoch = e;
-      __threadfence();
-    }
-  }
-}
 
 }  // namespace sp

@@ -39,6 +39,7 @@ AveragingRound::AveragingRound(const RoundConfig& cfg) : cfg_(cfg) {
   c.weight_decay = cfg_.weight_decay;
   c.bias_correction = cfg_.bias_correction ? 1 : 0;
   c.barrier_timeout_s = cfg_.barrier_timeout_s;
+  c.shard_lamb = cfg_.shard_lamb ? 1 : 0;
   check_status(sp_round_create(&c, &h_));
 }
 
@@ -87,8 +88,14 @@ void AveragingRound::run(const float* const* grads, float* p, float* m, float* v
 }
 
 void AveragingRound::run_host(const float* const* host_grads, float* p, float* m, float* v, int step,
-                              void* stream) {
-  check_status(sp_round_run_host(h_, host_grads, p, m, v, step, stream));
+                              void* stream, float* host_p_out) {
+  check_status(sp_round_run_host_params(h_, host_grads, p, m, v, step, host_p_out, stream));
+}
+
+float* AveragingRound::param_buffer() const {
+  float* p = sp_round_param_ptr(h_);
+  if (!p) throw std::invalid_argument("param_buffer: the round was created without shard_lamb");
+  return p;
 }
 
 sp_phase_times AveragingRound::run_phased(const float* const* grads, float* p, float* m, float* v,

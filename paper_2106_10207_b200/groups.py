@@ -13,9 +13,11 @@ from paper_2106_10207_b200 import _swarmplan
 
 
 def run_plan_gpu(n: int, m: int, values: torch.Tensor, weights=(), failures=(),
-                 out: torch.Tensor | None = None) -> dict:
+                 out: torch.Tensor | None = None, exact: bool = False) -> dict:
     """values: (n, dim) float64 CUDA tensor, one row per peer. Returns
-    run_plan's dict with "values" an (n, dim) float64 CUDA tensor."""
+    run_plan's dict with "values" an (n, dim) float64 CUDA tensor. The
+    default merge rule is the reference's (groups.cpp:126-151);
+    exact=True is SPEC.md:240-241's (see groups::MergeRule)."""
     if values.dim() != 2 or values.shape[0] != n:
         raise ValueError("values must be (n, dim)")
     if not values.is_cuda or values.dtype != torch.float64:
@@ -29,6 +31,6 @@ def run_plan_gpu(n: int, m: int, values: torch.Tensor, weights=(), failures=(),
         res = _swarmplan.run_plan_device(
             n, m, [values[i].data_ptr() for i in range(n)], dim,
             [out[i].data_ptr() for i in range(n)], [float(w) for w in weights],
-            [tuple(f) for f in failures], stream)
+            [tuple(f) for f in failures], stream, exact)
     res["values"] = out
     return res

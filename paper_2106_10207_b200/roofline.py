@@ -24,24 +24,32 @@ HBM_GBS = 6524.0
 SHARD_PENALTY = 1.1
 
 
-def rank_model(r, offsets, L, world, n, b, wire, shard, fused, fused_pack) -> dict:
-    """Algorithmic bytes per element for rank r given the
-    part fraction f it owns: per-kernel launch bytes (`alg`) and, for each
-    phase of the round (pack+scatter, reduce(+push), LAMB(+parameter push)),
-    the HBM bytes it must move and the NVLink bytes per direction (the larger
-    of out and in). Phases are separated by cross-rank barriers, so the
-    round's roofline is the sum over phases of the slowest rank's
-    max(HBM time, NVLink time)."""
+def rank_model(r, offsets, L, world, n, b, wire, shard, fused_pack) -> dict:
+    """Algorithmic bytes for rank r given the part fraction f
+    it owns.
+
+    `alg`: per-kernel §8(d) bytes of one launch (pack 4 + b per packed
+    element, weighted reduce G f b + f b, LAMB 24 + b per stepped element;
+    one GPU with one peer runs the pack inside LAMB, so k_lamb's launch
+    carries both: 28 + 2b). `impl`: the bytes k_lamb actually moves through
+    L2 per launch: §8(d)'s LAMB bytes plus pass 2's re-read of p (4 B; u
+    comes from the shared-memory stash), and with the fused pack its fp32
+    read and wire store (4 + b) but no wire re-read.
+    `phases`: for each phase of the round (pack+scatter, reduce(+push),
+    LAMB(+parameter push)) the HBM bytes and the NVLink bytes per direction
+    (the larger of out and in), per element of the vector. Phases are
+    separated by cross-rank barriers, so the round's roofline is the sum over
+    phases of the slowest rank's max(HBM time, NVLink time)."""
     G = L * world
     f = (offsets[(r + 1) * L] - offsets[r * L]) / n
     f_l = f if shard else 1.0  # fraction of the vector this rank's LAMB steps
+    pack_alg = 0.0 if (fused_pack or (wire == "fp32" and world == 1)) else L * n * (4 + b)
     alg = {
-        "pack_ms": 0.0 if fused_pack else (L * n * (4 + b)),
-        "reduce_ms": (G + (1 if shard else world)) * f * n * b,
-        # fused kernel: pass 1 reads g,p,m,v writes m,v; pass 2 reads p,m,v writes p
-        "moments_ms": f_l * n * (20 + b + (4 + b if fused_pack else 0.0)) + (n * 16.0 if fused else 0.0),
-        "update_ms": 0.0 if fused else f_l * n * 16.0,
+        "pack_ms": pack_alg,
+        "reduce_ms": (G * f * b + f * b) * n if G > 1 else 0.0,
+        "lamb_ms": f_l * n * (24 + b) + (n * (4 + b) if fused_pack else 0.0),
     }
+    impl = {"lamb_ms": f_l * n * (24 + b + 4) + (n * 4.0 if fused_pack else 0.0)}
     multi = world > 1
     # pack: read the fp32 gradients (4 L), write the wire of the owned range
     # (L f b from local peers, (G - L) f b arriving from the other ranks; the
@@ -64,7 +72,7 @@ def rank_model(r, offsets, L, world, n, b, wire, shard, fused, fused_pack) -> di
     lamb_hbm = f_l * (24 + b) + ((1 - f) * 4.0 if shard and multi else 0.0)
     lamb_nvl = max((world - 1) * f * 4.0, (1 - f) * 4.0) if (shard and multi) else 0.0
     phases = [(pack_hbm, pack_nvl), (red_hbm, red_nvl), (lamb_hbm, lamb_nvl)]
-    return {"f": f, "alg": alg, "phases": phases,
+    return {"f": f, "alg": alg, "impl": impl, "phases": phases,
             "hbm": sum(h for h, _ in phases), "nvl": sum(x for _, x in phases)}
 
 
@@ -98,6 +106,6 @@ def choose_shard_lamb(offsets, L: int, world: int, n: int, b: float, wire: str,
         return False
     t = {}
     for shard in (True, False):
-        ms = [rank_model(r, offsets, L, world, n, b, wire, shard, not shard, False) for r in range(world)]
+        ms = [rank_model(r, offsets, L, world, n, b, wire, shard, False) for r in range(world)]
         t[shard] = overlap_roofline(ms, n, peak)
     return t[True] * SHARD_PENALTY < t[False]

@@ -120,6 +120,17 @@ class AveragingRound:
         return offs
 
     # -- the round ----------------------------------------------------------
+    def _st(self, stream):
+        """cudaStream_t for the C-ABI: the given stream, else torch's current
+        stream on this device, so the round is ordered after the caller's
+        backward pass and before its next forward (the library never picks
+        a stream of its own; include/sp_round.h "Streams")."""
+        if stream is None:
+            import torch
+
+            return torch.cuda.current_stream(self.device).cuda_stream or None
+        return (stream or None) if isinstance(stream, int) else (stream.cuda_stream or None)
+
     def _ptrs(self, grads):
         if len(grads) != self.L:
             raise ValueError(f"expected {self.L} local gradients")
@@ -138,16 +149,18 @@ class AveragingRound:
         return t.data_ptr()
 
     def run(self, grads, p, m, v, step: int, stream=None) -> None:
-        st = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
+        st = self._st(stream)
         nat.check(self._lib.sp_round_run(self._h, self._ptrs(grads), self._dptr(p, self.n),
                                          self._dptr(m, self.n), self._dptr(v, self.n),
                                          int(step), st))
 
-    def run_host(self, host_grads, p, m, v, step: int, stream=None) -> None:
+    def run_host(self, host_grads, p, m, v, step: int, stream=None, p_out=None) -> None:
         """One round from HOST gradients (sp_round_run_host): pinned CPU
         float32 tensors, copied to a double-buffered device staging area on
         the round's copy stream, so this step's copy overlaps the previous
-        round. p, m, v stay device tensors."""
+        round. p, m, v stay device tensors. `p_out` (pinned CPU float32 of n
+        elements) receives the updated parameters, copied after the round on
+        `stream` (sp_round_run_host_params)."""
         import torch
 
         if len(host_grads) != self.L:
@@ -159,13 +172,18 @@ class AveragingRound:
             if g.is_cuda or g.dtype != torch.float32 or not g.is_contiguous() or g.numel() < self.n:
                 raise ValueError("host_grads: contiguous CPU float32 tensors of at least n elements")
             arr[i] = g.data_ptr()
-        st = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
-        nat.check(self._lib.sp_round_run_host(self._h, arr, self._dptr(p, self.n),
-                                              self._dptr(m, self.n), self._dptr(v, self.n),
-                                              int(step), st))
+        out = None
+        if p_out is not None:
+            if (p_out.is_cuda or p_out.dtype != torch.float32 or not p_out.is_contiguous()
+                    or p_out.numel() < self.n):
+                raise ValueError("p_out: contiguous CPU float32 tensor of at least n elements")
+            out = p_out.data_ptr()
+        nat.check(self._lib.sp_round_run_host_params(self._h, arr, self._dptr(p, self.n),
+                                                     self._dptr(m, self.n), self._dptr(v, self.n),
+                                                     int(step), out, self._st(stream)))
 
     def run_phased(self, grads, p, m, v, step: int, stream=None) -> dict:
-        st = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
+        st = self._st(stream)
         t = nat.SpPhaseTimes()
         nat.check(self._lib.sp_round_run_phased(self._h, self._ptrs(grads), self._dptr(p, self.n),
                                                 self._dptr(m, self.n), self._dptr(v, self.n),
@@ -175,7 +193,7 @@ class AveragingRound:
     # -- device-side accumulation (round step 1) ---------------------------
     def accumulate(self, local_peer: int, grad, samples: float, buf: int = 0, stream=None) -> None:
         """acc[buf][local_peer] (+)= grad (fp32, device) and count `samples`."""
-        st = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
+        st = self._st(stream)
         nat.check(self._lib.sp_round_accumulate(self._h, buf, local_peer, self._dptr(grad, self.n),
                                                 float(samples), st))
 
@@ -209,10 +227,9 @@ class AveragingRound:
 
         return torch.as_tensor(_View(), device=f"cuda:{self.device}")
 
-    def shard_cut(self) -> int:
-        """shard_lamb: tensors before this element index keep the replicated
-        LAMB (full m/v on every rank); tensors from it on are sharded."""
-        return int(self._lib.sp_round_shard_cut(self._h))
+    def lamb_windows(self) -> int:
+        """Tensor windows of the LAMB plan (sp_round_lamb_windows)."""
+        return int(self._lib.sp_round_lamb_windows(self._h))
 
     def own_range(self) -> tuple[int, int]:
         """[lo, hi) of the flattened vector this rank owns (averages, and with
@@ -234,7 +251,7 @@ class AveragingRound:
         accumulate into the other buffer on another stream while this round
         runs; order that stream after the round that last read the buffer it
         writes (an event recorded after run_accumulated(..., buf=b))."""
-        st = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
+        st = self._st(stream)
         nat.check(self._lib.sp_round_run_accumulated(self._h, buf, self._dptr(p, self.n),
                                                      self._dptr(m, self.n), self._dptr(v, self.n),
                                                      int(step), st))
@@ -255,7 +272,7 @@ class AveragingRound:
     def copy_trust_async(self, dst_ptr: int, stream=None) -> None:
         """Stream-ordered copy of the per-tensor trust ratios to dst_ptr
         (pinned host or device memory)."""
-        st = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
+        st = self._st(stream)
         nat.check(self._lib.sp_round_copy_trust(self._h, dst_ptr, st))
 
     def read_trust(self):
@@ -294,6 +311,8 @@ class AveragingRound:
 def fill_synthetic(t, seed: int, peer: int, scale: float, outlier_every: int = 997,
                    outlier_mult: float = 100.0, stream=None) -> None:
     """Device twin of oracle sp_oracle_fill_synthetic (bit-identical)."""
-    st = None if stream is None else stream.cuda_stream
+    import torch
+
+    st = (torch.cuda.current_stream(t.device).cuda_stream if stream is None else stream.cuda_stream) or None
     nat.check(nat.lib().sp_fill_synthetic(t.data_ptr(), t.numel(), seed, peer, scale,
                                           outlier_every, outlier_mult, st))

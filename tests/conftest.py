@@ -20,4 +20,7 @@ def _built():
 
     if os.environ.get("SP_SKIP_BUILD") != "1" and os.path.exists(_build.NVCC):
         _build.build_all()
+        from oracle import build_ref
+
+        build_ref.build()  # no-op without /root/reference (the GPU box uses the prebuilt .so)
     yield

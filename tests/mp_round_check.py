@@ -116,26 +116,26 @@ def main():
             rnd.run(grads, p, m, v, step)
         torch.cuda.synchronize()
         got, gs = rnd.read_wire(nat.SP_BUF_AVG)
-        cut = rnd.shard_cut() if args.shard_lamb else n
-        have = np.zeros(n, bool)  # sharded: the average of sharded tensors stays with the owner
-        have[:min(n, -(-cut // rnd.align) * rnd.align)] = True
+        have = np.zeros(n, bool)  # sharded: the average stays with the owner
+        if not args.shard_lamb:
+            have[:] = True
         have[lo:hi] = True
         if not np.array_equal(got[have], avg[have]):
             errors.append(f"step {step}: averaged vector differs ({int((got != avg).sum())} elems)")
         if wire == "q8":
             hs = np.zeros(len(avg_s), bool)
-            hs[:-(-min(n, -(-cut // block) * block) // block)] = True
+            if not args.shard_lamb:
+                hs[:] = True
             hs[lo // block:(hi + block - 1) // block] = True
         if wire == "q8" and not np.array_equal(gs[hs], avg_s[hs]):
             errors.append(f"step {step}: averaged q8 scales differ")
         trust = rnd.read_trust()
         O.lamb(wire, avg, avg_s, ph, mh, vh, sizes, HP, step, block, trust_in=trust)
-        # sharded: m and v are kept on the replicated prefix and the owned
-        # range of the sharded tensors; p everywhere
-        cut = rnd.shard_cut() if args.shard_lamb else n
+        # sharded: m and v are kept on the owned range only; p everywhere
         keep = np.zeros(n, bool)
-        keep[:cut] = True
-        keep[max(lo, cut):hi] = True
+        if not args.shard_lamb:
+            keep[:] = True
+        keep[lo:hi] = True
         for name, dev, host, msk in (("m", m, mh, keep), ("v", v, vh, keep), ("p", p, ph, None)):
             d = dev.cpu().numpy()
             if not (np.array_equal(d, host) if msk is None else np.array_equal(d[msk], host[msk])):

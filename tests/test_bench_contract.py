@@ -32,7 +32,9 @@ def test_reference_arm_line(args):
         assert k in d, k
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    # the reference's own run_plan (oracle/_ref) carries the averaging
+    assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
+    assert set(d["phase_ms"]) == {"pack_ms", "average_ms", "to_wire_ms", "lamb_ms"}
 
 
 def test_sweep_tensor_table():

@@ -34,7 +34,7 @@ def _launch(nproc, *extra, env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", f"--nproc-per-node={nproc}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
            os.path.join(HERE, "mp_round_check.py"), *extra]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300,
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
                        env=None if env is None else {**os.environ, **env})
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert r.returncode == 0 and lines, r.stdout[-2000:] + r.stderr[-3000:]
@@ -66,13 +66,6 @@ def test_owner_takes_everything_q8():
 
 
 @pytest.mark.parametrize("wire", ["fp16", "q8"])
-def test_one_kernel_round(wire):
-    """The opt-in single persistent kernel (pack/scatter, reduce/push, LAMB
-    in one launch with per-cell readiness counters) is bit-exact too."""
-    _launch(NGPU, "--wire", wire, "--peers-per-rank", "2", env={"SP_ROUND_FUSED": "1"})
-
-
-@pytest.mark.parametrize("wire", ["fp16", "q8"])
 def test_device_accumulation_multi_gpu(wire):
     """Micro-batches accumulated on each GPU; sample counts published over
     NVLink weight the average; buffers alternate per step (DPU)."""
@@ -97,21 +90,10 @@ def test_sharded_lamb_ragged_owners():
     _launch(NGPU, "--wire", "q8", "--shard-lamb", "--peers-per-rank", "2", "--accumulate")
 
 
-def test_sharded_lamb_hybrid_split():
-    # opt-in split: replicated LAMB for the leading tensors on a second stream
-    # beside the sharded chain (measured slower; kept bit-exact)
-    _launch(NGPU, "--wire", "fp16", "--shard-lamb", env={"SP_SHARD_FRACTION": "0.5"})
-
-
-@pytest.mark.parametrize("env", [
-    {"SP_SHARD_FUSED": "1", "SP_SHARD_LAG": "0", "SP_LAMB_CHUNK": "1024"},  # many items per tensor, pass 2 interleaved
-    {"SP_SHARD_FUSED": "1", "SP_SHARD_LAG": "37", "SP_LAMB_CHUNK": "2048"},
-    {"SP_SHARD_FUSED": "1"},  # one kernel, default lag
-])
-def test_sharded_lamb_one_kernel_schedules(env):
-    # k_shard_lamb_fused: per-tensor norm flags over NVLink inside one
-    # persistent kernel; every schedule must give the same bits
-    _launch(NGPU, "--wire", "fp16", "--shard-lamb", "--steps", "4", env=env)
+def test_sharded_lamb_many_steps_nonuniform():
+    # several rounds through the cached graph; the in-kernel norm exchange
+    # and the counter resets must hold across replays
+    _launch(NGPU, "--wire", "fp16", "--shard-lamb", "--steps", "4")
     fr = [0.0] * NGPU
     fr[-1], fr[0] = 0.7, 0.3
-    _launch(NGPU, "--wire", "q8", "--shard-lamb", "--fractions", ",".join(map(str, fr)), env=env)
+    _launch(NGPU, "--wire", "q8", "--shard-lamb", "--fractions", ",".join(map(str, fr)))

@@ -19,16 +19,25 @@ def _offsets(fleet, G, n=N, align=8):
 
 def test_one_gpu_bytes_match_survey():
     # G = 1 -> pack 4 + b, LAMB 24 + b, no NVLink
-    m = rank_model(0, [0, N], 1, 1, N, 2.0, "fp16", False, True, True)
+    m = rank_model(0, [0, N], 1, 1, N, 2.0, "fp16", False, True)
     assert m["hbm"] == pytest.approx(6.0 + 26.0)
     assert m["nvl"] == 0.0
-    fp32 = rank_model(0, [0, N], 1, 1, N, 4.0, "fp32", False, True, False)
+    # fused pack + LAMB: one launch carries both §8(d) terms (4 + b + 24 + b);
+    # the kernel moves 4 + b + 24 + 4 (no wire re-read, p re-read in pass 2)
+    assert m["alg"]["lamb_ms"] == pytest.approx(N * 32.0)
+    assert m["alg"]["pack_ms"] == 0.0
+    assert m["impl"]["lamb_ms"] == pytest.approx(N * 34.0)
+    fp32 = rank_model(0, [0, N], 1, 1, N, 4.0, "fp32", False, False)
     assert fp32["hbm"] == pytest.approx(28.0)  # zero-copy wire
+    assert fp32["alg"]["lamb_ms"] == pytest.approx(N * 28.0)
+    q8 = rank_model(0, [0] + [N] * 8, 8, 1, N, 1.0 + 4 / 4096, "q8", False, False)  # 8 virtual peers
+    assert q8["alg"]["pack_ms"] == pytest.approx(8 * N * (5 + 4 / 4096))
+    assert q8["alg"]["reduce_ms"] == pytest.approx(9 * N * (1 + 4 / 4096))
 
 
 def test_uniform_split_bytes():
     offs = _offsets(None, 4)
-    m = rank_model(1, offs, 1, 4, N, 2.0, "fp16", True, False, False)
+    m = rank_model(1, offs, 1, 4, N, 2.0, "fp16", True, False)
     assert m["f"] == pytest.approx(0.25, rel=1e-5)  # offsets aligned to 8 elements
     (ph, pn), (rh, rn), (lh, ln) = m["phases"]
     assert pn == pytest.approx(0.75 * 2.0, rel=1e-5)       # scatter out = in
@@ -42,7 +51,7 @@ def test_overlap_bound_is_below_serialized():
         offs = _offsets(fleet, G)
         L = G // world
         for shard in (True, False):
-            ms = [rank_model(r, offs, L, world, N, 2.0, "fp16", shard, not shard, False)
+            ms = [rank_model(r, offs, L, world, N, 2.0, "fp16", shard, False)
                   for r in range(world)]
             assert overlap_roofline(ms, N, 6524.0) <= round_roofline(ms, N, 6524.0) + 1e-15
 

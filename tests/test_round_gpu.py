@@ -26,6 +26,10 @@ SIGMA = float(np.float32(1e-3 * np.sqrt(3.0)))
 HET8C = [1 / 20] * 6 + [0.0, 7 / 10]
 HET4B = [1 / 22] * 3 + [19 / 22]
 RAGGED = [3, 1000, 70001, 2, 4096, 131075, 5]  # n = 206182, misaligned tensor edges
+# p against the oracle's own LAMB: trust ratios agree to rtol 2e-5 and the
+# LAMB direction is bounded by |m^|/sqrt(v^) + wd |p| <= ~10 here, so one
+# step moves p by at most lr * 10 * 2e-5 more or less than the oracle's
+P_ATOL = HP["lr"] * 10 * 2e-5
 
 
 def _dev(x):
@@ -71,6 +75,9 @@ def _run_case(wire, fractions, weights, sizes, steps=1, block=4096, warm=False, 
             assert np.array_equal(grads_d[g].cpu().numpy(), grads_h[g])
 
     packed = [None if x is None else O.pack(wire, x, block) for x in grads_h]
+    # the oracle's own LAMB (its fp64 trust ratios) alongside the one fed
+    # the device's trust ratios
+    p_own, m_own, v_own = p_h.copy(), m_h.copy(), v_h.copy()
     for step in range(1, steps + 1):
         rnd.run(grads_d, p_d, m_d, v_d, step)
         torch.cuda.synchronize()
@@ -97,6 +104,10 @@ def _run_case(wire, fractions, weights, sizes, steps=1, block=4096, warm=False, 
         np.testing.assert_array_equal(m_d.cpu().numpy(), m_h, err_msg="m")
         np.testing.assert_array_equal(v_d.cpu().numpy(), v_h, err_msg="v")
         np.testing.assert_array_equal(p_d.cpu().numpy(), p_h, err_msg="p")
+        # end to end against the oracle's own trust ratios (P_ATOL per step)
+        O.lamb(wire, avg, avg_s, p_own, m_own, v_own, sizes, HP, step, block)
+        np.testing.assert_allclose(p_d.cpu().numpy(), p_own, rtol=2e-7, atol=P_ATOL * step,
+                                   err_msg="p vs the oracle's own LAMB")
     rnd.close()
 
 
@@ -124,18 +135,6 @@ def test_round_parity_lp_planned(fleet, wire):
     plan = plan_round(spec_json(fleet), n, 4096 if wire == "q8" else 8)
     assert abs(sum(plan["fractions"]) - 1.0) < 1e-9
     _run_case(wire, plan["fractions"], plan["weights"], RAGGED, offsets=plan["offsets"])
-
-
-@pytest.mark.parametrize("env", [{"SP_SHARD_FUSED": "1", "SP_SHARD_LAG": "0", "SP_LAMB_CHUNK": "1024"},
-                                 {"SP_SHARD_FUSED": "1", "SP_SHARD_LAG": "11", "SP_LAMB_CHUNK": "2048"},
-                                 {"SP_SHARD_FUSED": "1"}])
-def test_sharded_lamb_schedules_one_rank(env, monkeypatch):
-    # one-kernel sharded LAMB (k_shard_lamb_fused) with interleaved pass-2
-    # items, and the kernel chain, against the oracle
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
-    _run_case("fp16", [0.25, 0.25, 0.25, 0.25], [5.0, 0.0, 3.0, 8.0], RAGGED, steps=3, warm=True,
-              shard=True)
 
 
 @pytest.mark.parametrize("wire", ["fp32", "fp16", "q8"])
@@ -171,6 +170,34 @@ def test_round_parity_multi_step_warm_state(wire):
 @pytest.mark.parametrize("block", [512, 16384])
 def test_round_parity_q8_block_sizes(block):
     _run_case("q8", [0.3, 0.7], [1.0, 2.0], RAGGED, block=block)
+
+
+@pytest.mark.parametrize("wire,shard", [("fp16", False), ("q8", False), ("fp32", True)])
+def test_lamb_tensor_larger_than_a_window(wire, shard):
+    # a 9.5M-element tensor does not fit half the shared-memory stash (about
+    # 4.3M elements on 148 SMs): it gets a window of its own, part of its
+    # chunks stashed and the rest recomputed from p, m', v' in pass 2;
+    # sharded on one rank: one window of 9.58M elements over the whole stash
+    sizes = [3, 9_500_001, 70001, 5]
+    _run_case(wire, [0.5, 0.5], [1.0, 3.0], sizes, steps=2, warm=True, shard=shard)
+
+
+def test_lamb_plan_windows():
+    import json
+    import os
+
+    tables = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "tensor_tables.json")))
+    al = tables["albert-large"]
+    rnd = AveragingRound(sum(al), al, wire="fp16")
+    rnd.assign([1.0], [1.0])
+    # 17.8M elements in windows of <= ~4.3M whole tensors (the 4,194,304
+    # FFN matrices alone fill one)
+    assert 5 <= rnd.lamb_windows() <= 8
+    rnd.close()
+    rnd = AveragingRound(sum(al), al, wire="fp16", shard_lamb=True)
+    rnd.assign([1.0], [1.0])
+    assert rnd.lamb_windows() == 1
+    rnd.close()
 
 
 def test_round_parity_albert_large_fp16_g8():
@@ -218,19 +245,6 @@ def test_bad_arguments_raise():
     with pytest.raises(RuntimeError):
         rnd.run([p, p], p, p, p, 1)  # before set_assignment
     rnd.close()
-
-
-@pytest.mark.parametrize("wire", ["fp32", "fp16", "q8"])
-def test_one_kernel_round_parity(wire, monkeypatch):
-    """Opt-in single persistent round kernel (sp_round_fused.cuh)."""
-    monkeypatch.setenv("SP_ROUND_FUSED", "1")
-    _run_case(wire, HET8C, [1.0] * 8, RAGGED, steps=2)
-
-
-def test_unfused_lamb_parity(monkeypatch):
-    """Three-kernel LAMB (moments / trust / update) stays available."""
-    monkeypatch.setenv("SP_LAMB_UNFUSED", "1")
-    _run_case("fp16", [0.5, 0.5], [1.0, 3.0], RAGGED, steps=2)
 
 
 @pytest.mark.parametrize("wire", ["fp32", "fp16", "q8"])
@@ -424,3 +438,76 @@ def test_run_host_matches_device_round(wire, shard):
         rnd.close()
     for a, b, name in zip(outs[0], outs[1], "pmv"):
         np.testing.assert_array_equal(a, b, err_msg=name)
+
+
+# ----------------------------------------------------------------------------
+# BASELINE.json configs 1-4 at full size (virtual peers on one GPU), the
+# averaged vector against the REFERENCE's own run_plan (oracle/_ref: the
+# fp64 weighted mean of groups.cpp:117-161 over the dequantized wire inputs).
+# Tolerance, elementwise, with a_g = (w_g / W) |x_g|:
+#   fp32 accumulation of G fmaf terms with fp32 weights: (G + 2) 2^-24 sum_g a_g
+#   plus the output's wire rounding: fp32 none, fp16 2^-11 |mean| + 2^-25,
+#   q8 half a code step of the output block (scale / 2).
+FULL_SIZE = {
+    "het4b-albert-base-fp32": ("albert-base", "fp32", "het4b"),
+    "g8-albert-large-fp16": ("albert-large", "fp16", None),
+    "g8-resnet50-q8": ("resnet50", "q8", None),
+    "het8c-albert-large-fp16": ("albert-large", "fp16", "het8c"),
+}
+
+
+@pytest.mark.parametrize("name", sorted(FULL_SIZE))
+def test_full_size_average_vs_reference_run_plan(name):
+    import json
+    import os
+
+    from oracle import ref as R
+    from paper_2106_10207_b200.dist import plan_round
+    from paper_2106_10207_b200.fleets import homogeneous, spec_json
+
+    table, wire, fleet = FULL_SIZE[name]
+    tables = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "tensor_tables.json")))
+    sizes = tables[table]
+    n = sum(sizes)
+    block = 4096
+    sj = spec_json(fleet) if fleet else json.dumps(homogeneous(8, 1.0, 1000.0, 4096.0, n))
+    plan = plan_round(sj, n, block if wire == "q8" else 8)
+    G = len(plan["fractions"])
+    weights = plan["weights"]
+    grads = []
+    for g in range(G):
+        t = torch.empty(n, device="cuda")
+        fill_synthetic(t, 7, g, SIGMA)
+        grads.append(t)
+    p = torch.zeros(n, device="cuda")
+    m, v = torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda")
+    rnd = AveragingRound(n, sizes, wire=wire, q8_block=block, peers_per_rank=G)
+    rnd.set_assignment(plan["offsets"], weights)
+    rnd.run(grads, p, m, v, 1)
+    torch.cuda.synchronize()
+    got_w, got_s = rnd.read_wire(nat.SP_BUF_AVG)
+    rnd.close()
+    del grads
+    got = O.dequant(wire, got_w, got_s, block)
+    # the reference's weighted mean of what each peer put on the wire
+    wires = []
+    for g in range(G):
+        x = O.fill_synthetic(n, 7, g, SIGMA)
+        q = O.pack(wire, x, block)
+        wires.append(None if weights[g] == 0 else O.dequant(wire, q[0], q[1], block))
+    want = R.weighted_mean(wires, weights)
+    W = sum(weights)
+    acc_mag = np.zeros(n, np.float64)
+    for g in range(G):
+        if wires[g] is not None:
+            acc_mag += (weights[g] / W) * np.abs(wires[g].astype(np.float64))
+    tol = (G + 2) * 2.0 ** -24 * acc_mag
+    if wire == "fp16":
+        tol += 2.0 ** -11 * np.abs(want) + 2.0 ** -25
+    elif wire == "q8":
+        tol += np.repeat(got_s.astype(np.float64), block)[:n] / 2 * (1 + 1e-6)
+    err = np.abs(got.astype(np.float64) - want)
+    bad = err > tol
+    assert not bad.any(), (f"{int(bad.sum())} elements outside tolerance; worst at "
+                           f"{int(np.argmax(err - tol))}: got {got[np.argmax(err - tol)]}, "
+                           f"want {want[np.argmax(err - tol)]}")
