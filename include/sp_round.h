@@ -184,6 +184,24 @@ void* sp_round_wire_ptr(sp_round* r, int local_peer);
  * every rank's copy (NULL without shard_lamb). */
 float* sp_round_param_ptr(sp_round* r);
 
+/* Host-only description of this rank's exchange plan (no device is touched;
+ * used to test the pointer tables at any world size, e.g. 8 ranks on a
+ * machine without GPUs). */
+typedef struct {
+  int pack_ranges;                          /* owner ranges K1 scatters to    */
+  int pack_owner[SP_MAX_RANKS];             /* in visiting order: next rank first */
+  int64_t pack_first_unit[SP_MAX_RANKS];    /* first wire unit of each range  */
+  int64_t pack_units[SP_MAX_RANKS];         /* units of each range            */
+  int pack_cta_begin[SP_MAX_RANKS + 1];     /* CTAs [begin[j], begin[j+1]) on range j */
+  int pack_ctas;                            /* K1 grid (x)                    */
+  int unit_elems;                           /* elements per wire unit         */
+  int64_t own_lo, own_hi;                   /* range this rank averages (K2)  */
+  int push_order[SP_MAX_RANKS];             /* rank order of pushes to all ranks (self last) */
+  int avg_push_ranks;                       /* ranks K2 writes the average to */
+} sp_plan_desc;
+int sp_round_describe(const sp_round_cfg* cfg, const int64_t* offsets, int sm_count,
+                      sp_plan_desc* out);
+
 /* Number of tensor windows of the LAMB plan (replicated LAMB: consecutive
  * tensors whose per-SM share of u fits half the shared-memory stash; sharded:
  * 1). Valid after sp_round_set_assignment; -1 for a null handle. */

@@ -49,6 +49,22 @@ class SpPhaseTimes(ctypes.Structure):
         "total_ms")]
 
 
+class SpPlanDesc(ctypes.Structure):
+    _fields_ = [
+        ("pack_ranges", ctypes.c_int),
+        ("pack_owner", ctypes.c_int * 8),
+        ("pack_first_unit", ctypes.c_int64 * 8),
+        ("pack_units", ctypes.c_int64 * 8),
+        ("pack_cta_begin", ctypes.c_int * 9),
+        ("pack_ctas", ctypes.c_int),
+        ("unit_elems", ctypes.c_int),
+        ("own_lo", ctypes.c_int64),
+        ("own_hi", ctypes.c_int64),
+        ("push_order", ctypes.c_int * 8),
+        ("avg_push_ranks", ctypes.c_int),
+    ]
+
+
 class PeerTimeout(RuntimeError):
     """A cross-rank barrier timed out (a peer process died or stalled)."""
 
@@ -83,6 +99,8 @@ def lib() -> ctypes.CDLL:
         "sp_round_avg_ptr": (vp, [vp]),
         "sp_round_param_ptr": (vp, [vp]),
         "sp_round_lamb_windows": (c_int, [vp]),
+        "sp_round_describe": (c_int, [ctypes.POINTER(SpRoundCfg), ctypes.POINTER(i64), c_int,
+                                      ctypes.POINTER(SpPlanDesc)]),
         "sp_round_padded_n": (i64, [vp]),
         "sp_round_trust_ptr": (vp, [vp]),
         "sp_round_copy_trust": (c_int, [vp, vp, vp]),
@@ -112,7 +130,7 @@ EXPORTED_SYMBOLS = [
     "sp_round_create", "sp_round_destroy", "sp_round_handle_bytes", "sp_round_export",
     "sp_round_connect", "sp_round_align", "sp_round_set_assignment", "sp_round_run",
     "sp_round_run_host", "sp_round_run_host_params", "sp_round_run_phased", "sp_round_wire_ptr",
-    "sp_round_avg_ptr", "sp_round_param_ptr", "sp_round_lamb_windows", "sp_round_padded_n",
+    "sp_round_avg_ptr", "sp_round_param_ptr", "sp_round_lamb_windows", "sp_round_describe", "sp_round_padded_n",
     "sp_round_trust_ptr", "sp_round_copy_trust", "sp_round_read", "sp_round_accumulate", "sp_round_accumulator_ptr",
     "sp_round_add_samples", "sp_round_samples", "sp_round_run_accumulated",
     "sp_vec_scale", "sp_vec_sum", "sp_vec_div", "sp_fill_synthetic", "sp_version", "sp_last_error",

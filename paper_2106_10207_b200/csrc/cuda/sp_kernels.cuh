@@ -25,9 +25,20 @@ namespace sp {
 #ifndef SP_LAMB_THREADS
 #define SP_LAMB_THREADS 256
 #endif
+#ifndef SP_LAMB_CTAS
+#define SP_LAMB_CTAS 3
+#endif
+#ifndef SP_LAMB_VEC
+#define SP_LAMB_VEC 2
+#endif
 constexpr int kLambThreads = SP_LAMB_THREADS;
-constexpr int kLambCtasPerSm = 1024 / kLambThreads;
-constexpr int kLambTile = 8192;     // max chunk length
+constexpr int kLambCtasPerSm = SP_LAMB_CTAS;  // register budget 65536 / (threads * CTAs)
+constexpr int kLambVec = SP_LAMB_VEC;          // float4 per thread in flight per array
+#ifndef SP_LAMB_ITERS
+#define SP_LAMB_ITERS 1
+#endif
+// max chunk length: SP_LAMB_ITERS passes of the CTA
+constexpr int kLambTile = kLambThreads * 4 * kLambVec * SP_LAMB_ITERS;
 constexpr int kPad = 16384;         // wire/avg buffers padded to this multiple
 
 struct BarrierArgs {
@@ -139,16 +150,13 @@ __device__ __forceinline__ void load_peers(const ReduceArgs& a, PeerView& pv) {
 }
 
 // One LAMB work item: a piece of one tensor, at most kLambTile elements,
-// processed by one CTA in both passes (sp_lamb.cuh).
-struct Chunk {
+// claimed by one CTA in pass 1 (sp_lamb.cuh).
+struct alignas(16) Chunk {
   long long start;
   int len;
   int tensor;
-  int stash;  // float offset of element `start` in the CTA's stash (start - stash = 0 mod 4),
-              // -1: not stashed, pass 2 recomputes u from p, m', v'
-  int run;    // slot of this chunk's (sum p^2, sum u^2) partial
-  int last;   // 1: last chunk of its run (the partial is stored after it)
-  int pad;
+  int tchunks;  // chunks of this tensor (in this rank's table)
+  int pad[3];
 };
 
 struct LambArgs {
@@ -736,49 +744,73 @@ __global__ void __launch_bounds__(1024) k_reduce_q8(ReduceArgs a) {
 // (/root/reference/SPEC.md:519); this follows You et al. (2019) as cited by
 // the paper.
 
-template <int W>
-__device__ __forceinline__ float4 load_grad4(const LambArgs& a, int64_t i) {
-  if constexpr (W != SP_WIRE_Q8) {
-    if (a.g32) {  // fused pack
-      const float4 x = *reinterpret_cast<const float4*>(a.g32 + i);
-      if constexpr (W == SP_WIRE_FP32) {
-        *reinterpret_cast<float4*>(static_cast<float*>(a.wire_out) + i) = x;
-        return x;
-      } else {
-        const uint32_t lo = pack_half2(x.x, x.y), hi = pack_half2(x.z, x.w);
-        *reinterpret_cast<uint2*>(static_cast<__half*>(a.wire_out) + i) = make_uint2(lo, hi);
-        const float2 f0 = unpack_half2(lo), f1 = unpack_half2(hi);
-        return make_float4(f0.x, f0.y, f1.x, f1.y);
-      }
+// The averaged gradient of 4 elements in two steps, so that a thread issues
+// every load of an iteration before the first dependent store: grad_load
+// issues the load (raw wire bits, or the fp32 gradient when the pack is
+// fused), grad_finish converts it and, with the fused pack, stores the wire
+// values.
+struct GradRaw {
+  float4 f;    // fp32 gradient (fused pack) or fp32 wire
+  uint2 h;     // fp16 wire
+  uint32_t q;  // q8 codes
+  float s;     // q8 scale
+};
+
+// FP: the pack is fused (one rank, one peer, fp32/fp16 wire; a.g32 set).
+template <int W, bool FP>
+__device__ __forceinline__ GradRaw grad_load(const LambArgs& a, int64_t i) {
+  GradRaw r;
+  if constexpr (FP) {
+    r.f = *reinterpret_cast<const float4*>(a.g32 + i);
+    return r;
+  }
+  if constexpr (W == SP_WIRE_FP32) {
+    r.f = *reinterpret_cast<const float4*>(static_cast<const float*>(a.avg) + i);
+  } else if constexpr (W == SP_WIRE_FP16) {
+    r.h = *reinterpret_cast<const uint2*>(static_cast<const __half*>(a.avg) + i);
+  } else {
+    r.q = *reinterpret_cast<const uint32_t*>(static_cast<const int8_t*>(a.avg) + i);
+    r.s = a.avg_scale[i >> a.qshift];
+  }
+  return r;
+}
+
+template <int W, bool FP>
+__device__ __forceinline__ float4 grad_finish(const LambArgs& a, int64_t i, const GradRaw& r) {
+  if constexpr (FP) {  // fused pack: the identity average, rounded to the wire format
+    static_assert(W != SP_WIRE_Q8, "the q8 pack is never fused");
+    if constexpr (W == SP_WIRE_FP32) {
+      *reinterpret_cast<float4*>(static_cast<float*>(a.wire_out) + i) = r.f;
+      return r.f;
+    } else {
+      const uint32_t lo = pack_half2(r.f.x, r.f.y), hi = pack_half2(r.f.z, r.f.w);
+      *reinterpret_cast<uint2*>(static_cast<__half*>(a.wire_out) + i) = make_uint2(lo, hi);
+      const float2 f0 = unpack_half2(lo), f1 = unpack_half2(hi);
+      return make_float4(f0.x, f0.y, f1.x, f1.y);
     }
   }
   if constexpr (W == SP_WIRE_FP32) {
-    return *reinterpret_cast<const float4*>(static_cast<const float*>(a.avg) + i);
+    return r.f;
   } else if constexpr (W == SP_WIRE_FP16) {
-    uint2 u = *reinterpret_cast<const uint2*>(static_cast<const __half*>(a.avg) + i);
-    float2 lo = unpack_half2(u.x), hi = unpack_half2(u.y);
+    const float2 lo = unpack_half2(r.h.x), hi = unpack_half2(r.h.y);
     return make_float4(lo.x, lo.y, hi.x, hi.y);
   } else {
-    const uint32_t u = *reinterpret_cast<const uint32_t*>(static_cast<const int8_t*>(a.avg) + i);
-    const float s = a.avg_scale[i >> a.qshift];
-    const float4 q = dequant4(u);
-    return make_float4(__fmul_rn(q.x, s), __fmul_rn(q.y, s), __fmul_rn(q.z, s), __fmul_rn(q.w, s));
+    const float4 q = dequant4(r.q);
+    return make_float4(__fmul_rn(q.x, r.s), __fmul_rn(q.y, r.s), __fmul_rn(q.z, r.s), __fmul_rn(q.w, r.s));
   }
 }
 
-template <int W>
+template <int W, bool FP>
 __device__ __forceinline__ float load_grad1(const LambArgs& a, int64_t i) {
-  if constexpr (W != SP_WIRE_Q8) {
-    if (a.g32) {  // fused pack
-      const float x = a.g32[i];
-      if constexpr (W == SP_WIRE_FP32) {
-        static_cast<float*>(a.wire_out)[i] = x;
-        return x;
-      } else {
-        const __half h = __float2half_rn(x);
-        static_cast<__half*>(a.wire_out)[i] = h;
-        return __half2float(h);
-      }
+  if constexpr (FP) {  // fused pack
+    const float x = a.g32[i];
+    if constexpr (W == SP_WIRE_FP32) {
+      static_cast<float*>(a.wire_out)[i] = x;
+      return x;
+    } else {
+      const __half h = __float2half_rn(x);
+      static_cast<__half*>(a.wire_out)[i] = h;
+      return __half2float(h);
     }
   }
   if constexpr (W == SP_WIRE_FP32) {

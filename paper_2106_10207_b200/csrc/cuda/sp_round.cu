@@ -93,16 +93,18 @@ struct sp_round {
   bool coop = true;  // cooperative launch accepted (also inside graph capture)
   Chunk* d_chunks = nullptr;
   size_t cap_chunks = 0;
-  int2* d_wrange = nullptr;
-  size_t cap_wrange = 0;
-  int2* d_trun = nullptr;
-  size_t cap_trun = 0;
-  float2* d_partial = nullptr;
+  int2* d_wchunk = nullptr;
+  size_t cap_wchunk = 0;
+  int2* d_tchunk = nullptr;
+  size_t cap_tchunk = 0;
+  float2* d_partial = nullptr;  // per chunk
   size_t cap_partial = 0;
-  int* d_cnt = nullptr;  // barrier counters (cap 64)
+  int* d_ovf = nullptr;         // per chunk slot: overflow lists of the windows
+  size_t cap_ovf = 0;
+  int* d_cnt = nullptr;         // queue / barrier / tensor counters (LambPlan::cnt)
+  size_t cap_cnt = 0;
   unsigned long long* d_trace = nullptr;  // SP_LAMB_TRACE builds only
   int nwin = 0;
-  std::vector<int> win_tensors;  // first tensor of each window (diagnostics)
   float* d_trust = nullptr;
   float* d_step_scale = nullptr;
   float* d_hp = nullptr;
@@ -179,112 +181,108 @@ int validate_cfg(const sp_round_cfg* c) {
 }
 
 // ------------------------------------------------------------- LAMB plan
-// Builds the static work split of k_lamb (sp_lamb.cuh):
-//   windows  replicated: consecutive whole tensors whose per-CTA share fits
-//            half the stash (a larger tensor gets a window of its own);
-//            sharded: one window, this rank's owned range;
-//   CTAs     each window's elements split evenly (boundaries multiples of 4);
-//   chunks   a CTA's range cut at tensor edges and every multiple of
-//            kLambTile; stashed in order while they fit (offset = start mod 4);
-//   runs     consecutive chunks of one tensor in one CTA (one norm partial).
-struct PlanBuilder {
-  std::vector<Chunk> chunks;
-  std::vector<int2> wrange;
-  std::vector<int2> trun;
-  int runs = 0;
-  int nwin = 0;
-};
-
-void plan_window(PlanBuilder& pb, const std::vector<int64_t>& tstart, int64_t lo, int64_t hi, int grid,
-                 int64_t cap) {
-  const int T = (int)tstart.size() - 1;
-  const int64_t E = hi - lo;
-  int64_t prev = lo;
-  for (int c = 0; c < grid; ++c) {
-    int64_t e = c + 1 == grid ? hi : lo + (int64_t)((__int128)E * (c + 1) / grid);
-    if (c + 1 < grid) e = std::max(prev, std::min(hi, e / 4 * 4));
-    int2 rg;
-    rg.x = (int)pb.chunks.size();
-    int64_t s = prev;
-    int t = (int)(std::upper_bound(tstart.begin(), tstart.end(), s) - tstart.begin()) - 1;
-    int64_t used = 0;
-    int cur_tensor = -1;
-    while (s < e) {
-      while (t + 1 < T && tstart[(size_t)t + 1] <= s) ++t;
-      int64_t ce = std::min({e, tstart[(size_t)t + 1], (s / kLambTile + 1) * kLambTile});
-      Chunk ch{};
-      ch.start = s;
-      ch.len = (int)(ce - s);
-      ch.tensor = t;
-      const int64_t o = used + (((s - used) % 4) + 4) % 4;  // o = s (mod 4)
-      if (o + ch.len <= cap) {
-        ch.stash = (int)o;
-        used = o + ch.len;
-      } else {
-        ch.stash = -1;
-      }
-      if (t != cur_tensor) {  // a new run
-        if (!pb.chunks.empty() && (int)pb.chunks.size() > rg.x) pb.chunks.back().last = 1;
-        if (pb.trun[(size_t)t].x < 0) pb.trun[(size_t)t].x = pb.runs;
-        ++pb.runs;
-        cur_tensor = t;
-      }
-      ch.run = pb.runs - 1;
-      pb.trun[(size_t)t].y = pb.runs;
-      pb.chunks.push_back(ch);
-      s = ce;
-    }
-    if ((int)pb.chunks.size() > rg.x) pb.chunks.back().last = 1;
-    rg.y = (int)pb.chunks.size();
-    pb.wrange.push_back(rg);
-    prev = e;
-  }
-  ++pb.nwin;
-}
+// Tables of k_lamb (sp_lamb.cuh):
+//   windows  replicated: sets of whole tensors filling at most kWindowFill
+//            of half of all stashes (a larger tensor gets a window of its
+//            own); sharded: one window, this rank's range;
+//   chunks   each window cut at tensor edges and every multiple of
+//            kLambTile, in element order; CTAs claim them at run time;
+//   tensors  the chunk range of every tensor (its norm partials).
+// Windows are kept below the stash capacity so that the dynamic claims,
+// which give fast CTAs more chunks, rarely overflow a CTA's half.
+constexpr double kWindowFill = 0.92;
 
 int build_lamb_plan(sp_round* r) {
   const int T = (int)r->tsizes.size();
-  const int grid = r->lamb_grid;
   std::vector<int64_t> tstart((size_t)T + 1, 0);
   for (int t = 0; t < T; ++t) tstart[(size_t)t + 1] = tstart[(size_t)t] + r->tsizes[(size_t)t];
-  PlanBuilder pb;
-  pb.trun.assign((size_t)T, make_int2(-1, -1));
-  const int64_t stash_floats = (int64_t)(r->stash_bytes / 4);
-  r->win_tensors.clear();
+  std::vector<Chunk> chunks;
+  std::vector<int2> wchunk, tchunk((size_t)T, make_int2(0, 0));
+  // chunks of [lo, hi) (tensor t's elements or a clipped part of them),
+  // every multiple of kLambTile a boundary
+  auto add_range = [&](int t, int64_t lo, int64_t hi) {
+    if (hi <= lo) return;
+    if (tchunk[(size_t)t].y == tchunk[(size_t)t].x) tchunk[(size_t)t].x = (int)chunks.size();
+    for (int64_t s = lo; s < hi;) {
+      const int64_t e = std::min(hi, (s / kLambTile + 1) * kLambTile);
+      Chunk ch{};
+      ch.start = s;
+      ch.len = (int)(e - s);
+      ch.tensor = t;
+      chunks.push_back(ch);
+      s = e;
+    }
+    tchunk[(size_t)t].y = (int)chunks.size();
+  };
+  auto open_window = [&]() { wchunk.push_back(make_int2((int)chunks.size(), 0)); };
+  auto close_window = [&]() { wchunk.back().y = (int)chunks.size(); };
   if (r->shard) {
-    plan_window(pb, tstart, r->own_lo(), r->own_hi(), grid, stash_floats);
+    open_window();
+    for (int t = 0; t < T; ++t)
+      add_range(t, std::max(tstart[(size_t)t], r->own_lo()), std::min(tstart[(size_t)t + 1], r->own_hi()));
+    close_window();
   } else {
-    const int64_t half = stash_floats / 2;
-    // per-CTA stash need of a window of E elements over k tensors (chunk
-    // alignment slack <= 3 floats per chunk)
-    auto need = [&](int64_t E, int k) {
-      const int64_t per = (E + grid - 1) / grid + 4;
-      return per + 3 * (per / kLambTile + 2 + k);
-    };
-    int t = 0;
-    while (t < T) {
-      int t1 = t + 1;
-      int64_t E = r->tsizes[(size_t)t];
-      while (t1 < T && need(E + r->tsizes[(size_t)t1], t1 + 1 - t) <= half) E += r->tsizes[(size_t)t1++];
-      r->win_tensors.push_back(t);
-      plan_window(pb, tstart, tstart[(size_t)t], tstart[(size_t)t1], grid, half);
-      t = t1;
+    // Windows are sets of whole tensors (not necessarily adjacent), at most
+    // `fill` elements unless one tensor alone is larger: longest tensors
+    // first, each into the least loaded window it fits, with as few windows
+    // as the total allows, so the windows come out of similar size and the
+    // split-phase barrier of one window is hidden by the next window's pass 1.
+    // Largest windows first, smallest last (its pass 2 is not overlapped).
+    const double fill = (double)(r->stash_bytes / 8) * r->lamb_grid * kWindowFill;
+    std::vector<int> order((size_t)T);
+    for (int t = 0; t < T; ++t) order[(size_t)t] = t;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int x, int y) { return r->tsizes[(size_t)x] > r->tsizes[(size_t)y]; });
+    int64_t rest = 0;
+    for (int t = 0; t < T; ++t)
+      if ((double)r->tsizes[(size_t)t] <= fill) rest += r->tsizes[(size_t)t];
+    std::vector<std::vector<int>> win;
+    std::vector<int64_t> load;
+    for (int t : order)
+      if ((double)r->tsizes[(size_t)t] > fill) {
+        win.push_back({t});
+        load.push_back(r->tsizes[(size_t)t]);
+      }
+    const size_t big = win.size();
+    for (size_t k = 0; k < (size_t)std::ceil((double)rest / fill); ++k) {
+      win.emplace_back();
+      load.push_back(0);
+    }
+    for (int t : order) {
+      const int64_t sz = r->tsizes[(size_t)t];
+      if ((double)sz > fill) continue;
+      size_t best = win.size();
+      for (size_t k = big; k < win.size(); ++k)
+        if ((double)(load[k] + sz) <= fill && (best == win.size() || load[k] < load[best])) best = k;
+      if (best == win.size()) {  // no room: one more window
+        win.emplace_back();
+        load.push_back(0);
+        best = win.size() - 1;
+      }
+      win[best].push_back(t);
+      load[best] += sz;
+    }
+    std::vector<size_t> wo;
+    for (size_t k = 0; k < win.size(); ++k)
+      if (load[k] > 0) wo.push_back(k);
+    std::stable_sort(wo.begin(), wo.end(), [&](size_t x, size_t y) { return load[x] > load[y]; });
+    for (size_t k : wo) {
+      std::sort(win[k].begin(), win[k].end());  // tensor order inside a window
+      open_window();
+      for (int t : win[k]) add_range(t, tstart[(size_t)t], tstart[(size_t)t + 1]);
+      close_window();
     }
   }
-  for (auto& x : pb.trun)
-    if (x.x < 0) x = make_int2(0, 0);  // no run on this rank (sharded)
-  r->nwin = pb.nwin;
-  if (r->nwin + 4 > 64) return fail(SP_ERR_STATE, "LAMB plan: too many windows");
+  for (Chunk& ch : chunks) ch.tchunks = tchunk[(size_t)ch.tensor].y - tchunk[(size_t)ch.tensor].x;
+  r->nwin = (int)wchunk.size();
+  const size_t ncnt = 4 * (size_t)r->nwin + 4 + (size_t)T;
   SP_CUDA(cudaSetDevice(r->cfg.device));
-  if (int rc = upload(r->d_chunks, r->cap_chunks, pb.chunks)) return rc;
-  if (int rc = upload(r->d_wrange, r->cap_wrange, pb.wrange)) return rc;
-  if (int rc = upload(r->d_trun, r->cap_trun, pb.trun)) return rc;
-  if (pb.runs > (int)r->cap_partial || !r->d_partial) {
-    cudaFree(r->d_partial);
-    r->d_partial = nullptr;
-    r->cap_partial = std::max(pb.runs, 1);
-    SP_CUDA(cudaMalloc(&r->d_partial, r->cap_partial * sizeof(float2)));
-  }
+  if (int rc = upload(r->d_chunks, r->cap_chunks, chunks)) return rc;
+  if (int rc = upload(r->d_wchunk, r->cap_wchunk, wchunk)) return rc;
+  if (int rc = upload(r->d_tchunk, r->cap_tchunk, tchunk)) return rc;
+  if (int rc = upload(r->d_partial, r->cap_partial, std::vector<float2>(chunks.size()))) return rc;
+  if (int rc = upload(r->d_ovf, r->cap_ovf, std::vector<int>(chunks.size()))) return rc;
+  if (int rc = upload(r->d_cnt, r->cap_cnt, std::vector<int>(ncnt, 0))) return rc;
   return SP_OK;
 }
 
@@ -309,6 +307,12 @@ const char* avg_buffer(const sp_round* r) {
   const char* id = identity_avg(r);
   return id ? id : r->avg(r->cfg.rank);
 }
+
+// Rank order of every push to all ranks (averages, parameters, norm pairs):
+// the next rank first and this rank last, so that at any moment the ranks
+// write to different owners (all-to-all without incast: ~660 vs ~400 GB/s
+// per direction on 4x B200, profiles/r01/p2p_bw.txt).
+int push_rank(int rank, int world, int k) { return (rank + 1 + k) % world; }
 
 LambArgs make_lamb_args(sp_round* r, float* p, float* m, float* v) {
   const sp_round_cfg& c = r->cfg;
@@ -343,7 +347,7 @@ BarrierArgs make_barrier(sp_round* r) {
   return ba;
 }
 
-template <int W>
+template <int W, bool FP>
 cudaError_t launch_lamb_w(sp_round* r, const LambArgs& a, const LambPlan& pl, cudaStream_t st) {
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3((unsigned)r->lamb_grid);
@@ -355,16 +359,17 @@ cudaError_t launch_lamb_w(sp_round* r, const LambArgs& a, const LambPlan& pl, cu
   at[0].val.cooperative = 1;
   lc.attrs = at;
   lc.numAttrs = r->coop ? 1 : 0;
-  return cudaLaunchKernelEx(&lc, k_lamb<W>, a, pl);
+  return cudaLaunchKernelEx(&lc, k_lamb<W, FP>, a, pl);
 }
 
 int launch_lamb(sp_round* r, const LambArgs& a, const BarrierArgs& ba, cudaStream_t st) {
   const sp_round_cfg& c = r->cfg;
   LambPlan pl{};
   pl.chunks = r->d_chunks;
-  pl.wrange = r->d_wrange;
-  pl.trun = r->d_trun;
+  pl.wchunk = r->d_wchunk;
+  pl.tchunk = r->d_tchunk;
   pl.partial = r->d_partial;
+  pl.ovf = r->d_ovf;
   pl.cnt = r->d_cnt;
   pl.trust = r->d_trust;
   pl.step_scale = r->d_step_scale;
@@ -372,15 +377,11 @@ int launch_lamb(sp_round* r, const LambArgs& a, const BarrierArgs& ba, cudaStrea
   pl.half = (int)(r->stash_bytes / 8);
   pl.T = c.num_tensors;
   pl.shard = r->shard ? 1 : 0;
-  pl.nbar = r->shard ? 3 : r->nwin;
-#ifdef SP_LAMB_TRACE
-  if (!r->d_trace) cudaMalloc(&r->d_trace, (size_t)r->lamb_grid * 64 * sizeof(unsigned long long));
   pl.trace = r->d_trace;
-#endif
   if (r->shard) {
     pl.push.ndst = c.world;
     for (int k = 0; k < c.world; ++k) {
-      const int d = (c.rank + 1 + k) % c.world;  // next rank first, self last
+      const int d = push_rank(c.rank, c.world, k);
       pl.table[k] = r->norms(d);
       pl.push.dst[k] = r->param(d);
     }
@@ -389,9 +390,13 @@ int launch_lamb(sp_round* r, const LambArgs& a, const BarrierArgs& ba, cudaStrea
   }
   cudaError_t e;
   switch (c.wire) {
-    case SP_WIRE_FP32: e = launch_lamb_w<SP_WIRE_FP32>(r, a, pl, st); break;
-    case SP_WIRE_FP16: e = launch_lamb_w<SP_WIRE_FP16>(r, a, pl, st); break;
-    default: e = launch_lamb_w<SP_WIRE_Q8>(r, a, pl, st); break;
+    case SP_WIRE_FP32:
+      e = a.g32 ? launch_lamb_w<SP_WIRE_FP32, true>(r, a, pl, st) : launch_lamb_w<SP_WIRE_FP32, false>(r, a, pl, st);
+      break;
+    case SP_WIRE_FP16:
+      e = a.g32 ? launch_lamb_w<SP_WIRE_FP16, true>(r, a, pl, st) : launch_lamb_w<SP_WIRE_FP16, false>(r, a, pl, st);
+      break;
+    default: e = launch_lamb_w<SP_WIRE_Q8, false>(r, a, pl, st); break;
   }
   if (e != cudaSuccess) return fail(SP_ERR_CUDA, std::string("k_lamb launch: ") + cudaGetErrorString(e));
   return SP_OK;
@@ -409,8 +414,43 @@ int barrier(const BarrierArgs& ba, cudaStream_t st) {
   return SP_OK;
 }
 
+// The host half of K1: the owner ranges this rank scatters to (visited from
+// the next rank on, empty ranges skipped), in wire units (a q8 block or one
+// 16-byte vector), and the CTAs given to each range in proportion to its
+// length (>= 1 each). Returns the number of CTAs. Host-only (sp_round_describe
+// exposes it for tests at any world size).
+int pack_plan(const sp_round_cfg& c, int L, const int64_t* offsets, int sm_count, PackArgs& a) {
+  const int64_t unit = c.wire == SP_WIRE_Q8 ? c.q8_block : (c.wire == SP_WIRE_FP16 ? 8 : 4);
+  a.nr = 0;
+  a.pref[0] = 0;
+  for (int d = 1; d <= c.world; ++d) {
+    const int k = (c.rank + d) % c.world;
+    const int64_t lo = offsets[(size_t)k * L], hi = offsets[(size_t)(k + 1) * L];
+    if (hi <= lo) continue;
+    a.owner[a.nr] = k;
+    a.lo[a.nr] = lo / unit;
+    a.pref[a.nr + 1] = a.pref[a.nr] + (hi + unit - 1) / unit - lo / unit;
+    ++a.nr;
+  }
+  a.cta0[0] = 0;
+  const int64_t units = a.pref[a.nr];
+  if (units <= 0) return 0;
+  const int64_t per_cta = c.wire == SP_WIRE_Q8 ? 1 : 256;  // units per CTA per pass
+  const int want = c.wire == SP_WIRE_Q8 ? (int)std::min<int64_t>(units, (int64_t)sm_count * 16)
+                                        : grid_for(units, 256, sm_count, 8);
+  int total = 0;
+  for (int j = 0; j < a.nr; ++j) {
+    const int64_t len = a.pref[j + 1] - a.pref[j];
+    int nct = (int)std::max<int64_t>(1, (int64_t)((double)want * (double)len / (double)units + 0.5));
+    nct = (int)std::min<int64_t>(nct, (len + per_cta - 1) / per_cta);
+    total += std::max(1, nct);
+    a.cta0[j + 1] = total;
+  }
+  return total;
+}
+
 // K1: pack every local peer's gradient, scattering each owner's range into
-// that owner's inbox; ranges visited starting with the next rank's.
+// that owner's inbox (pack_plan).
 int enqueue_pack(sp_round* r, const float* const* grads, cudaStream_t st) {
   const sp_round_cfg& c = r->cfg;
   PackArgs a{};
@@ -426,37 +466,12 @@ int enqueue_pack(sp_round* r, const float* const* grads, cudaStream_t st) {
     else
       a.src[l] = nullptr;  // nothing to pack (aggregation-only or zero-copy)
   }
-  const int64_t unit = c.wire == SP_WIRE_Q8 ? c.q8_block : (c.wire == SP_WIRE_FP16 ? 8 : 4);
-  a.nr = 0;
-  a.pref[0] = 0;
-  for (int d = 1; d <= c.world; ++d) {
-    const int k = (c.rank + d) % c.world;
-    const int64_t lo = r->offsets[(size_t)k * r->L], hi = r->offsets[(size_t)(k + 1) * r->L];
-    if (hi <= lo) continue;
-    a.owner[a.nr] = k;
-    a.lo[a.nr] = lo / unit;
-    a.pref[a.nr + 1] = a.pref[a.nr] + (hi + unit - 1) / unit - lo / unit;
-    ++a.nr;
-  }
+  const int total = pack_plan(c, r->L, r->offsets.data(), r->sm_count, a);
   a.n = r->n;
   a.npad = r->npad;
   a.qblock = c.q8_block;
-  const int64_t units = a.pref[a.nr];
-  if (!any || units <= 0) return SP_OK;
+  if (!any || total <= 0) return SP_OK;
   const int threads = c.wire == SP_WIRE_Q8 ? c.q8_block / 16 : 256;
-  const int64_t per_cta = c.wire == SP_WIRE_Q8 ? 1 : 256;  // units per CTA per pass
-  const int want = c.wire == SP_WIRE_Q8 ? (int)std::min<int64_t>(units, (int64_t)r->sm_count * 16)
-                                        : grid_for(units, 256, r->sm_count, 8);
-  // CTAs split over the ranges in proportion to their lengths (>= 1 each)
-  int total = 0;
-  a.cta0[0] = 0;
-  for (int j = 0; j < a.nr; ++j) {
-    const int64_t len = a.pref[j + 1] - a.pref[j];
-    int nct = (int)std::max<int64_t>(1, (int64_t)((double)want * (double)len / (double)units + 0.5));
-    nct = (int)std::min<int64_t>(nct, (len + per_cta - 1) / per_cta);
-    total += std::max(1, nct);
-    a.cta0[j + 1] = total;
-  }
   dim3 grid((unsigned)total, r->L);
   if (c.wire == SP_WIRE_Q8) k_pack_q8<<<grid, threads, 0, st>>>(a);
   else if (c.wire == SP_WIRE_FP16) k_pack_fp16<<<grid, threads, 0, st>>>(a);
@@ -494,7 +509,7 @@ int enqueue_reduce(sp_round* r, cudaStream_t st) {
   if (ra.hi <= ra.lo) return SP_OK;
   const int nd = r->shard ? 1 : c.world;
   ra.ndst = nd;
-  for (int k = 0; k < nd; ++k) ra.dst[k] = r->avg((c.rank + 1 + k + (c.world - nd)) % c.world);
+  for (int k = 0; k < nd; ++k) ra.dst[k] = r->avg(push_rank(c.rank, c.world, k + (c.world - nd)));
   if (c.wire == SP_WIRE_Q8) {
     const int64_t nb = (ra.hi + c.q8_block - 1) / c.q8_block - ra.lo / c.q8_block;
     const int grid = (int)std::min<int64_t>(nb, (int64_t)r->sm_count * 16);
@@ -647,20 +662,20 @@ int launch_graph(sp_round* r, const std::vector<const void*>& key, const float* 
 
 // k_lamb runs kLambCtasPerSm CTAs per SM; each gets an equal share of the
 // SM's shared memory (less the per-CTA reservation) as its stash.
-template <int W>
+template <int W, bool FP>
 int lamb_func_setup(sp_round* r, int per_sm_smem, int optin, int reserved) {
   cudaFuncAttributes fa{};
-  SP_CUDA(cudaFuncGetAttributes(&fa, k_lamb<W>));
+  SP_CUDA(cudaFuncGetAttributes(&fa, k_lamb<W, FP>));
   const size_t share = (size_t)per_sm_smem / kLambCtasPerSm - (size_t)reserved - fa.sharedSizeBytes;
   const size_t dyn = std::min(share, (size_t)optin - fa.sharedSizeBytes) / 64 * 64;
   r->stash_bytes = r->stash_bytes ? std::min(r->stash_bytes, dyn) : dyn;
-  SP_CUDA(cudaFuncSetAttribute(k_lamb<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+  SP_CUDA(cudaFuncSetAttribute(k_lamb<W, FP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
   return SP_OK;
 }
 
-template <int W>
+template <int W, bool FP>
 int lamb_occupancy(sp_round* r, int* per_sm) {
-  SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_lamb<W>, kLambThreads, r->stash_bytes));
+  SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_lamb<W, FP>, kLambThreads, r->stash_bytes));
   return SP_OK;
 }
 
@@ -713,15 +728,19 @@ int sp_round_create(const sp_round_cfg* cfg, sp_round** out) {
     sp_round_destroy(r);
     return code;
   };
-  if (int rc2 = lamb_func_setup<SP_WIRE_FP32>(r, per_sm_smem, optin, reserved)) return cleanup(rc2);
-  if (int rc2 = lamb_func_setup<SP_WIRE_FP16>(r, per_sm_smem, optin, reserved)) return cleanup(rc2);
-  if (int rc2 = lamb_func_setup<SP_WIRE_Q8>(r, per_sm_smem, optin, reserved)) return cleanup(rc2);
+  if (int rc2 = lamb_func_setup<SP_WIRE_FP32, false>(r, per_sm_smem, optin, reserved)) return cleanup(rc2);
+  if (int rc2 = lamb_func_setup<SP_WIRE_FP32, true>(r, per_sm_smem, optin, reserved)) return cleanup(rc2);
+  if (int rc2 = lamb_func_setup<SP_WIRE_FP16, false>(r, per_sm_smem, optin, reserved)) return cleanup(rc2);
+  if (int rc2 = lamb_func_setup<SP_WIRE_FP16, true>(r, per_sm_smem, optin, reserved)) return cleanup(rc2);
+  if (int rc2 = lamb_func_setup<SP_WIRE_Q8, false>(r, per_sm_smem, optin, reserved)) return cleanup(rc2);
   {
-    int occ[3] = {};
-    if (int rc2 = lamb_occupancy<SP_WIRE_FP32>(r, &occ[0])) return cleanup(rc2);
-    if (int rc2 = lamb_occupancy<SP_WIRE_FP16>(r, &occ[1])) return cleanup(rc2);
-    if (int rc2 = lamb_occupancy<SP_WIRE_Q8>(r, &occ[2])) return cleanup(rc2);
-    const int per_sm = std::min({occ[0], occ[1], occ[2], kLambCtasPerSm});
+    int occ[5] = {};
+    if (int rc2 = lamb_occupancy<SP_WIRE_FP32, false>(r, &occ[0])) return cleanup(rc2);
+    if (int rc2 = lamb_occupancy<SP_WIRE_FP32, true>(r, &occ[1])) return cleanup(rc2);
+    if (int rc2 = lamb_occupancy<SP_WIRE_FP16, false>(r, &occ[2])) return cleanup(rc2);
+    if (int rc2 = lamb_occupancy<SP_WIRE_FP16, true>(r, &occ[3])) return cleanup(rc2);
+    if (int rc2 = lamb_occupancy<SP_WIRE_Q8, false>(r, &occ[4])) return cleanup(rc2);
+    const int per_sm = std::min({occ[0], occ[1], occ[2], occ[3], occ[4], kLambCtasPerSm});
     if (per_sm < 1) return cleanup(fail(SP_ERR_CUDA, "k_lamb does not fit on an SM (registers / shared memory)"));
     r->lamb_grid = per_sm * r->sm_count;  // cooperative: every CTA resident at once
   }
@@ -740,10 +759,8 @@ int sp_round_create(const sp_round_cfg* cfg, sp_round** out) {
   if ((e = cudaMalloc(&r->d_trust, ntens * sizeof(float))) != cudaSuccess ||
       (e = cudaMalloc(&r->d_step_scale, ntens * sizeof(float))) != cudaSuccess ||
       (e = cudaMalloc(&r->d_hp, 4 * sizeof(float))) != cudaSuccess ||
-      (e = cudaMalloc(&r->d_cnt, 64 * sizeof(int))) != cudaSuccess ||
       (e = cudaMalloc(&r->epoch, sizeof(unsigned long long))) != cudaSuccess)
     return cleanup(fail(SP_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e)));
-  cudaMemset(r->d_cnt, 0, 64 * sizeof(int));
   cudaMemset(r->epoch, 0, sizeof(unsigned long long));
   cudaMemset(r->d_trust, 0, ntens * sizeof(float));
   if ((e = cudaHostAlloc(&r->h_err, sizeof(int), cudaHostAllocMapped)) != cudaSuccess)
@@ -769,8 +786,9 @@ int sp_round_destroy(sp_round* r) {
     if (r->base[k] && k != r->cfg.rank) cudaIpcCloseMemHandle(r->base[k]);
   cudaFree(r->shared);
   cudaFree(r->d_chunks);
-  cudaFree(r->d_wrange);
-  cudaFree(r->d_trun);
+  cudaFree(r->d_wchunk);
+  cudaFree(r->d_tchunk);
+  cudaFree(r->d_ovf);
   cudaFree(r->d_partial);
   cudaFree(r->d_cnt);
   cudaFree(r->d_trace);
@@ -844,6 +862,9 @@ int sp_round_set_assignment(sp_round* r, const int64_t* offsets, const double* w
   r->offsets.assign(offsets, offsets + G + 1);
   r->weights.assign(weights, weights + G);
   if (int rc = build_lamb_plan(r)) return rc;
+#ifdef SP_LAMB_TRACE
+  if (!r->d_trace) SP_CUDA(cudaMalloc(&r->d_trace, (size_t)r->lamb_grid * 64 * sizeof(unsigned long long)));
+#endif
   r->assigned = true;
   drop_graphs(r);
   return SP_OK;
@@ -945,6 +966,32 @@ int sp_round_run_phased(sp_round* r, const float* const* grads, float* p, float*
 }
 
 int sp_round_lamb_windows(const sp_round* r) { return r ? r->nwin : -1; }
+
+int sp_round_describe(const sp_round_cfg* cfg, const int64_t* offsets, int sm_count, sp_plan_desc* out) {
+  if (int rc = validate_cfg(cfg)) return rc;
+  if (!offsets || !out || sm_count < 1) return fail(SP_ERR_ARG, "null argument");
+  const int L = cfg->peers_per_rank, world = cfg->world, G = L * world;
+  if (offsets[0] != 0 || offsets[G] != cfg->n) return fail(SP_ERR_ARG, "offsets must start at 0 and end at n");
+  for (int g = 0; g < G; ++g)
+    if (offsets[g + 1] < offsets[g]) return fail(SP_ERR_ARG, "offsets must be non-decreasing");
+  *out = sp_plan_desc{};
+  PackArgs a{};
+  out->pack_ctas = pack_plan(*cfg, L, offsets, sm_count, a);
+  out->pack_ranges = a.nr;
+  out->unit_elems = cfg->wire == SP_WIRE_Q8 ? cfg->q8_block : (cfg->wire == SP_WIRE_FP16 ? 8 : 4);
+  for (int j = 0; j < a.nr; ++j) {
+    out->pack_owner[j] = a.owner[j];
+    out->pack_first_unit[j] = a.lo[j];
+    out->pack_units[j] = a.pref[j + 1] - a.pref[j];
+    out->pack_cta_begin[j] = a.cta0[j];
+  }
+  out->pack_cta_begin[a.nr] = a.cta0[a.nr];
+  out->own_lo = offsets[(size_t)cfg->rank * L];
+  out->own_hi = offsets[(size_t)(cfg->rank + 1) * L];
+  for (int k = 0; k < world; ++k) out->push_order[k] = push_rank(cfg->rank, world, k);
+  out->avg_push_ranks = cfg->shard_lamb ? 1 : world;
+  return SP_OK;
+}
 
 #ifdef SP_LAMB_TRACE
 // Diagnostic builds: per-CTA globaltimer stamps of the last k_lamb launch

@@ -63,36 +63,49 @@ def check_same_plan(offsets, weights, group=None) -> None:
         raise RuntimeError("ranks disagree on the round assignment (offsets/weights)")
 
 
-def share_fd(fd: int | None, src: int = 0, group=None, tag: str = "sp") -> int:
+def share_fd(fd: int | None, src: int = 0, group=None, tag: str = "sp", timeout_s: float = 60.0) -> int:
     """Give every rank of one node a file descriptor owned by rank `src`.
 
     CUDA multicast objects and VMM allocations are shared between processes
     as POSIX file descriptors (cuMemExportToShareableHandle), which cannot
     travel through torch.distributed. Rank `src` listens on an abstract Unix
-    socket whose name it all-gathers; every other rank connects and receives
-    the descriptor with SCM_RIGHTS. Returns the local descriptor (`fd` itself
-    on `src`; the caller closes received ones)."""
+    socket whose name (with a random nonce) it all-gathers together with
+    every rank's pid; every other rank connects and receives the descriptor
+    with SCM_RIGHTS. The source hands the descriptor only to a peer whose
+    SO_PEERCRED pid and uid are one of the job's ranks (a descriptor maps GPU
+    memory of the job), each once, and gives up after `timeout_s`. Returns
+    the local descriptor (`fd` itself on `src`; the caller closes received
+    ones)."""
     import os
+    import secrets
     import socket
+    import struct
 
     import torch.distributed as dist
 
     rank, world = dist.get_rank(group), dist.get_world_size(group)
-    names: list = [None] * world
-    name = f"\0{tag}-{os.getpid()}-{rank}" if rank == src else None
-    dist.all_gather_object(names, name, group=group)
-    path = names[src]
+    info: list = [None] * world
+    name = f"\0{tag}-{secrets.token_hex(16)}" if rank == src else None
+    dist.all_gather_object(info, (name, os.getpid(), os.getuid()), group=group)
+    path = info[src][0]
     if rank == src:
         if fd is None:
             raise ValueError("the source rank must pass a descriptor")
+        expected = {(pid, uid) for r, (_, pid, uid) in enumerate(info) if r != src}
         srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
         srv.bind(path)
         srv.listen(world)
+        srv.settimeout(timeout_s)
         dist.barrier(group=group)  # listening before anyone connects
         try:
-            for _ in range(world - 1):
+            while expected:
                 conn, _ = srv.accept()
                 with conn:
+                    cred = conn.getsockopt(socket.SOL_SOCKET, socket.SO_PEERCRED, struct.calcsize("3i"))
+                    pid, uid, _ = struct.unpack("3i", cred)
+                    if (pid, uid) not in expected:
+                        continue  # not one of this job's ranks (or already served)
+                    expected.discard((pid, uid))
                     socket.send_fds(conn, [b"fd"], [fd])
         finally:
             srv.close()
@@ -100,6 +113,7 @@ def share_fd(fd: int | None, src: int = 0, group=None, tag: str = "sp") -> int:
         return fd
     dist.barrier(group=group)
     with socket.socket(socket.AF_UNIX, socket.SOCK_STREAM) as c:
+        c.settimeout(timeout_s)
         c.connect(path)
         _, fds, _, _ = socket.recv_fds(c, 16, 1)
     dist.barrier(group=group)

@@ -38,8 +38,11 @@ def part_offsets(n: int, fractions: Sequence[float], align: int) -> list[int]:
     for k in range(1, G):
         cum += float(fractions[k - 1])
         x = n * cum / align
-        # llround semantics (half away from zero), as in the C++/C versions
-        o = align * int(math.floor(x + 0.5))
+        # std::llround (half away from zero) as the C++ partition.cpp does;
+        # x >= 0, and x - floor(x) is exact, unlike floor(x + 0.5) (which
+        # rounds 0.49999999999999994 up)
+        f = math.floor(x)
+        o = align * (int(f) + (1 if x - f >= 0.5 else 0))
         out[k] = min(n, max(out[k - 1], o))
     out[G] = n
     return out

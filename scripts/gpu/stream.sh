@@ -1,0 +1,2 @@
+mkdir -p gpurun_out
+timeout 300 scripts/micro/stream_bw > gpurun_out/stream_bw.txt 2>&1

@@ -206,3 +206,16 @@ def test_part_offsets_het8c_shape():
     lens = [b - a for a, b in zip(offs, offs[1:])]
     assert lens[6] == 0  # the client owns nothing
     assert abs(lens[7] / 17847474 - 0.7) < 1e-5
+
+
+def test_part_offsets_round_half_away_exactly():
+    # x = n * cum / align just below 0.5: llround gives 0, floor(x + 0.5)
+    # would give 1; the Python mirror, the C++ partitioner and
+    # the C oracle agree
+    from paper_2106_10207_b200 import _swarmplan as sp
+
+    f = 0.49999999999999994
+    for n, fr, align in [(1, [f, 1 - f], 1), (2, [f / 2, 1 - f / 2], 1), (8, [f / 8 * 8, 1.0], 8)]:
+        want = sp.part_offsets(n, fr, align)
+        assert part_offsets(n, fr, align) == want == O.part_offsets(n, fr, align), (n, fr)
+    assert part_offsets(1, [f, 1 - f], 1) == [0, 0, 1]
