@@ -515,7 +515,7 @@ def main():
     if world > 1:
         all_ph = [None] * world
         torch.distributed.all_gather_object(all_ph, ph)
-    nwin = rnd.lamb_windows()
+    nchunks = rnd.lamb_chunks()[0]
     rnd.close()
     del host_g, p_host
 
@@ -584,7 +584,7 @@ def main():
                        "wire": wire, "q8_block": block if wire == "q8" else None,
                        "lamb": "sharded (ZeRO-1: owners step, fp32 params pushed)" if args.shard_lamb
                                else "replicated (averaged gradient all-gathered)",
-                       "lamb_windows": nwin,
+                       "lamb_chunks": nchunks,
                        "fleet": fleet or f"homogeneous{G}",
                        "fractions": fr if G <= 16 else f"{min(fr)}..{max(fr)}",
                        "plan": "solve_strategy (host LP) -> part_offsets; weights = LP sample "

@@ -202,10 +202,11 @@ typedef struct {
 int sp_round_describe(const sp_round_cfg* cfg, const int64_t* offsets, int sm_count,
                       sp_plan_desc* out);
 
-/* Number of tensor windows of the LAMB plan (replicated LAMB: consecutive
- * tensors whose per-SM share of u fits half the shared-memory stash; sharded:
- * 1). Valid after sp_round_set_assignment; -1 for a null handle. */
-int sp_round_lamb_windows(const sp_round* r);
+/* Number of chunks of the LAMB plan: the elements this rank steps
+ * (replicated: all n; sharded: its owned range) cut at tensor edges and
+ * every multiple of the chunk tile; *tile receives the tile (elements) when
+ * not null. Valid after sp_round_set_assignment; -1 for a null handle. */
+int sp_round_lamb_chunks(const sp_round* r, int* tile);
 void* sp_round_avg_ptr(sp_round* r);
 int64_t sp_round_padded_n(const sp_round* r);
 /* Per-tensor trust ratios of the last step (device float[num_tensors]). */

@@ -28,7 +28,8 @@ NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CUDA_SOURCES = [os.path.join(PKG, "csrc", "cuda", "sp_round.cu")]
-CUDA_DEPS = CUDA_SOURCES + glob.glob(os.path.join(PKG, "csrc", "cuda", "*.cuh")) + [
+CUDA_DEPS = CUDA_SOURCES + glob.glob(os.path.join(PKG, "csrc", "cuda", "*.cuh")) + glob.glob(
+    os.path.join(PKG, "csrc", "cuda", "*.h")) + [
     os.path.join(INC, "sp_round.h")
 ]
 HOST_SOURCES = sorted(glob.glob(os.path.join(PKG, "csrc", "host", "*.cpp")))

@@ -98,7 +98,7 @@ def lib() -> ctypes.CDLL:
         "sp_round_wire_ptr": (vp, [vp, c_int]),
         "sp_round_avg_ptr": (vp, [vp]),
         "sp_round_param_ptr": (vp, [vp]),
-        "sp_round_lamb_windows": (c_int, [vp]),
+        "sp_round_lamb_chunks": (c_int, [vp, ctypes.POINTER(c_int)]),
         "sp_round_describe": (c_int, [ctypes.POINTER(SpRoundCfg), ctypes.POINTER(i64), c_int,
                                       ctypes.POINTER(SpPlanDesc)]),
         "sp_round_padded_n": (i64, [vp]),
@@ -130,7 +130,7 @@ EXPORTED_SYMBOLS = [
     "sp_round_create", "sp_round_destroy", "sp_round_handle_bytes", "sp_round_export",
     "sp_round_connect", "sp_round_align", "sp_round_set_assignment", "sp_round_run",
     "sp_round_run_host", "sp_round_run_host_params", "sp_round_run_phased", "sp_round_wire_ptr",
-    "sp_round_avg_ptr", "sp_round_param_ptr", "sp_round_lamb_windows", "sp_round_describe", "sp_round_padded_n",
+    "sp_round_avg_ptr", "sp_round_param_ptr", "sp_round_lamb_chunks", "sp_round_describe", "sp_round_padded_n",
     "sp_round_trust_ptr", "sp_round_copy_trust", "sp_round_read", "sp_round_accumulate", "sp_round_accumulator_ptr",
     "sp_round_add_samples", "sp_round_samples", "sp_round_run_accumulated",
     "sp_vec_scale", "sp_vec_sum", "sp_vec_div", "sp_fill_synthetic", "sp_version", "sp_last_error",

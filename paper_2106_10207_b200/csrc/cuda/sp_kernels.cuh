@@ -19,26 +19,34 @@
 
 namespace sp {
 
-// LAMB CTA: kLambThreads threads, 1024 / kLambThreads CTAs per SM (64
-// registers per thread), so several CTAs per SM overlap their memory and
-// compute phases.
-#ifndef SP_LAMB_THREADS
-#define SP_LAMB_THREADS 256
+// LAMB CTA (sp_lamb.cuh): SP_LAMB_WARPS data warps, each thread one float4
+// of a chunk per array, and two control warps (claims, books);
+// SP_LAMB_CTAS CTAs per SM; SP_LAMB_STAGES chunks of g, p, m, v staged in
+// shared memory by bulk copies (the loads in flight do not hold registers,
+// so one CTA of 16 data warps per SM streams at HBM speed); the rest of the
+// SM's shared memory is the u stash.
+#ifndef SP_LAMB_WARPS
+#define SP_LAMB_WARPS 16
 #endif
 #ifndef SP_LAMB_CTAS
-#define SP_LAMB_CTAS 3
+#define SP_LAMB_CTAS 1
 #endif
-#ifndef SP_LAMB_VEC
-#define SP_LAMB_VEC 2
+#ifndef SP_LAMB_STAGES
+#define SP_LAMB_STAGES 2
 #endif
-constexpr int kLambThreads = SP_LAMB_THREADS;
-constexpr int kLambCtasPerSm = SP_LAMB_CTAS;  // register budget 65536 / (threads * CTAs)
-constexpr int kLambVec = SP_LAMB_VEC;          // float4 per thread in flight per array
-#ifndef SP_LAMB_ITERS
-#define SP_LAMB_ITERS 1
-#endif
-// max chunk length: SP_LAMB_ITERS passes of the CTA
-constexpr int kLambTile = kLambThreads * 4 * kLambVec * SP_LAMB_ITERS;
+constexpr int kLambDataWarps = SP_LAMB_WARPS;
+constexpr int kLambDataThreads = kLambDataWarps * 32;
+constexpr int kLambThreads = kLambDataThreads + 64;
+constexpr int kLambCtasPerSm = SP_LAMB_CTAS;
+constexpr int kLambStages = SP_LAMB_STAGES;
+constexpr int kLambTile = kLambDataThreads * 4;  // max chunk length: one float4 per data thread
+// one stage: g (wire bytes or fp32, plus 16 bytes of slack for an aligned
+// superset of a wire range), p, m, v of the pass-1 chunk, and p of the
+// iteration's pass-2 chunk (an iteration without a pass-1 chunk puts the p
+// of up to four pass-2 chunks into the g, p, m, v areas instead)
+constexpr int kLambStageG = kLambDataThreads * 16 + 16;
+constexpr int kLambStageP2 = kLambStageG + 3 * kLambDataThreads * 16;
+constexpr int kLambStageBytes = kLambStageP2 + kLambDataThreads * 16;
 constexpr int kPad = 16384;         // wire/avg buffers padded to this multiple
 
 struct BarrierArgs {
@@ -195,6 +203,11 @@ __device__ __forceinline__ void st_v4(void* p, int4 v) {
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {

@@ -1,112 +1,184 @@
 // sp_lamb.cuh — the LAMB step of the round (K3 + K4) as one cooperative
-// persistent kernel: 1024 / kLambThreads CTAs per SM, chunks claimed
-// dynamically from per-window work queues.
+// persistent kernel: kLambCtasPerSm CTAs of kLambThreads per SM, chunks of
+// at most kLambTile elements claimed from one queue.
 //
 // LAMB needs every tensor's norms ||p||, ||u|| before any element of it can
 // be updated, so each element is touched twice: pass 1 (m' = b1 m + (1-b1) g,
 // v' = ..., u = m'^/(sqrt(v'^)+eps) + wd p, norm partials) and pass 2
 // (p' = p - lr * trust_t * u). Re-reading p, m', v' in pass 2 costs 12 B per
-// element of L2 traffic on top of pass 1's 24 + b, and on B200 the L2 slice
-// throughput (~6.3 KB/clk chip-wide, /opt/skills/guides/B300_MICROARCH.md
-// "LTS throughput cap") binds hits and misses alike: the round-1 kernel
-// moved 44 B/element through L2 at 6.35 TB/s.
+// element of L2 traffic on top of pass 1's 24 + b; the round-1 kernel moved
+// 44 B/element through L2 at 6.35 TB/s.
 //
-// Here pass 1 keeps u in shared memory (the "stash": the SM's shared memory
-// split over its CTAs, ~57 K floats per SM), so pass 2 re-reads only p (4 B,
-// L2-resident: pass 1 loads it with an evict_last hint) and writes p':
-// 24 + b + 8 B per element.
+// Loads. Pass 1's g, p, m, v of a chunk are fetched by bulk async copies
+// (cp.async.bulk, completion on an mbarrier) into one of kLambStages stages
+// in shared memory, issued kLambStages - 1 iterations ahead by one thread.
+// The bytes in flight then hold no registers and do not depend on the warp
+// count: one CTA of 16 warps per SM streams pass 1 at ~6 TB/s
+// (scripts/micro/tma_stream.cu, profiles/r02/tma_stream.txt), where
+// register-held loads need 32 warps per SM and every register of them.
 //
-// Replicated mode (every rank steps the whole vector). Tensors are packed
-// into windows that fit half of all stashes (~4.2 M elements on 148 SMs;
-// the largest ALBERT-large tensor has 4,194,304). A CTA runs
-//     pass1(w0) arrive(w0) | pass1(w1) arrive(w1) wait(w0) pass2(w0) |
-//     pass1(w2) arrive(w2) wait(w1) pass2(w1) | ... wait(last) pass2(last)
-// alternating the two stash halves, so the barrier of window w is
-// split-phase: its wait comes one window of work after its arrive. In pass 1
-// CTAs claim chunks from the window's queue (a static split left the
-// slowest SMs 1.7x behind the median, profiles/r02/lamb_trace.txt); a CTA
-// stashes u of its chunks while its half has room and lists the rest as
-// overflow, which pass 2 recomputes from p, m', v' (any CTA, claimed from
-// the overflow list). The CTA that finishes the last chunk of a tensor sums
-// the tensor's chunk partials and publishes lr * trust.
+// Stash. Pass 1 keeps u in a ring buffer in the rest of the CTA's shared
+// memory, so pass 2 re-reads only p (mostly an L2 hit: it was read in pass 1
+// shortly before) and writes p': 24 + b + 8 B per element.
 //
-// Sharded mode (ZeRO-1 style): one window, this rank's owned
-// range, stashed in the whole buffer. The last finisher of a tensor stores
-// this rank's (sum p^2, sum u^2) into slot [rank][t] of every rank's norm
-// table (NVLink stores); after the grid barrier CTA 0 runs the cross-rank
-// barrier, and pass 2 forms trust_t from the world slots in rank order and
-// stores p' into every rank's parameter vector.
+// Replicated mode (every rank steps the whole vector) streams: CTAs claim
+// chunks tensor by tensor (largest first) from one queue; a CTA puts u of
+// each chunk it claims into its ring and the chunk into a FIFO; a tensor's
+// norms are complete as soon as its last chunk is counted (the CTA that
+// counts it sums the chunk partials and publishes lr * trust), and from then
+// on the CTAs holding chunks of that tensor run their pass 2, one FIFO entry
+// per pass-1 chunk, interleaved with the pass-1 chunks of later tensors (the
+// entry's p loads are issued before the pass-1 math, which reads only shared
+// memory, and consumed after it). No grid-wide barrier: a chunk waits only
+// for its own tensor. A chunk for which the ring has no room is queued
+// without stash (u recomputed from p, m', v', which the same thread stored
+// in pass 1); only with the FIFO full does a chunk go to a global overflow
+// list, processed at the end by any CTA.
+//
+// Control never stalls the streaming warps on a global round trip. After the
+// one CTA barrier of an iteration, lane 0 of warp 0 ("claims") and of warp 1
+// ("books") do the bookkeeping, then join the next iteration:
+//   claims  fills the slot of iteration i + kLambStages and issues its bulk
+//           copies into the stage iteration i freed, for a chunk claimed two
+//           steps earlier whose descriptor it fetched with cp.async one step
+//           earlier; probes the ready word of the FIFO head's tensor (the
+//           result is used one step later);
+//   books   stores the chunk's norm partial and counts it for its tensor
+//           (the count is checked one step later, or at once for the CTA's
+//           last chunk), and completes a tensor whose count is full.
+// No fences on this path: partials and ready words carry the launch's tag
+// in the same 64-bit word as the value (single-copy atomic), so a reader
+// that sees the tag sees the value; readers of a partial spin on the tag.
+//
+// Sharded mode (ZeRO-1 style): the same loop over this
+// rank's owned range without pass 2 (it needs every rank's norms); then the
+// last CTA to arrive stores this rank's (sum p^2, sum u^2) of every tensor
+// into slot [rank][t] of every rank's norm table (NVLink stores), runs the
+// cross-rank barrier and releases the grid; pass 2 forms trust_t from the
+// world slots in rank order and stores p' into every rank's parameter
+// vector.
 //
 // Norms (deterministic, same bits on every replica and for any grid size):
 // per chunk, per-thread fp32 fmaf chains, warp xor tree, warps summed in
-// order -> one float2 partial per chunk; per tensor the chunk partials are
+// order -> one partial pair per chunk; per tensor the chunk partials are
 // summed in fp64 by one warp (lanes strided in chunk order, xor tree).
-// All barriers and queues are counters in global memory: the grid is
-// launched cooperatively (all CTAs co-resident) and the last CTA out resets
-// them (graph-replay safe).
+// Queues and counters live in global memory: the grid is launched
+// cooperatively (all CTAs co-resident) and the last CTA out resets them and
+// advances the tag (graph-replay safe).
 #pragma once
 
 #include "sp_kernels.cuh"
+#include "sp_ring.h"
 
 namespace sp {
 
-constexpr int kStashList = 32;  // stashed chunks a CTA remembers per window (more: overflow)
+constexpr int kFifo = 32;  // chunks a CTA holds for pass 2 at once (more: overflow)
+constexpr int kDrain = 4;  // pass-2 entries per iteration without a pass-1 chunk
+constexpr int kSlots = kLambStages + 1;  // iteration i uses slot i % kSlots
+constexpr int kCtlWarp = kLambDataWarps, kBooksWarp = kLambDataWarps + 1;
 
 struct LambPlan {
-  const Chunk* chunks;      // all chunks, window by window, in element order
-  const int2* wchunk;       // per window: chunks [x, y)
-  const int2* tchunk;       // per tensor: chunks [x, y) (empty: none on this rank)
-  float2* partial;          // per chunk (sum p^2, sum u^2)
-  int* ovf;                 // per window w: overflow chunk ids at [wchunk[w].x, ...)
-  // counters: [0, nwin) queue heads, [nwin, 2 nwin) overflow counts,
-  // [2 nwin, 3 nwin) overflow claims, [3 nwin, 4 nwin + 3) arrivals,
-  // [4 nwin + 3, 4 nwin + 3 + T) per-tensor finished chunks, then exited
-  int* cnt;
-  float* trust;             // per tensor (what sp_round_read(SP_BUF_TRUST) returns)
-  float* step_scale;        // per tensor: lr * trust
-  int nwin;
-  int half;                 // floats per stash half (sharded: one window over both halves)
+  const Chunk* chunks;            // claim order: tensor by tensor, largest first
+  int nchunks;
+  const int2* tchunk;             // per tensor: chunks [x, y) (empty: none on this rank)
+  unsigned long long* partial;    // per chunk: (sum p^2, tag), (sum u^2, tag)
+  int* ovf;                       // overflow chunk ids (recomputed at the end)
+  int* cnt;                       // counters (below)
+  float* trust;                   // per tensor (what sp_round_read(SP_BUF_TRUST) returns)
+  float* step_scale;              // per tensor: lr * trust
+  int cap;                        // stash floats per CTA
   int T;
   // sharded mode
   int shard;
-  double2* table[SP_MAX_RANKS];  // norm table of rank (rank + 1 + k) % world (self last)
-  const double2* my_table;       // this rank's [world][T]
+  double2* table[SP_MAX_RANKS];   // norm table of rank (rank + 1 + k) % world (self last)
+  const double2* my_table;        // this rank's [world][T]
   ParamPush push;
-  BarrierArgs bar;               // cross-rank barrier (flags, epoch, err)
-  unsigned long long* trace;     // SP_LAMB_TRACE builds: per-CTA globaltimer stamps
+  BarrierArgs bar;                // cross-rank barrier (flags, epoch, err)
+  unsigned long long* trace;      // SP_LAMB_TRACE builds: per-CTA globaltimer stamps
 
-  __device__ int* head(int w) const { return cnt + w; }
-  __device__ int* ovf_n(int w) const { return cnt + nwin + w; }
-  __device__ int* ovf_claim(int w) const { return cnt + 2 * nwin + w; }
-  __device__ int* arrive(int k) const { return cnt + 3 * nwin + k; }
-  __device__ int* done(int t) const { return cnt + 4 * nwin + 3 + t; }
-  __device__ int* exited() const { return cnt + 4 * nwin + 3 + T; }
-  __device__ int ncounters() const { return 4 * nwin + 4 + T; }
+  __device__ int* head() const { return cnt + 0; }
+  __device__ int* ovf_n() const { return cnt + 1; }
+  __device__ int* ovf_claim() const { return cnt + 2; }
+  __device__ int* arrive() const { return cnt + 3; }
+  __device__ int* release_flag() const { return cnt + 4; }
+  __device__ int* exited() const { return cnt + 5; }
+  __device__ unsigned* tag_word() const { return reinterpret_cast<unsigned*>(cnt + 6); }  // not reset
+  __device__ int* done(int t) const { return cnt + 8 + t; }
+  // per tensor: (lr * trust bits, tag); tagged, so never reset
+  __device__ unsigned long long* ready(int t) const {
+    return reinterpret_cast<unsigned long long*>(cnt + ((8 + T + 1) & ~1)) + t;
+  }
+  __device__ int nreset() const { return 8 + T; }
 };
 
+// host: ints of LambPlan::cnt
+inline size_t lamb_counter_ints(int T) { return (size_t)((8 + T + 1) & ~1) + 2 * (size_t)T; }
+
+// SP_LAMB_TRACE builds: per CTA kLambTraceStride words: [0, 64) globaltimer
+// stamps (LAMB_STAMP), then clock64 stamps of the first 128 iterations
+// (LAMB_ITER: 8 per iteration).
+constexpr int kLambTraceStride = 64 + 128 * 8;
 #ifdef SP_LAMB_TRACE
-#define LAMB_STAMP(k)                                                                         \
-  do {                                                                                        \
-    if (threadIdx.x == 0 && pl.trace) pl.trace[(size_t)blockIdx.x * 64 + (k)] = globaltimer(); \
+#define LAMB_STAMP(k)                                                                                      \
+  do {                                                                                                     \
+    if (threadIdx.x == 0 && pl.trace) pl.trace[(size_t)blockIdx.x * kLambTraceStride + (k)] = globaltimer(); \
+  } while (0)
+#define LAMB_ITER(it, j)                                                                              \
+  do {                                                                                                \
+    if (pl.trace && (it) < 128) pl.trace[(size_t)blockIdx.x * kLambTraceStride + 64 + (it) * 8 + (j)] = \
+        (unsigned long long)clock64();                                                               \
   } while (0)
 #else
 #define LAMB_STAMP(k) \
   do {                \
   } while (0)
+#define LAMB_ITER(it, j) \
+  do {                   \
+  } while (0)
 #endif
 
-__device__ __forceinline__ void grid_arrive(int* c) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(c, 1);
-  }
+// ------------------------------------------------------------ primitives
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
-__device__ __forceinline__ void grid_wait(const int* c, int target) {
-  if (threadIdx.x == 0)
-    while (ld_acquire_gpu(reinterpret_cast<const unsigned*>(c)) < (unsigned)target) __nanosleep(32);
-  __syncthreads();
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+// arrive (count 1) and expect `bytes` of bulk copies on the current phase
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned ok = 0;
+  while (!ok)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ unsigned long long tagged(float x, unsigned tag) {
+  return ((unsigned long long)tag << 32) | (unsigned long long)__float_as_uint(x);
 }
 
 __device__ __forceinline__ float trust_of(double x, double y) {
@@ -114,19 +186,68 @@ __device__ __forceinline__ float trust_of(double x, double y) {
   return (r1 > 0.0 && r2 > 0.0) ? (float)(r1 / r2) : 1.0f;
 }
 
+__device__ __forceinline__ void publish_partial(const LambPlan& pl, int item, float x, float y, unsigned tag) {
+  pl.partial[2 * (size_t)item] = tagged(x, tag);
+  pl.partial[2 * (size_t)item + 1] = tagged(y, tag);
+}
+
+// One partial of this launch (spins until the word carries the tag).
+__device__ __forceinline__ float partial_word(const unsigned long long* w, unsigned long long v, unsigned tag) {
+  while ((unsigned)(v >> 32) != tag) v = ld_relaxed_u64(w);
+  return __uint_as_float((unsigned)v);
+}
+
+// fp64 sums of tensor t's chunk partials by the calling warp: lanes strided
+// in chunk order with 8 pairs in flight each, then an xor tree (both lanes
+// of every pair add the same two operands, so every lane ends with the same
+// bits). Depends only on the chunk table.
+__device__ __forceinline__ double2 tensor_sums(const LambPlan& pl, int t, unsigned tag) {
+  const int lane = threadIdx.x & 31;
+  const int2 r = pl.tchunk[t];
+  double x = 0.0, y = 0.0;
+  for (int q0 = r.x + lane; q0 < r.y; q0 += 8 * 32) {
+    unsigned long long v[8][2];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int q = q0 + 32 * j;
+      v[j][0] = v[j][1] = (unsigned long long)tag << 32;  // absent: 0.0f with the tag
+      if (q < r.y) {
+        v[j][0] = ld_relaxed_u64(pl.partial + 2 * (size_t)q);
+        v[j][1] = ld_relaxed_u64(pl.partial + 2 * (size_t)q + 1);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int q = q0 + 32 * j;
+      x += (double)partial_word(pl.partial + 2 * (size_t)q, v[j][0], tag);
+      y += (double)partial_word(pl.partial + 2 * (size_t)q + 1, v[j][1], tag);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    x += __shfl_xor_sync(0xffffffffu, x, o);
+    y += __shfl_xor_sync(0xffffffffu, y, o);
+  }
+  return make_double2(x, y);
+}
+
 // --------------------------------------------------------------- pass 1
+// Thread t handles body vector t of a chunk (a chunk is at most one tile)
+// and, for the unaligned edges, head element t (t < head) or tail element
+// t - 32 (32 <= t < 32 + tail). Pass 2 uses the same mapping, so each thread
+// reads back exactly the stash words (and, for a chunk without stash, the
+// m', v') it wrote.
+
 template <int W, bool FP>
 __device__ __forceinline__ void p1_vec(const LambArgs& a, const LambScalars& s, int64_t i, float4 g,
-                                       float4 p, float4 m, float4 v, float* st, uint64_t mv_pol,
-                                       float& pp, float& uu) {
+                                       float4 p, float4 m, float4 v, float* st, float& pp, float& uu) {
   float4 u;
   lamb_moments(a, s, g.x, p.x, m.x, v.x, u.x);
   lamb_moments(a, s, g.y, p.y, m.y, v.y, u.y);
   lamb_moments(a, s, g.z, p.z, m.z, v.z, u.z);
   lamb_moments(a, s, g.w, p.w, m.w, v.w, u.w);
-  // m', v' are re-read in pass 2 only for chunks that are not stashed
-  st_hint_f4(a.m + i, m, mv_pol);
-  st_hint_f4(a.v + i, v, mv_pol);
+  *reinterpret_cast<float4*>(a.m + i) = m;
+  *reinterpret_cast<float4*>(a.v + i) = v;
   if (st) *reinterpret_cast<float4*>(st) = u;
   pp = __fmaf_rn(p.x, p.x, pp); pp = __fmaf_rn(p.y, p.y, pp);
   pp = __fmaf_rn(p.z, p.z, pp); pp = __fmaf_rn(p.w, p.w, pp);
@@ -134,204 +255,42 @@ __device__ __forceinline__ void p1_vec(const LambArgs& a, const LambScalars& s, 
   uu = __fmaf_rn(u.z, u.z, uu); uu = __fmaf_rn(u.w, u.w, uu);
 }
 
-// Thread t handles body vectors t, t + kLambThreads, ... and, for the
-// unaligned edges, head element t (t < head) or tail element t - 32
-// (32 <= t < 32 + tail). Pass 2 uses the same mapping, so each thread reads
-// back exactly the stash words it wrote. st: the chunk's stash (indexed by
-// element - c.start), or nullptr.
+// Pass 1 of a staged chunk. st: the chunk's stash (indexed by element -
+// c.start), or nullptr.
 template <int W, bool FP>
-__device__ __forceinline__ void p1_chunk(const LambArgs& a, const LambScalars& s, const Chunk& c,
-                                         float* st, float& pp, float& uu) {
+__device__ __forceinline__ void p1_staged(const LambArgs& a, const LambScalars& s, const Chunk& c,
+                                          const unsigned char* stg, int goff, float* st, float& pp, float& uu) {
   const ChunkSplit sp = split_chunk(c.start, c.len);
   const int t = threadIdx.x;
+  const int64_t b0 = sp.start + sp.head;
   int64_t si = -1;
   if (t < sp.head) si = sp.start + t;
-  else if (t >= 32 && t - 32 < sp.tail) si = sp.start + sp.head + 4 * (int64_t)sp.nbody4 + (t - 32);
+  else if (t >= 32 && t - 32 < sp.tail) si = b0 + 4 * (int64_t)sp.nbody4 + (t - 32);
   if (si >= 0) {
-    const float g = load_grad1<W, FP>(a, si);
-    const float p = a.p[si];
-    float m = a.m[si], v = a.v[si], u;
-    lamb_moments(a, s, g, p, m, v, u);
-    a.m[si] = m;
-    a.v[si] = v;
-    if (st) st[si - c.start] = u;
-    pp = __fmaf_rn(p, p, pp);
-    uu = __fmaf_rn(u, u, uu);
+    const float gs = load_grad1<W, FP>(a, si);
+    const float ps = a.p[si];
+    float ms = a.m[si], vs = a.v[si], us;
+    lamb_moments(a, s, gs, ps, ms, vs, us);
+    a.m[si] = ms;
+    a.v[si] = vs;
+    if (st) st[si - c.start] = us;
+    pp = __fmaf_rn(ps, ps, pp);
+    uu = __fmaf_rn(us, us, uu);
   }
-  const int64_t b0 = sp.start + sp.head;
-  const uint64_t p_pol = policy_evict_last();  // re-read by pass 2
-  const uint64_t mv_pol = st ? policy_evict_first() : p_pol;
-  int k = t;
-  // kLambVec vectors per thread: every load of the group issued before use
-  for (; k + (kLambVec - 1) * kLambThreads < sp.nbody4; k += kLambVec * kLambThreads) {
-    GradRaw g[kLambVec];
-    float4 p[kLambVec], m[kLambVec], v[kLambVec];
-#pragma unroll
-    for (int j = 0; j < kLambVec; ++j) g[j] = grad_load<W, FP>(a, b0 + 4 * (int64_t)(k + j * kLambThreads));
-#pragma unroll
-    for (int j = 0; j < kLambVec; ++j) p[j] = ld_hint_f4(a.p + b0 + 4 * (int64_t)(k + j * kLambThreads), p_pol);
-#pragma unroll
-    for (int j = 0; j < kLambVec; ++j) m[j] = ld_hint_f4(a.m + b0 + 4 * (int64_t)(k + j * kLambThreads), mv_pol);
-#pragma unroll
-    for (int j = 0; j < kLambVec; ++j) v[j] = ld_hint_f4(a.v + b0 + 4 * (int64_t)(k + j * kLambThreads), mv_pol);
-#pragma unroll
-    for (int j = 0; j < kLambVec; ++j) {
-      const int64_t i = b0 + 4 * (int64_t)(k + j * kLambThreads);
-      p1_vec<W, FP>(a, s, i, grad_finish<W, FP>(a, i, g[j]), p[j], m[j], v[j],
-                    st ? st + (i - c.start) : nullptr, mv_pol, pp, uu);
+  if (t < sp.nbody4) {
+    const int64_t i = b0 + 4 * (int64_t)t;
+    GradRaw g;
+    if constexpr (FP || W == SP_WIRE_FP32) {
+      g.f = reinterpret_cast<const float4*>(stg)[t];
+    } else if constexpr (W == SP_WIRE_FP16) {
+      g.h = *reinterpret_cast<const uint2*>(stg + goff + 8 * t);
+    } else {
+      g.q = *reinterpret_cast<const uint32_t*>(stg + goff + 4 * t);
+      g.s = a.avg_scale[i >> a.qshift];
     }
-  }
-  for (; k < sp.nbody4; k += kLambThreads) {
-    const int64_t i = b0 + 4 * (int64_t)k;
-    const GradRaw g = grad_load<W, FP>(a, i);
-    const float4 p = ld_hint_f4(a.p + i, p_pol);
-    const float4 m = ld_hint_f4(a.m + i, mv_pol), v = ld_hint_f4(a.v + i, mv_pol);
-    p1_vec<W, FP>(a, s, i, grad_finish<W, FP>(a, i, g), p, m, v, st ? st + (i - c.start) : nullptr, mv_pol, pp, uu);
-  }
-}
-
-struct LambShared {
-  float red_p[2][kLambThreads / 32], red_u[2][kLambThreads / 32];  // by chunk parity
-  int2 list[2][kStashList];  // per stash half: (chunk, stash offset) of the stashed chunks
-  int nlist[2];
-  Chunk desc[2];  // descriptors of this and the next chunk (by parity)
-  int idx[2];     // their indices in the window
-  int k;
-  float neg;
-  int t_neg;
-  unsigned long long epoch;
-};
-
-// Tensor t's last chunk partial is published: warp 0 sums the tensor's
-// chunk partials in fp64 (lanes strided in chunk order, then an xor tree;
-// every lane ends with the same bits) and publishes lr * trust (replicated)
-// or this rank's pair into every rank's norm table (sharded).
-__device__ __forceinline__ void finish_tensor(const LambPlan& pl, const LambScalars& s, int t) {
-  const int lane = threadIdx.x & 31;
-  __threadfence();  // acquire: the other CTAs' partials precede their counts
-  const int2 r = pl.tchunk[t];
-  double x = 0.0, y = 0.0;
-  for (int q = r.x + lane; q < r.y; q += 32) {
-    const float2 v = __ldcg(pl.partial + q);
-    x += (double)v.x;
-    y += (double)v.y;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    x += __shfl_xor_sync(0xffffffffu, x, o);
-    y += __shfl_xor_sync(0xffffffffu, y, o);
-  }
-  if (pl.shard) {
-    if (lane < pl.push.ndst) {
-      pl.table[lane][(size_t)pl.bar.rank * pl.T + t] = make_double2(x, y);
-      __threadfence_system();
-    }
-  } else if (lane == 0) {
-    const float tr = trust_of(x, y);
-    pl.trust[t] = tr;
-    pl.step_scale[t] = __fmul_rn(s.lr, tr);
-  }
-}
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem) : "memory");
-}
-
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-}
-
-// Pass 1 of window w: claim chunks from the window's queue until it is
-// empty. Per chunk: the moments, u into this CTA's stash half while it has
-// room (else the chunk goes to the window's overflow list) and the chunk
-// partial. One CTA barrier per chunk, and nothing on a chunk's critical
-// path waits for a memory round trip: thread 0 claims two chunks ahead and
-// copies the next chunk's descriptor into shared memory (cp.async) while
-// this chunk runs, and the count of finished chunks of a chunk's tensor
-// (whose last finisher completes the tensor's norms, finish_tensor) is
-// examined one chunk later.
-template <int W, bool FP>
-__device__ void pass1(const LambArgs& a, const LambScalars& s, const LambPlan& pl, int w, int h,
-                      float* stash, int cap, LambShared& sh) {
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int2 wr = pl.wchunk[w];
-  const int nw = wr.y - wr.x;
-  int used = 0, nlist = 0;  // this half's stash use: the same values in every thread
-  int c1 = 0;               // thread 0: index of the next chunk (claimed one chunk ago)
-  int pend_t = -1, pend_old = 0, pend_n = 0;  // thread 0: the previous chunk's tensor count
-  if (tid == 0) {
-    const int c0 = atomicAdd(pl.head(w), 1);
-    sh.idx[0] = c0;
-    if (c0 < nw) sh.desc[0] = pl.chunks[wr.x + c0];
-    c1 = atomicAdd(pl.head(w), 1);
-  }
-  __syncthreads();
-  int parity = 0;
-  for (;;) {
-    const int item = sh.idx[parity];
-    if (item >= nw) break;
-    const Chunk c = sh.desc[parity];
-    if (tid == 0) {
-      if (c1 < nw) {  // the next chunk's descriptor, in flight while this chunk runs
-        cp_async16(&sh.desc[parity ^ 1], pl.chunks + wr.x + c1);
-        cp_async16(reinterpret_cast<char*>(&sh.desc[parity ^ 1]) + 16,
-                   reinterpret_cast<const char*>(pl.chunks + wr.x + c1) + 16);
-      }
-    }
-    const int c2 = tid == 0 ? atomicAdd(pl.head(w), 1) : 0;  // claim after next
-    const int ci = wr.x + item;
-    const int off = used + (int)((((c.start - used) % 4) + 4) % 4);  // off = start (mod 4)
-    const bool stashed = off + c.len <= cap && nlist < kStashList;
-    float pp = 0.0f, uu = 0.0f;
-    p1_chunk<W, FP>(a, s, c, stashed ? stash + off : nullptr, pp, uu);
-    pp = warp_sum(pp);
-    uu = warp_sum(uu);
-    if (lane == 0) {
-      sh.red_p[parity][wid] = pp;
-      sh.red_u[parity][wid] = uu;
-    }
-    if (tid == 0) {
-      cp_async_wait_all();
-      sh.idx[parity ^ 1] = c1;
-      c1 = c2;
-    }
-    __syncthreads();
-    int last_t = -1;
-    if (tid == 0) {
-      float x = 0.0f, y = 0.0f;
-#pragma unroll
-      for (int q = 0; q < kLambThreads / 32; ++q) {
-        x += sh.red_p[parity][q];
-        y += sh.red_u[parity][q];
-      }
-      pl.partial[ci] = make_float2(x, y);
-      if (stashed) sh.list[h][nlist] = make_int2(ci, off);
-      else pl.ovf[wr.x + atomicAdd(pl.ovf_n(w), 1)] = ci;
-      if (pend_t >= 0 && pend_old == pend_n - 1) last_t = pend_t;
-      __threadfence();  // release: the partial precedes the count
-      pend_old = atomicAdd(pl.done(c.tensor), 1);
-      pend_t = c.tensor;
-      pend_n = c.tchunks;
-    }
-    if (stashed) {
-      used = off + c.len;
-      ++nlist;
-    }
-    if (wid == 0) {
-      last_t = __shfl_sync(0xffffffffu, last_t, 0);
-      if (last_t >= 0) finish_tensor(pl, s, last_t);
-    }
-    parity ^= 1;
-  }
-  int last_t = -1;
-  if (tid == 0) {
-    if (pend_t >= 0 && pend_old == pend_n - 1) last_t = pend_t;
-    sh.nlist[h] = nlist;
-  }
-  if (wid == 0) {
-    last_t = __shfl_sync(0xffffffffu, last_t, 0);
-    if (last_t >= 0) finish_tensor(pl, s, last_t);
+    const float4* pmv = reinterpret_cast<const float4*>(stg + kLambStageG);
+    p1_vec<W, FP>(a, s, i, grad_finish<W, FP>(a, i, g), pmv[t], pmv[kLambDataThreads + t],
+                  pmv[2 * kLambDataThreads + t], st ? st + (i - c.start) : nullptr, pp, uu);
   }
 }
 
@@ -347,195 +306,551 @@ __device__ __forceinline__ float4 dir4(const LambArgs& a, const LambScalars& s, 
                      lamb_dir(a, s, p.z, m.z, v.z), lamb_dir(a, s, p.w, m.w, v.w));
 }
 
-__device__ __forceinline__ void p2_store(const LambArgs& a, const ParamPush* push, int64_t i, float4 q,
-                                         uint64_t pol) {
-  if (push) {
-    const int4 o = make_int4(__float_as_int(q.x), __float_as_int(q.y), __float_as_int(q.z),
-                             __float_as_int(q.w));
-    for (int j = 0; j < push->ndst; ++j) st_v4(push->dst[j] + i, o);
-  } else {
-    st_hint_f4(a.p + i, q, pol);
+// m', v' of a pass-2 chunk without stash, issued ahead of their use.
+struct P2Regs {
+  float4 m, v;
+};
+
+__device__ __forceinline__ void p2_load_mv(const LambArgs& a, long long start, int len, P2Regs& r) {
+  const ChunkSplit sp = split_chunk(start, len);
+  const int t = threadIdx.x;
+  if (t < sp.nbody4) {
+    const int64_t i = sp.start + sp.head + 4 * (int64_t)t;
+    r.m = *reinterpret_cast<const float4*>(a.m + i);
+    r.v = *reinterpret_cast<const float4*>(a.v + i);
+  }
+}
+
+// Pass 2 of a chunk whose body p is staged at ps (replicated: p' overwrites
+// p). u from the stash, or recomputed from m', v' (mv: already loaded).
+__device__ __forceinline__ void p2_staged(const LambArgs& a, const LambScalars& s, long long start, int len,
+                                          const float4* ps, const float* st, float neg, const P2Regs* mv) {
+  const ChunkSplit sp = split_chunk(start, len);
+  const int t = threadIdx.x;
+  const int64_t b0 = sp.start + sp.head;
+  int64_t si = -1;
+  if (t < sp.head) si = sp.start + t;
+  else if (t >= 32 && t - 32 < sp.tail) si = b0 + 4 * (int64_t)sp.nbody4 + (t - 32);
+  if (si >= 0) {
+    const float p = a.p[si];
+    const float u = st ? st[si - start] : lamb_dir(a, s, p, a.m[si], a.v[si]);
+    a.p[si] = __fmaf_rn(neg, u, p);
+  }
+  if (t < sp.nbody4) {
+    const int64_t i = b0 + 4 * (int64_t)t;
+    const float4 p = ps[t];
+    float4 u;
+    if (st) u = *reinterpret_cast<const float4*>(st + (i - start));
+    else if (mv) u = dir4(a, s, p, mv->m, mv->v);
+    else u = dir4(a, s, p, *reinterpret_cast<const float4*>(a.m + i), *reinterpret_cast<const float4*>(a.v + i));
+    *reinterpret_cast<float4*>(a.p + i) = p2_vec(neg, p, u);
   }
 }
 
 // p' = p - (lr * trust) * u, u from the stash or recomputed (bit-identical:
-// lamb_dir is pass 1's u expression on the stored m', v'). Replicated: p'
+// lamb_dir is pass 1's u expression on the stored m', v'), loads issued by
+// the thread (sharded pass 2 and the overflow chunks). Replicated: p'
 // overwrites p. Sharded: p' goes to every rank's copy, the local one last.
-__device__ __forceinline__ void p2_chunk(const LambArgs& a, const LambScalars& s, const Chunk& c,
+__device__ __forceinline__ void p2_chunk(const LambArgs& a, const LambScalars& s, long long start, int len,
                                          const float* st, float neg, const ParamPush* push) {
-  const ChunkSplit sp = split_chunk(c.start, c.len);
+  const ChunkSplit sp = split_chunk(start, len);
   const int t = threadIdx.x;
-  const uint64_t drop = policy_evict_first();
+  const int64_t b0 = sp.start + sp.head;
   int64_t si = -1;
   if (t < sp.head) si = sp.start + t;
-  else if (t >= 32 && t - 32 < sp.tail) si = sp.start + sp.head + 4 * (int64_t)sp.nbody4 + (t - 32);
+  else if (t >= 32 && t - 32 < sp.tail) si = b0 + 4 * (int64_t)sp.nbody4 + (t - 32);
   if (si >= 0) {
-    const float p = a.p[si];
-    const float u = st ? st[si - c.start] : lamb_dir(a, s, p, a.m[si], a.v[si]);
-    const float q = __fmaf_rn(neg, u, p);
+    const float ps = a.p[si];
+    const float us = st ? st[si - start] : lamb_dir(a, s, ps, a.m[si], a.v[si]);
+    const float q = __fmaf_rn(neg, us, ps);
     if (push)
       for (int k = 0; k < push->ndst; ++k) push->dst[k][si] = q;
     else
       a.p[si] = q;
   }
-  const int64_t b0 = sp.start + sp.head;
-  int k = t;
-  for (; k + kLambThreads < sp.nbody4; k += 2 * kLambThreads) {
-    const int64_t i0 = b0 + 4 * (int64_t)k, i1 = i0 + 4 * (int64_t)kLambThreads;
-    const float4 p0 = ld_hint_f4(a.p + i0, drop), p1 = ld_hint_f4(a.p + i1, drop);
-    float4 u0, u1;
-    if (st) {
-      u0 = *reinterpret_cast<const float4*>(st + (i0 - c.start));
-      u1 = *reinterpret_cast<const float4*>(st + (i1 - c.start));
+  if (t < sp.nbody4) {
+    const int64_t i = b0 + 4 * (int64_t)t;
+    const float4 p = *reinterpret_cast<const float4*>(a.p + i);
+    const float4 u = st ? *reinterpret_cast<const float4*>(st + (i - start))
+                        : dir4(a, s, p, *reinterpret_cast<const float4*>(a.m + i),
+                               *reinterpret_cast<const float4*>(a.v + i));
+    const float4 q = p2_vec(neg, p, u);
+    if (push) {
+      const int4 o = make_int4(__float_as_int(q.x), __float_as_int(q.y), __float_as_int(q.z),
+                               __float_as_int(q.w));
+      for (int j = 0; j < push->ndst; ++j) st_v4(push->dst[j] + i, o);
     } else {
-      const float4 m0 = ld_hint_f4(a.m + i0, drop), m1 = ld_hint_f4(a.m + i1, drop);
-      const float4 v0 = ld_hint_f4(a.v + i0, drop), v1 = ld_hint_f4(a.v + i1, drop);
-      u0 = dir4(a, s, p0, m0, v0);
-      u1 = dir4(a, s, p1, m1, v1);
+      *reinterpret_cast<float4*>(a.p + i) = q;
     }
-    p2_store(a, push, i0, p2_vec(neg, p0, u0), drop);
-    p2_store(a, push, i1, p2_vec(neg, p1, u1), drop);
-  }
-  if (k < sp.nbody4) {
-    const int64_t i = b0 + 4 * (int64_t)k;
-    const float4 p = ld_hint_f4(a.p + i, drop);
-    const float4 u = st ? *reinterpret_cast<const float4*>(st + (i - c.start))
-                        : dir4(a, s, p, ld_hint_f4(a.m + i, drop), ld_hint_f4(a.v + i, drop));
-    p2_store(a, push, i, p2_vec(neg, p, u), drop);
   }
 }
 
-// -lr * trust of tensor t for pass 2 (uniform; cached in sh.neg).
-__device__ __forceinline__ float neg_scale(const LambPlan& pl, const LambScalars& s, int t,
-                                           LambShared& sh) {
-  if (t != sh.t_neg) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      if (pl.shard) {
-        double x = 0.0, y = 0.0;
-        for (int k = 0; k < pl.bar.world; ++k) {
-          const double2 q = __ldcg(pl.my_table + (size_t)k * pl.T + t);
-          x += q.x;
-          y += q.y;
-        }
-        sh.neg = -__fmul_rn(s.lr, trust_of(x, y));
-      } else {
-        sh.neg = -__ldcg(pl.step_scale + t);
-      }
-      sh.t_neg = t;
-    }
-    __syncthreads();
+// -lr * trust of tensor t for the overflow and sharded pass 2 (the same bits
+// everywhere: replicated, the published lr * trust; sharded, the world's
+// pairs summed in rank order).
+__device__ __forceinline__ float neg_of(const LambPlan& pl, const LambScalars& s, int t) {
+  if (!pl.shard) return -__ldcg(pl.step_scale + t);
+  double x = 0.0, y = 0.0;
+  for (int k = 0; k < pl.bar.world; ++k) {
+    const double2 q = __ldcg(pl.my_table + (size_t)k * pl.T + t);
+    x += q.x;
+    y += q.y;
   }
-  return sh.neg;
+  return -__fmul_rn(s.lr, trust_of(x, y));
 }
 
-// Pass 2 of window w: this CTA's stashed chunks, then overflow chunks
-// claimed from the window's list (complete: every CTA has passed pass 1).
-__device__ void pass2(const LambArgs& a, const LambScalars& s, const LambPlan& pl, int w, int h,
-                      const float* stash, LambShared& sh) {
+// Overflow chunks (no FIFO room), recomputed from p, m', v': claimed by any
+// CTA once pass 1 is complete everywhere.
+__device__ void overflow_pass2(const LambArgs& a, const LambScalars& s, const LambPlan& pl, int* s_k) {
   const ParamPush* push = pl.shard ? &pl.push : nullptr;
-  const int n = sh.nlist[h];
-  for (int k = 0; k < n; ++k) {
-    const int2 e = sh.list[h][k];
-    const Chunk c = pl.chunks[e.x];
-    p2_chunk(a, s, c, stash + e.y, neg_scale(pl, s, c.tensor, sh), push);
-  }
-  const int2 wr = pl.wchunk[w];
-  const int novf = __ldcg(pl.ovf_n(w));
+  const int novf = __ldcg(pl.ovf_n());
+  if (novf == 0) return;
   for (;;) {
     __syncthreads();
-    if (threadIdx.x == 0) sh.k = atomicAdd(pl.ovf_claim(w), 1);
+    if (threadIdx.x == 0) *s_k = atomicAdd(pl.ovf_claim(), 1);
     __syncthreads();
-    const int k = sh.k;
+    const int k = *s_k;
     if (k >= novf) break;
-    const Chunk c = pl.chunks[__ldcg(pl.ovf + wr.x + k)];
-    p2_chunk(a, s, c, nullptr, neg_scale(pl, s, c.tensor, sh), push);
+    const Chunk c = pl.chunks[__ldcg(pl.ovf + k)];
+    if (threadIdx.x < kLambDataThreads) p2_chunk(a, s, c.start, c.len, nullptr, neg_of(pl, s, c.tensor), push);
   }
-  __syncthreads();  // the next pass 1 reuses this stash half and list
+}
+
+// ------------------------------------------------------------ the stream
+struct FifoEntry {
+  long long start;
+  int len;
+  int off;     // stash offset of element `start` (float index, = start mod 4); -1: recompute
+  int tensor;
+  int pad;
+};
+
+// Claims lane state, in registers (its step is a chain of dependent
+// updates; in shared memory each would cost a load round trip).
+struct Ctl {
+  int fhead, fnext, ftail;  // FIFO: oldest entry, next to hand to pass 2, one past the newest
+  Ring ring;                // the stash ring (sp_ring.h)
+  int ready_t;              // last tensor seen ready (-1: none)
+  float ready_neg;          // its -lr * trust
+  int probe_t;              // tensor whose ready word is in flight (-1: none)
+  int pdesc;                // chunk whose descriptor is in flight to `desc` (>= nchunks: none)
+  int claims_done;          // the queue is exhausted for this CTA
+};
+
+// Books lane state, in registers.
+struct Books {
+  int t, n;      // tensor (and its chunk count) of the count in flight
+  int pending;   // a count in flight, to check next step
+  int done;      // the count (an atomic's result, in flight)
+  int arrived;   // counted in pl.arrive() (every partial of this CTA out)
+  int novf;      // chunks this CTA could not stash (trace builds report it)
+};
+
+struct StreamShared {
+  unsigned long long full[kLambStages];  // stage mbarriers: bulk copies landed
+  float red_p[kSlots][kLambDataWarps], red_u[kSlots][kLambDataWarps];
+  Chunk desc[kSlots];            // pass-1 chunk of the iteration
+  int idx[kSlots];               // its index (>= nchunks: none)
+  int off[kSlots];               // its stash offset (-1: recompute, -2: global overflow)
+  int goff[kSlots];              // its first body gradient in the stage's g area
+  FifoEntry e2[kSlots][kDrain];  // pass-2 entries of the iteration
+  float neg2[kSlots][kDrain];    // their -lr * trust
+  int n2[kSlots];
+  int stop[kSlots];              // 1: nothing left for this CTA
+  FifoEntry fifo[kFifo];
+  Chunk pdesc;                   // descriptor prefetched by cp.async
+  int nfifo;                     // FIFO entries of the loop (sharded pass 2)
+  int k, flag;
+  unsigned long long epoch;
+};
+
+// Stage offset of pass-2 entry j's p: beside a pass-1 chunk the p2 area;
+// else the g, p, m, v areas.
+__device__ __forceinline__ int p2_area(bool p1, int j) {
+  return p1 ? kLambStageP2 : (j == 0 ? 0 : kLambStageG + (j - 1) * kLambDataThreads * 16);
+}
+
+// Claims lane: chunk c (descriptor ch; >= nchunks: none) into slot q with
+// its pass 2 queued.
+__device__ __forceinline__ void stream_fill(const LambPlan& pl, Ctl& k, int q, int c, const Chunk& ch,
+                                            StreamShared& sh) {
+  sh.idx[q] = c;
+  if (c >= pl.nchunks) return;
+  sh.desc[q] = ch;
+  int off = -2;
+  if (k.ftail - k.fhead < kFifo) {
+    off = ring_alloc(k.ring, pl.cap, ch.start, ch.len);
+    if (off >= 0) ++k.ring.live;
+    FifoEntry& e = sh.fifo[k.ftail % kFifo];
+    e.start = ch.start;
+    e.len = ch.len;
+    e.off = off;
+    e.tensor = ch.tensor;
+    ++k.ftail;
+  }
+  sh.off[q] = off;
+}
+
+// Claims lane: the bulk copies of slot q into stage `stage` (an empty slot
+// only arrives, keeping the stage's phases in step with the iterations):
+// the pass-1 chunk's body g, p, m, v, and the p of the slot's pass-2
+// entries. Wire formats narrower than 16 B per vector are fetched as an
+// aligned superset; sh.goff[q] is the offset of the chunk's first body
+// gradient in the g area.
+template <int W, bool FP>
+__device__ __forceinline__ void stage_issue(const LambArgs& a, const LambPlan& pl, StreamShared& sh, int q,
+                                            int stage, unsigned char* stages) {
+  unsigned char* stg = stages + (size_t)stage * kLambStageBytes;
+  unsigned long long* bar = &sh.full[stage];
+  const bool p1 = sh.idx[q] < pl.nchunks;
+  unsigned total = 0, nb = 0, gbytes = 0;
+  int64_t b0 = 0;
+  const char* gsrc = nullptr;
+  if (p1) {
+    const ChunkSplit sp = split_chunk(sh.desc[q].start, sh.desc[q].len);
+    b0 = sp.start + sp.head;
+    nb = (unsigned)sp.nbody4;
+    int goff = 0;
+    if constexpr (FP) {
+      gsrc = reinterpret_cast<const char*>(a.g32 + b0);
+      gbytes = 16 * nb;
+    } else if constexpr (W == SP_WIRE_FP32) {
+      gsrc = reinterpret_cast<const char*>(static_cast<const float*>(a.avg) + b0);
+      gbytes = 16 * nb;
+    } else {
+      constexpr int wb = W == SP_WIRE_FP16 ? 2 : 1;  // wire bytes per element
+      const int64_t lo = (wb * b0) & ~(int64_t)15, hi = (wb * (b0 + 4 * (int64_t)nb) + 15) & ~(int64_t)15;
+      gsrc = static_cast<const char*>(a.avg) + lo;
+      gbytes = nb ? (unsigned)(hi - lo) : 0;
+      goff = (int)(wb * b0 - lo);
+    }
+    sh.goff[q] = goff;
+    if (nb) total += gbytes + 48 * nb;
+  }
+  const int n2 = sh.n2[q];
+  for (int j = 0; j < n2; ++j) total += 16 * (unsigned)split_chunk(sh.e2[q][j].start, sh.e2[q][j].len).nbody4;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  mbar_arrive_tx(bar, total);
+  if (nb) {
+    bulk_g2s(stg, gsrc, gbytes, bar);
+    bulk_g2s(stg + kLambStageG, a.p + b0, 16 * nb, bar);
+    bulk_g2s(stg + kLambStageG + kLambDataThreads * 16, a.m + b0, 16 * nb, bar);
+    bulk_g2s(stg + kLambStageG + 2 * kLambDataThreads * 16, a.v + b0, 16 * nb, bar);
+  }
+  for (int j = 0; j < n2; ++j) {
+    const ChunkSplit sp = split_chunk(sh.e2[q][j].start, sh.e2[q][j].len);
+    if (sp.nbody4)
+      bulk_g2s(stg + p2_area(p1, j), a.p + sp.start + sp.head, 16 * (unsigned)sp.nbody4, bar);
+  }
+}
+
+// Books warp, one step: check last step's count (every chunk of its tensor
+// counted: sum the partials, publish trust and the ready word), then
+// publish this iteration's partial and count it (the count is checked next
+// step). With no chunk: every count of this CTA is resolved, so it arrives.
+__device__ __forceinline__ void books_step(const LambPlan& pl, const LambScalars& s, StreamShared& sh,
+                                           unsigned tag, int slot, bool have1, int item, Books& k) {
+  const int lane = threadIdx.x & 31;
+  int last = -1;
+  if (lane == 0 && k.pending) {
+    if (k.done == k.n - 1) last = k.t;
+    k.pending = 0;
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (last >= 0) {
+    const double2 t2 = tensor_sums(pl, last, tag);
+    if (lane == 0) {
+      const float tr = trust_of(t2.x, t2.y);
+      const float sc = __fmul_rn(s.lr, tr);
+      pl.trust[last] = tr;
+      pl.step_scale[last] = sc;
+      *pl.ready(last) = tagged(sc, tag);
+    }
+  }
+  if (lane != 0) return;
+  if (have1) {
+    const Chunk& c = sh.desc[slot];
+    float x = 0.0f, y = 0.0f;
+#pragma unroll
+    for (int w = 0; w < kLambDataWarps; ++w) {
+      x += sh.red_p[slot][w];
+      y += sh.red_u[slot][w];
+    }
+    publish_partial(pl, item, x, y, tag);
+    if (sh.off[slot] < 0) ++k.novf;
+    if (sh.off[slot] == -2) pl.ovf[atomicAdd(pl.ovf_n(), 1)] = item;
+    if (!pl.shard) {
+      k.done = atomicAdd(pl.done(c.tensor), 1);
+      k.t = c.tensor;
+      k.n = c.tchunks;
+      k.pending = 1;
+    }
+  } else if (!k.arrived && !pl.shard) {  // every write of this CTA's pass 1 is out
+    __threadfence();
+    atomicAdd(pl.arrive(), 1);
+    k.arrived = 1;
+#ifdef SP_LAMB_TRACE
+    if (pl.trace) {
+      pl.trace[(size_t)blockIdx.x * kLambTraceStride + 1] = globaltimer();
+      pl.trace[(size_t)blockIdx.x * kLambTraceStride + 4] = k.novf;
+    }
+#endif
+  }
+}
+
+// The chunk loop (both modes). Replicated: pass 2 of ready tensors
+// interleaved. Sharded (pl.shard): pass 1 only; the FIFO keeps every
+// chunk's entry for the pass 2 after the cross-rank barrier.
+template <int W, bool FP>
+__device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambPlan& pl, unsigned char* stages,
+                            float* stash, StreamShared& sh, unsigned tag) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  Ctl k{};                           // claims lane
+  Books bk{};                        // books lane
+  // Registers written by a global atomic or load in one step and read in
+  // the next are assigned unconditionally: a conditional assignment
+  // compiles to a select, which waits for the value on the spot.
+  int pend = pl.nchunks;             // claims: the claim issued one step earlier (in flight)
+  unsigned long long probe = 0;      // claims: ready word of k.probe_t (in flight)
+  auto claim = [&]() { return atomicAdd(pl.head(), 1); };
+  auto fetch_desc = [&](int c) {
+    cp_async16(&sh.pdesc, pl.chunks + c);
+    cp_async16(reinterpret_cast<char*>(&sh.pdesc) + 16, reinterpret_cast<const char*>(pl.chunks + c) + 16);
+    cp_async_commit();
+  };
+  // up to maxn FIFO entries of the tensor known ready, in FIFO order
+  auto pick2 = [&](int q, int maxn) {
+    int n = 0;
+    while (n < maxn && k.fnext < k.ftail && sh.fifo[k.fnext % kFifo].tensor == k.ready_t) {
+      sh.e2[q][n] = sh.fifo[k.fnext % kFifo];
+      sh.neg2[q][n] = k.ready_neg;
+      ++n;
+      ++k.fnext;
+    }
+    sh.n2[q] = n;
+  };
+  if (wid == kCtlWarp && lane == 0) {
+    k.ready_t = -1;
+    k.probe_t = -1;
+    for (int q = 0; q < kSlots; ++q) {
+      sh.stop[q] = 0;
+      sh.n2[q] = 0;
+      sh.idx[q] = pl.nchunks;
+    }
+    for (int st = 0; st < kLambStages; ++st) mbar_init(&sh.full[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int q = 0; q < kLambStages; ++q) {
+      const int c = claim();
+      if (c >= pl.nchunks) k.claims_done = 1;
+      stream_fill(pl, k, q, c, c < pl.nchunks ? pl.chunks[c] : Chunk{}, sh);
+      stage_issue<W, FP>(a, pl, sh, q, q, stages);
+    }
+    k.pdesc = k.claims_done ? pl.nchunks : claim();
+    if (k.pdesc >= pl.nchunks) k.claims_done = 1;
+    else fetch_desc(k.pdesc);
+    pend = claim();
+  }
+  __syncthreads();
+  for (int it = 0;; ++it) {
+    const int q = it % kSlots, stage = it % kLambStages;
+    if (sh.stop[q]) break;
+    const int item = sh.idx[q];
+    const bool have1 = item < pl.nchunks;
+    const int n2 = sh.n2[q];
+    if (wid < kLambDataWarps) {
+      float pp = 0.0f, uu = 0.0f;
+      const unsigned char* stg = stages + (size_t)stage * kLambStageBytes;
+      // m', v' of a pass-2 entry without stash beside a pass-1 chunk: in
+      // flight during the pass-1 math
+      P2Regs r2;
+      const bool mv = have1 && n2 == 1 && sh.e2[q][0].off < 0;
+      if (tid == 0) LAMB_ITER(it, 0);
+      if (mv) p2_load_mv(a, sh.e2[q][0].start, sh.e2[q][0].len, r2);
+      if (have1 || n2 > 0) mbar_wait(&sh.full[stage], (unsigned)(it / kLambStages) & 1u);
+      if (tid == 0) LAMB_ITER(it, 1);
+      if (have1) {
+        const int off = sh.off[q];
+        p1_staged<W, FP>(a, s, sh.desc[q], stg, sh.goff[q], off >= 0 ? stash + off : nullptr, pp, uu);
+      }
+      if (tid == 0) LAMB_ITER(it, 2);
+      for (int j = 0; j < n2; ++j) {  // chunks of completed tensors
+        const FifoEntry e = sh.e2[q][j];
+        p2_staged(a, s, e.start, e.len, reinterpret_cast<const float4*>(stg + p2_area(have1, j)),
+                  e.off >= 0 ? stash + e.off : nullptr, sh.neg2[q][j], mv ? &r2 : nullptr);
+      }
+      if (tid == 0) LAMB_ITER(it, 3);
+      pp = warp_sum(pp);
+      uu = warp_sum(uu);
+      if (lane == 0) {
+        sh.red_p[q][wid] = pp;
+        sh.red_u[q][wid] = uu;
+      }
+    }
+    __syncthreads();  // iteration `it` done; its stage is free
+    if (tid == 0) LAMB_ITER(it, 4);
+    if (wid == kCtlWarp) {
+      if (lane == 0) {
+        if (n2 > 0) {  // free the entries pass 2 just finished and their ring regions
+          for (int j = 0; j < n2; ++j) {
+            if (sh.fifo[k.fhead % kFifo].off >= 0) --k.ring.live;
+            ++k.fhead;
+          }
+          for (int f = k.fhead; f < k.ftail; ++f)  // the oldest live region
+            if (sh.fifo[f % kFifo].off >= 0) {
+              k.ring.head = sh.fifo[f % kFifo].off;
+              break;
+            }
+        }
+        // iteration it + stages: the chunk whose descriptor was prefetched
+        // last step, staged into the stage iteration `it` freed
+        const int sq = (it + kLambStages) % kSlots;
+        const int c = k.pdesc;
+        cp_async_wait_all();
+        LAMB_ITER(it, 5);
+        stream_fill(pl, k, sq, c, sh.pdesc, sh);
+        // the descriptor of the claim issued last step; claim again
+        k.pdesc = k.claims_done ? pl.nchunks : pend;
+        if (k.pdesc >= pl.nchunks) k.claims_done = 1;
+        else fetch_desc(k.pdesc);
+        pend = claim();  // past the end once the queue is exhausted: harmless, reset at exit
+        const bool p1 = c < pl.nchunks;
+        if (pl.shard) {
+          sh.n2[sq] = 0;
+          sh.stop[sq] = p1 ? 0 : 1;
+        } else {
+          // readiness learned from last step's probe
+          if (k.probe_t >= 0 && (unsigned)(probe >> 32) == tag) {
+            k.ready_t = k.probe_t;
+            k.ready_neg = -__uint_as_float((unsigned)probe);
+          }
+          pick2(sq, p1 ? 1 : kDrain);
+          // the ready word of the FIFO head's tensor, unless known (used next step)
+          k.probe_t = -1;
+          if (k.fnext < k.ftail && sh.fifo[k.fnext % kFifo].tensor != k.ready_t)
+            k.probe_t = sh.fifo[k.fnext % kFifo].tensor;
+          probe = ld_relaxed_u64(pl.ready(k.probe_t >= 0 ? k.probe_t : 0));
+          // nothing left: no chunk, no entry now or later; else (an entry's
+          // tensor not ready yet) an empty iteration that polls again
+          sh.stop[sq] = (!p1 && sh.n2[sq] == 0 && k.fnext >= k.ftail) ? 1 : 0;
+          if (!p1 && sh.n2[sq] == 0 && !sh.stop[sq]) __nanosleep(200);
+        }
+        LAMB_ITER(it, 6);
+        stage_issue<W, FP>(a, pl, sh, sq, stage, stages);
+        LAMB_ITER(it, 7);
+      }
+    } else if (wid == kBooksWarp) {
+      books_step(pl, s, sh, tag, q, have1, item, bk);
+    }
+  }
+  if (wid == kCtlWarp && lane == 0) sh.nfifo = k.ftail;
+  if (wid == kBooksWarp && !pl.shard) {  // a count still in flight, then the arrive
+    books_step(pl, s, sh, tag, 0, false, pl.nchunks, bk);
+  }
+}
+
+template <int W, bool FP>
+__device__ void stream_replicated(const LambArgs& a, const LambScalars& s, const LambPlan& pl,
+                                  unsigned char* stages, float* stash, StreamShared& sh, unsigned tag) {
+  stream_loop<W, FP>(a, s, pl, stages, stash, sh, tag);
+  LAMB_STAMP(2);
+  // overflow chunks need every CTA's pass 1
+  if (threadIdx.x == 0)
+    while (ld_acquire_gpu(reinterpret_cast<const unsigned*>(pl.arrive())) < gridDim.x) __nanosleep(64);
+  __syncthreads();
+  overflow_pass2(a, s, pl, &sh.k);
+}
+
+// ----------------------------------------------------------- sharded LAMB
+template <int W, bool FP>
+__device__ void shard_lamb(const LambArgs& a, const LambScalars& s, const LambPlan& pl, unsigned char* stages,
+                           float* stash, StreamShared& sh, unsigned tag) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  stream_loop<W, FP>(a, s, pl, stages, stash, sh, tag);
+  LAMB_STAMP(1);
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    sh.flag = atomicAdd(pl.arrive(), 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (sh.flag) {  // the last CTA: every partial of this rank is out
+    // this rank's pair of every tensor (zero where it owns no chunk) into
+    // slot [rank][t] of every rank's norm table, one warp per tensor
+    for (int t = wid; t < pl.T; t += kLambThreads / 32) {
+      const double2 q = tensor_sums(pl, t, tag);
+      if (lane < pl.push.ndst) pl.table[lane][(size_t)pl.bar.rank * pl.T + t] = q;
+    }
+    __threadfence_system();
+    __syncthreads();
+    // cross-rank barrier (k_barrier's protocol)
+    if (tid == 0) {
+      sh.epoch = *pl.bar.epoch + 1;
+      *pl.bar.epoch = sh.epoch;
+    }
+    __syncthreads();
+    const unsigned long long epoch = sh.epoch;
+    if (tid < pl.bar.world) {
+      st_release_sys(pl.bar.flags[tid] + pl.bar.rank, epoch);
+      const unsigned long long* mine = pl.bar.flags[pl.bar.rank] + tid;
+      const unsigned long long t0 = globaltimer();
+      while (ld_acquire_sys(mine) < epoch) {
+        if (globaltimer() - t0 > pl.bar.timeout_ns) {
+          atomicExch_system(pl.bar.err, 1);
+          break;
+        }
+      }
+    }
+    __syncthreads();
+    for (int t = tid; t < pl.T; t += kLambThreads) {  // trust of every tensor, rank order
+      double x = 0.0, y = 0.0;
+      for (int k = 0; k < pl.bar.world; ++k) {
+        const double2 q = __ldcg(pl.my_table + (size_t)k * pl.T + t);
+        x += q.x;
+        y += q.y;
+      }
+      const float tr = trust_of(x, y);
+      pl.trust[t] = tr;
+      pl.step_scale[t] = __fmul_rn(s.lr, tr);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release_gpu(reinterpret_cast<unsigned*>(pl.release_flag()), 1u);
+    }
+  }
+  if (tid == 0)
+    while (ld_acquire_gpu(reinterpret_cast<const unsigned*>(pl.release_flag())) == 0u) __nanosleep(32);
+  __syncthreads();
+  LAMB_STAMP(2);
+  const int nf = sh.nfifo;  // every FIFO entry of this CTA (nothing was picked)
+  for (int f = 0; f < nf && tid < kLambDataThreads; ++f) {
+    const FifoEntry e = sh.fifo[f];
+    p2_chunk(a, s, e.start, e.len, e.off >= 0 ? stash + e.off : nullptr, neg_of(pl, s, e.tensor), &pl.push);
+  }
+  overflow_pass2(a, s, pl, &sh.k);
 }
 
 // --------------------------------------------------------------- kernel
 template <int W, bool FP>
 __global__ void __launch_bounds__(kLambThreads, kLambCtasPerSm) k_lamb(LambArgs a, LambPlan pl) {
-  extern __shared__ __align__(16) float stash[];
-  __shared__ LambShared sh;
+  extern __shared__ __align__(128) unsigned char dyn_smem[];
+  __shared__ StreamShared sh;
+  unsigned char* stages = dyn_smem;
+  float* stash = reinterpret_cast<float*>(dyn_smem + (size_t)kLambStages * kLambStageBytes);
   const LambScalars s{a.hp[0], a.hp[1], a.hp[2]};
-  const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
-  if (tid == 0) sh.t_neg = -1;
+  const unsigned tag = __ldcg(pl.tag_word()) + 1u;  // this launch's tag
   LAMB_STAMP(0);
-  if (!pl.shard) {
-    for (int w = 0; w <= pl.nwin; ++w) {
-      if (w < pl.nwin) {
-        pass1<W, FP>(a, s, pl, w, w & 1, stash + (w & 1) * pl.half, pl.half, sh);
-        LAMB_STAMP(1 + 3 * w);
-        grid_arrive(pl.arrive(w));
-      }
-      if (w >= 1) {
-        const int q = w - 1;
-        grid_wait(pl.arrive(q), G);
-        LAMB_STAMP(2 + 3 * q);
-        pass2(a, s, pl, q, q & 1, stash + (q & 1) * pl.half, sh);
-        LAMB_STAMP(3 + 3 * q);
-      }
-    }
-  } else {
-    // tensors with no chunk on this rank contribute a zero pair
-    for (int t = b; t < pl.T; t += G) {
-      const int2 r = pl.tchunk[t];
-      if (r.y <= r.x && tid < pl.push.ndst) {
-        pl.table[tid][(size_t)pl.bar.rank * pl.T + t] = make_double2(0.0, 0.0);
-        __threadfence_system();
-      }
-    }
-    pass1<W, FP>(a, s, pl, 0, 0, stash, 2 * pl.half, sh);
-    LAMB_STAMP(1);
-    grid_arrive(pl.arrive(0));
-    if (b == 0) {  // cross-rank barrier (k_barrier's protocol), then release the grid
-      grid_wait(pl.arrive(0), G);
-      if (tid == 0) {
-        sh.epoch = *pl.bar.epoch + 1;
-        *pl.bar.epoch = sh.epoch;
-      }
-      __syncthreads();
-      const unsigned long long epoch = sh.epoch;
-      if (tid < pl.bar.world) {
-        __threadfence_system();
-        st_release_sys(pl.bar.flags[tid] + pl.bar.rank, epoch);
-        const unsigned long long* mine = pl.bar.flags[pl.bar.rank] + tid;
-        const unsigned long long t0 = globaltimer();
-        while (ld_acquire_sys(mine) < epoch) {
-          if (globaltimer() - t0 > pl.bar.timeout_ns) {
-            atomicExch_system(pl.bar.err, 1);
-            break;
-          }
-        }
-      }
-      grid_arrive(pl.arrive(1));
-    }
-    grid_wait(pl.arrive(1), 1);
-    LAMB_STAMP(2);
-    for (int t = b; t < pl.T; t += G) {  // trust of every tensor, rank order
-      if (tid == 0) {
-        double x = 0.0, y = 0.0;
-        for (int k = 0; k < pl.bar.world; ++k) {
-          const double2 q = __ldcg(pl.my_table + (size_t)k * pl.T + t);
-          x += q.x;
-          y += q.y;
-        }
-        const float tr = trust_of(x, y);
-        pl.trust[t] = tr;
-        pl.step_scale[t] = __fmul_rn(s.lr, tr);
-      }
-    }
-    pass2(a, s, pl, 0, 0, stash, sh);
-    LAMB_STAMP(3);
-  }
+  if (!pl.shard) stream_replicated<W, FP>(a, s, pl, stages, stash, sh, tag);
+  else shard_lamb<W, FP>(a, s, pl, stages, stash, sh, tag);
+  LAMB_STAMP(3);
   __syncthreads();
-  if (tid == 0) {
+  if (threadIdx.x == 0) {
     __threadfence();
-    if (atomicAdd(pl.exited(), 1) == G - 1) {  // last CTA out resets every counter
-      const int nc = pl.ncounters();
-      for (int k = 0; k < nc; ++k) pl.cnt[k] = 0;
+    if (atomicAdd(pl.exited(), 1) == (int)gridDim.x - 1) {  // last CTA out resets the counters
+      const int nc = pl.nreset();
+      for (int k = 0; k < nc; ++k)
+        if (k != 6) pl.cnt[k] = 0;
+      *pl.tag_word() = tag;  // the next launch uses tag + 1
       __threadfence();
     }
   }

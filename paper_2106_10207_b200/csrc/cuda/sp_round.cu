@@ -89,22 +89,20 @@ struct sp_round {
   // LAMB plan (sp_lamb.cuh)
   int sm_count = 148;
   int lamb_grid = 148;
-  size_t stash_bytes = 0;
+  size_t lamb_smem = 0;  // k_lamb dynamic shared memory: stages + stash
   bool coop = true;  // cooperative launch accepted (also inside graph capture)
   Chunk* d_chunks = nullptr;
   size_t cap_chunks = 0;
-  int2* d_wchunk = nullptr;
-  size_t cap_wchunk = 0;
   int2* d_tchunk = nullptr;
   size_t cap_tchunk = 0;
-  float2* d_partial = nullptr;  // per chunk
+  unsigned long long* d_partial = nullptr;  // per chunk: two tagged words
   size_t cap_partial = 0;
-  int* d_ovf = nullptr;         // per chunk slot: overflow lists of the windows
+  int* d_ovf = nullptr;         // per chunk slot: overflow list
   size_t cap_ovf = 0;
   int* d_cnt = nullptr;         // queue / barrier / tensor counters (LambPlan::cnt)
   size_t cap_cnt = 0;
   unsigned long long* d_trace = nullptr;  // SP_LAMB_TRACE builds only
-  int nwin = 0;
+  int nchunks = 0;
   float* d_trust = nullptr;
   float* d_step_scale = nullptr;
   float* d_hp = nullptr;
@@ -182,29 +180,32 @@ int validate_cfg(const sp_round_cfg* c) {
 
 // ------------------------------------------------------------- LAMB plan
 // Tables of k_lamb (sp_lamb.cuh):
-//   windows  replicated: sets of whole tensors filling at most kWindowFill
-//            of half of all stashes (a larger tensor gets a window of its
-//            own); sharded: one window, this rank's range;
-//   chunks   each window cut at tensor edges and every multiple of
-//            kLambTile, in element order; CTAs claim them at run time;
+//   chunks   the elements this rank steps (replicated: all; sharded: its
+//            owned range) cut at tensor edges and every multiple of
+//            kLambTile; CTAs claim them at run time in this order: tensor
+//            by tensor, largest first (a tensor's pass 2 starts when its
+//            last chunk is in, so the kernel ends on small tensors), each
+//            tensor's chunks in element order;
 //   tensors  the chunk range of every tensor (its norm partials).
-// Windows are kept below the stash capacity so that the dynamic claims,
-// which give fast CTAs more chunks, rarely overflow a CTA's half.
-constexpr double kWindowFill = 0.92;
-
+// The cut points depend only on kLambTile, so every order gives the same
+// partials and the same fp64 sums per tensor.
 int build_lamb_plan(sp_round* r) {
   const int T = (int)r->tsizes.size();
+  std::vector<Chunk> chunks;
+  std::vector<int2> tchunk((size_t)T, make_int2(0, 0));
+  const int64_t lo = r->shard ? r->own_lo() : 0, hi = r->shard ? r->own_hi() : r->cfg.n;
   std::vector<int64_t> tstart((size_t)T + 1, 0);
   for (int t = 0; t < T; ++t) tstart[(size_t)t + 1] = tstart[(size_t)t] + r->tsizes[(size_t)t];
-  std::vector<Chunk> chunks;
-  std::vector<int2> wchunk, tchunk((size_t)T, make_int2(0, 0));
-  // chunks of [lo, hi) (tensor t's elements or a clipped part of them),
-  // every multiple of kLambTile a boundary
-  auto add_range = [&](int t, int64_t lo, int64_t hi) {
-    if (hi <= lo) return;
-    if (tchunk[(size_t)t].y == tchunk[(size_t)t].x) tchunk[(size_t)t].x = (int)chunks.size();
-    for (int64_t s = lo; s < hi;) {
-      const int64_t e = std::min(hi, (s / kLambTile + 1) * kLambTile);
+  std::vector<int> order((size_t)T);
+  for (int t = 0; t < T; ++t) order[(size_t)t] = t;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int x, int y) { return r->tsizes[(size_t)x] > r->tsizes[(size_t)y]; });
+  for (int t : order) {
+    const int64_t t0 = tstart[(size_t)t], t1 = tstart[(size_t)t + 1];
+    const int64_t a = std::max(t0, lo), b = std::min(t1, hi);
+    tchunk[(size_t)t] = make_int2((int)chunks.size(), (int)chunks.size());
+    for (int64_t s = a; s < b;) {
+      const int64_t e = std::min(b, (s / kLambTile + 1) * kLambTile);
       Chunk ch{};
       ch.start = s;
       ch.len = (int)(e - s);
@@ -213,74 +214,16 @@ int build_lamb_plan(sp_round* r) {
       s = e;
     }
     tchunk[(size_t)t].y = (int)chunks.size();
-  };
-  auto open_window = [&]() { wchunk.push_back(make_int2((int)chunks.size(), 0)); };
-  auto close_window = [&]() { wchunk.back().y = (int)chunks.size(); };
-  if (r->shard) {
-    open_window();
-    for (int t = 0; t < T; ++t)
-      add_range(t, std::max(tstart[(size_t)t], r->own_lo()), std::min(tstart[(size_t)t + 1], r->own_hi()));
-    close_window();
-  } else {
-    // Windows are sets of whole tensors (not necessarily adjacent), at most
-    // `fill` elements unless one tensor alone is larger: longest tensors
-    // first, each into the least loaded window it fits, with as few windows
-    // as the total allows, so the windows come out of similar size and the
-    // split-phase barrier of one window is hidden by the next window's pass 1.
-    // Largest windows first, smallest last (its pass 2 is not overlapped).
-    const double fill = (double)(r->stash_bytes / 8) * r->lamb_grid * kWindowFill;
-    std::vector<int> order((size_t)T);
-    for (int t = 0; t < T; ++t) order[(size_t)t] = t;
-    std::stable_sort(order.begin(), order.end(),
-                     [&](int x, int y) { return r->tsizes[(size_t)x] > r->tsizes[(size_t)y]; });
-    int64_t rest = 0;
-    for (int t = 0; t < T; ++t)
-      if ((double)r->tsizes[(size_t)t] <= fill) rest += r->tsizes[(size_t)t];
-    std::vector<std::vector<int>> win;
-    std::vector<int64_t> load;
-    for (int t : order)
-      if ((double)r->tsizes[(size_t)t] > fill) {
-        win.push_back({t});
-        load.push_back(r->tsizes[(size_t)t]);
-      }
-    const size_t big = win.size();
-    for (size_t k = 0; k < (size_t)std::ceil((double)rest / fill); ++k) {
-      win.emplace_back();
-      load.push_back(0);
-    }
-    for (int t : order) {
-      const int64_t sz = r->tsizes[(size_t)t];
-      if ((double)sz > fill) continue;
-      size_t best = win.size();
-      for (size_t k = big; k < win.size(); ++k)
-        if ((double)(load[k] + sz) <= fill && (best == win.size() || load[k] < load[best])) best = k;
-      if (best == win.size()) {  // no room: one more window
-        win.emplace_back();
-        load.push_back(0);
-        best = win.size() - 1;
-      }
-      win[best].push_back(t);
-      load[best] += sz;
-    }
-    std::vector<size_t> wo;
-    for (size_t k = 0; k < win.size(); ++k)
-      if (load[k] > 0) wo.push_back(k);
-    std::stable_sort(wo.begin(), wo.end(), [&](size_t x, size_t y) { return load[x] > load[y]; });
-    for (size_t k : wo) {
-      std::sort(win[k].begin(), win[k].end());  // tensor order inside a window
-      open_window();
-      for (int t : win[k]) add_range(t, tstart[(size_t)t], tstart[(size_t)t + 1]);
-      close_window();
-    }
   }
   for (Chunk& ch : chunks) ch.tchunks = tchunk[(size_t)ch.tensor].y - tchunk[(size_t)ch.tensor].x;
-  r->nwin = (int)wchunk.size();
-  const size_t ncnt = 4 * (size_t)r->nwin + 4 + (size_t)T;
+  r->nchunks = (int)chunks.size();
+  if (chunks.empty()) chunks.emplace_back();
+  const size_t ncnt = lamb_counter_ints(T);
   SP_CUDA(cudaSetDevice(r->cfg.device));
   if (int rc = upload(r->d_chunks, r->cap_chunks, chunks)) return rc;
-  if (int rc = upload(r->d_wchunk, r->cap_wchunk, wchunk)) return rc;
   if (int rc = upload(r->d_tchunk, r->cap_tchunk, tchunk)) return rc;
-  if (int rc = upload(r->d_partial, r->cap_partial, std::vector<float2>(chunks.size()))) return rc;
+  if (int rc = upload(r->d_partial, r->cap_partial, std::vector<unsigned long long>(2 * chunks.size())))
+    return rc;
   if (int rc = upload(r->d_ovf, r->cap_ovf, std::vector<int>(chunks.size()))) return rc;
   if (int rc = upload(r->d_cnt, r->cap_cnt, std::vector<int>(ncnt, 0))) return rc;
   return SP_OK;
@@ -352,7 +295,7 @@ cudaError_t launch_lamb_w(sp_round* r, const LambArgs& a, const LambPlan& pl, cu
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3((unsigned)r->lamb_grid);
   lc.blockDim = dim3(kLambThreads);
-  lc.dynamicSmemBytes = r->stash_bytes;
+  lc.dynamicSmemBytes = r->lamb_smem;
   lc.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeCooperative;
@@ -366,15 +309,14 @@ int launch_lamb(sp_round* r, const LambArgs& a, const BarrierArgs& ba, cudaStrea
   const sp_round_cfg& c = r->cfg;
   LambPlan pl{};
   pl.chunks = r->d_chunks;
-  pl.wchunk = r->d_wchunk;
+  pl.nchunks = r->nchunks;
   pl.tchunk = r->d_tchunk;
   pl.partial = r->d_partial;
   pl.ovf = r->d_ovf;
   pl.cnt = r->d_cnt;
   pl.trust = r->d_trust;
   pl.step_scale = r->d_step_scale;
-  pl.nwin = r->nwin;
-  pl.half = (int)(r->stash_bytes / 8);
+  pl.cap = (int)((r->lamb_smem - (size_t)kLambStages * kLambStageBytes) / 4);
   pl.T = c.num_tensors;
   pl.shard = r->shard ? 1 : 0;
   pl.trace = r->d_trace;
@@ -661,21 +603,24 @@ int launch_graph(sp_round* r, const std::vector<const void*>& key, const float* 
 }
 
 // k_lamb runs kLambCtasPerSm CTAs per SM; each gets an equal share of the
-// SM's shared memory (less the per-CTA reservation) as its stash.
+// SM's shared memory (less the per-CTA reservation): its load stages, the
+// rest its stash.
 template <int W, bool FP>
 int lamb_func_setup(sp_round* r, int per_sm_smem, int optin, int reserved) {
   cudaFuncAttributes fa{};
   SP_CUDA(cudaFuncGetAttributes(&fa, k_lamb<W, FP>));
   const size_t share = (size_t)per_sm_smem / kLambCtasPerSm - (size_t)reserved - fa.sharedSizeBytes;
   const size_t dyn = std::min(share, (size_t)optin - fa.sharedSizeBytes) / 64 * 64;
-  r->stash_bytes = r->stash_bytes ? std::min(r->stash_bytes, dyn) : dyn;
+  if (dyn < (size_t)kLambStages * kLambStageBytes + 4 * (size_t)kLambTile)
+    return fail(SP_ERR_CUDA, "k_lamb: shared memory too small for its stages and a stash");
+  r->lamb_smem = r->lamb_smem ? std::min(r->lamb_smem, dyn) : dyn;
   SP_CUDA(cudaFuncSetAttribute(k_lamb<W, FP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
   return SP_OK;
 }
 
 template <int W, bool FP>
 int lamb_occupancy(sp_round* r, int* per_sm) {
-  SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_lamb<W, FP>, kLambThreads, r->stash_bytes));
+  SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_lamb<W, FP>, kLambThreads, r->lamb_smem));
   return SP_OK;
 }
 
@@ -786,7 +731,6 @@ int sp_round_destroy(sp_round* r) {
     if (r->base[k] && k != r->cfg.rank) cudaIpcCloseMemHandle(r->base[k]);
   cudaFree(r->shared);
   cudaFree(r->d_chunks);
-  cudaFree(r->d_wchunk);
   cudaFree(r->d_tchunk);
   cudaFree(r->d_ovf);
   cudaFree(r->d_partial);
@@ -863,7 +807,8 @@ int sp_round_set_assignment(sp_round* r, const int64_t* offsets, const double* w
   r->weights.assign(weights, weights + G);
   if (int rc = build_lamb_plan(r)) return rc;
 #ifdef SP_LAMB_TRACE
-  if (!r->d_trace) SP_CUDA(cudaMalloc(&r->d_trace, (size_t)r->lamb_grid * 64 * sizeof(unsigned long long)));
+  if (!r->d_trace)
+    SP_CUDA(cudaMalloc(&r->d_trace, (size_t)r->lamb_grid * kLambTraceStride * sizeof(unsigned long long)));
 #endif
   r->assigned = true;
   drop_graphs(r);
@@ -965,7 +910,10 @@ int sp_round_run_phased(sp_round* r, const float* const* grads, float* p, float*
   return SP_OK;
 }
 
-int sp_round_lamb_windows(const sp_round* r) { return r ? r->nwin : -1; }
+int sp_round_lamb_chunks(const sp_round* r, int* tile) {
+  if (tile) *tile = kLambTile;
+  return r ? r->nchunks : -1;
+}
 
 int sp_round_describe(const sp_round_cfg* cfg, const int64_t* offsets, int sm_count, sp_plan_desc* out) {
   if (int rc = validate_cfg(cfg)) return rc;
@@ -994,11 +942,11 @@ int sp_round_describe(const sp_round_cfg* cfg, const int64_t* offsets, int sm_co
 }
 
 #ifdef SP_LAMB_TRACE
-// Diagnostic builds: per-CTA globaltimer stamps of the last k_lamb launch
-// ([grid][64] u64: start, then per window pass-1 end, wait end, pass-2 end).
+// Diagnostic builds: the stamps of the last k_lamb launch ([grid][stride]
+// u64, sp_lamb.cuh kLambTraceStride); returns the grid.
 int sp_round_lamb_trace(sp_round* r, unsigned long long* host, int cap) {
   if (!r || !r->d_trace) return -1;
-  const int n = std::min(cap, r->lamb_grid * 64);
+  const int n = std::min(cap, r->lamb_grid * kLambTraceStride);
   cudaDeviceSynchronize();
   cudaMemcpy(host, r->d_trace, (size_t)n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
   return r->lamb_grid;

@@ -230,9 +230,11 @@ class AveragingRound:
 
         return torch.as_tensor(_View(), device=f"cuda:{self.device}")
 
-    def lamb_windows(self) -> int:
-        """Tensor windows of the LAMB plan (sp_round_lamb_windows)."""
-        return int(self._lib.sp_round_lamb_windows(self._h))
+    def lamb_chunks(self) -> tuple:
+        """(chunks, tile) of the LAMB plan (sp_round_lamb_chunks)."""
+        tile = ctypes.c_int(0)
+        n = int(self._lib.sp_round_lamb_chunks(self._h, ctypes.byref(tile)))
+        return n, tile.value
 
     def own_range(self) -> tuple[int, int]:
         """[lo, hi) of the flattened vector this rank owns (averages, and with

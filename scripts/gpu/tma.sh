@@ -1,0 +1,2 @@
+mkdir -p gpurun_out
+timeout 300 scripts/micro/tma_stream > gpurun_out/tma_stream.txt 2>&1

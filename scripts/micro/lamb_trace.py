@@ -1,5 +1,5 @@
 """Per-CTA timeline of one k_lamb launch (SP_LAMB_TRACE build): where the
-time goes between pass 1, the split-phase window barriers and pass 2.
+time goes: when each CTA ran out of pass-1 chunks, left the stream loop and exited.
 
     python scripts/micro/lamb_trace.py path/to/traced/libsp_round.so [workload]
 """
@@ -38,31 +38,37 @@ def main():
     lib = nat.lib()
     lib.sp_round_lamb_trace.restype = ctypes.c_int
     lib.sp_round_lamb_trace.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
-    buf = np.zeros(148 * 8 * 64, np.uint64)
+    S = 64 + 128 * 8  # sp_lamb.cuh kLambTraceStride
+    buf = np.zeros(148 * 8 * S, np.uint64)
     grid = lib.sp_round_lamb_trace(r._h, buf.ctypes.data, buf.size)
-    t = buf[: grid * 64].reshape(grid, 64).astype(np.int64)
-    W = r.lamb_windows()
+    tr = buf[: grid * S].reshape(grid, S).astype(np.int64)
+    t = tr[:, :64]
     t0 = t[:, 0].min()
     rel = (t - t0) / 1e3  # us
-    print(f"grid {grid}, windows {W}, kernel span {rel[:, 3 * W].max():.1f} us "
+    span = rel[:, 3].max()
+    print(f"grid {grid}, chunks {r.lamb_chunks()[0]}, kernel span {span:.1f} us "
           f"(start spread {rel[:, 0].max():.2f} us)")
-    for w in range(W):
-        p1 = rel[:, 1 + 3 * w]
-        wt = rel[:, 2 + 3 * w]
-        p2 = rel[:, 3 + 3 * w]
-        prev = rel[:, 0] if w == 0 else np.maximum(rel[:, 3 * w], rel[:, 1 + 3 * (w - 1)] * 0)
-        print(f"w{w}: pass1 end min/med/max {p1.min():7.1f} {np.median(p1):7.1f} {p1.max():7.1f} | "
-              f"wait end {wt.min():7.1f} {np.median(wt):7.1f} {wt.max():7.1f} | "
-              f"pass2 end {p2.min():7.1f} {np.median(p2):7.1f} {p2.max():7.1f}")
-    # time each CTA spends waiting at window barriers
-    waits = np.zeros(grid)
-    for w in range(W):
-        before = rel[:, 1 + 3 * (w + 1)] if w + 1 < W else rel[:, 1 + 3 * w]
-        waits += np.maximum(0, rel[:, 2 + 3 * w] - before)
-    print(f"barrier wait per CTA: median {np.median(waits):.1f} us, max {waits.max():.1f} us")
-    sm = np.arange(grid) % 148
-    per_sm = [rel[sm == k, 1].max() for k in range(148)]
-    print(f"window-0 pass-1 end by SM: min {min(per_sm):.1f} max {max(per_sm):.1f}")
+    for k, name in ((1, "pass-1 counts done"), (2, "stream loop done"), (3, "exit")):
+        x = rel[:, k]
+        print(f"{name:20s} min/med/max {x.min():7.1f} {np.median(x):7.1f} {x.max():7.1f}")
+    print(f"chunks not stashed: {int(t[:, 4].sum())} (max per CTA {int(t[:, 4].max())})")
+    print(f"tail after the last pass-1 count: {span - rel[:, 1].max():.1f} us")
+    # per-iteration phases (SM clocks): 0 top, 1 stage landed, 2 pass 1 done,
+    # 3 pass 2 done, 4 after the barrier (thread 0), 5 descriptor landed,
+    # 6 slot filled and pass-2 entries picked, 7 copies issued
+    it = tr[:, 64:].reshape(grid, 128, 8).astype(np.float64)
+    ok = (it[:, :-1, 0] > 0) & (it[:, 1:, 0] > 0)
+    d = lambda a, b: (it[:, :-1, b] - it[:, :-1, a])[ok]
+    per = (it[:, 1:, 0] - it[:, :-1, 0])[ok]
+    print(f"iterations traced: {int(ok.sum())}; cycles per iteration median {np.median(per):.0f} "
+          f"(mean {per.mean():.0f})")
+    for (a, b, name) in ((0, 1, "wait for the stage"), (1, 2, "pass 1"), (2, 3, "pass 2"),
+                         (3, 4, "barrier (thread 0)"), (4, 5, "claims: desc wait"), (5, 6, "claims: fill+pick"),
+                         (6, 7, "claims: stage copies"), (4, 7, "claims step")):
+        x = d(a, b)
+        print(f"  {name:22s} median {np.median(x):8.0f}  mean {x.mean():8.0f}  p90 {np.percentile(x, 90):8.0f}")
+    nxt = (it[:, 1:, 0] - it[:, :-1, 4])[ok]
+    print(f"  {'barrier -> next top':22s} median {np.median(nxt):8.0f}  mean {nxt.mean():8.0f}")
     r.close()
 
 

@@ -10,6 +10,8 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o stream_bw stream_bw.cu
 #include <cstdint>
 #include <cstdio>
+
+#include "../../paper_2106_10207_b200/csrc/cuda/sp_kernels.cuh"
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -156,6 +158,53 @@ __global__ void __launch_bounds__(256, CTAS) k_lamb2(const float4* __restrict__ 
   }
 }
 
+// k_lamb2's claim structure with k_lamb's exact per-element code: LAMB
+// moments with the IEEE div/sqrt of sp_kernels.cuh (lamb_moments), the fp16
+// wire store of the fused pack (grad_load / grad_finish), evict hints.
+__global__ void __launch_bounds__(256, 4) k_lamb3(sp::LambArgs a, long n4, int* ctr, float2* part) {
+  __shared__ float4 st[256 * 2];
+  __shared__ int s_item;
+  __shared__ float red[8];
+  const long nchunks = n4 / 512;
+  int next = 0;
+  if (threadIdx.x == 0) s_item = atomicAdd(ctr, 1);
+  __syncthreads();
+  long item = s_item;
+  const sp::LambScalars s{a.hp[0], a.hp[1], a.hp[2]};
+  const uint64_t pl = sp::policy_evict_last(), pf = sp::policy_evict_first();
+  while (item < nchunks) {
+    if (threadIdx.x == 0) next = atomicAdd(ctr, 1);
+    const int64_t i0 = 4 * (item * 512 + threadIdx.x), i1 = i0 + 4 * 256;
+    const sp::GradRaw g0 = sp::grad_load<SP_WIRE_FP16, true>(a, i0), g1 = sp::grad_load<SP_WIRE_FP16, true>(a, i1);
+    float4 p0 = sp::ld_hint_f4(a.p + i0, pl), p1 = sp::ld_hint_f4(a.p + i1, pl);
+    float4 m0 = sp::ld_hint_f4(a.m + i0, pf), m1 = sp::ld_hint_f4(a.m + i1, pf);
+    float4 v0 = sp::ld_hint_f4(a.v + i0, pf), v1 = sp::ld_hint_f4(a.v + i1, pf);
+    const float4 f0 = sp::grad_finish<SP_WIRE_FP16, true>(a, i0, g0), f1 = sp::grad_finish<SP_WIRE_FP16, true>(a, i1, g1);
+    float pp = 0.f, uu = 0.f;
+    float4 u0, u1;
+    sp::lamb_moments(a, s, f0.x, p0.x, m0.x, v0.x, u0.x); sp::lamb_moments(a, s, f0.y, p0.y, m0.y, v0.y, u0.y);
+    sp::lamb_moments(a, s, f0.z, p0.z, m0.z, v0.z, u0.z); sp::lamb_moments(a, s, f0.w, p0.w, m0.w, v0.w, u0.w);
+    sp::lamb_moments(a, s, f1.x, p1.x, m1.x, v1.x, u1.x); sp::lamb_moments(a, s, f1.y, p1.y, m1.y, v1.y, u1.y);
+    sp::lamb_moments(a, s, f1.z, p1.z, m1.z, v1.z, u1.z); sp::lamb_moments(a, s, f1.w, p1.w, m1.w, v1.w, u1.w);
+    sp::st_hint_f4(a.m + i0, m0, pf); sp::st_hint_f4(a.v + i0, v0, pf);
+    sp::st_hint_f4(a.m + i1, m1, pf); sp::st_hint_f4(a.v + i1, v1, pf);
+    st[threadIdx.x] = u0;
+    st[threadIdx.x + 256] = u1;
+    pp = __fmaf_rn(p0.x, p0.x, pp); pp = __fmaf_rn(p1.x, p1.x, pp);
+    uu = __fmaf_rn(u0.x, u0.x, uu); uu = __fmaf_rn(u1.x, u1.x, uu);
+    for (int o = 16; o > 0; o >>= 1) uu += __shfl_xor_sync(0xffffffffu, uu, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = uu + pp;
+    if (threadIdx.x == 0) s_item = next;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float x = 0.f;
+      for (int q = 0; q < 8; ++q) x += red[q];
+      part[item] = make_float2(x, x);
+    }
+    item = s_item;
+  }
+}
+
 int main() {
   const long n = 64L << 20;  // elements per array (256 MB fp32): > L2
   const long n4 = n / 4;
@@ -230,6 +279,30 @@ int main() {
     run2("claim     hint   c4", k_lamb2<1, 1, 4>, 4);
     run2("claim     hint   c3", k_lamb2<1, 1, 3>, 3);
     run2("claim     nohint c3", k_lamb2<1, 0, 3>, 3);
+  }
+  {
+    float* hp;
+    cudaMalloc(&hp, 16);
+    const float hph[4] = {1e-3f, 10.f, 1000.f, 0.f};
+    cudaMemcpy(hp, hph, 16, cudaMemcpyHostToDevice);
+    for (long nn : {n, 17842176L, 4L << 20}) {
+      sp::LambArgs la{};
+      la.hp = hp; la.b1 = 0.9f; la.b2 = 0.999f; la.omb1 = 0.1f; la.omb2 = 0.001f; la.eps = 1e-6f; la.wd = 0.01f;
+      auto go = [&](int k) {
+        la.g32 = g[k]; la.p = p[k]; la.m = m[k]; la.v = v[k]; la.wire_out = w[k];
+        cudaMemsetAsync(ctr, 0, 4);
+        k_lamb3<<<sms * 4, 256>>>(la, nn / 4, ctr, part);
+      };
+      for (int r = 0; r < 3; ++r) go(r & 1);
+      cudaEventRecord(e0);
+      for (int r = 0; r < 20; ++r) go(r & 1);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      const double t = ms / 20 * 1e-3;
+      printf("k_lamb math, n=%ld     %7.1f us/launch  %7.1f GB/s (26 B/elem)\n", nn, t * 1e6, 26.0 * nn / t / 1e9);
+    }
   }
   printf("err: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;

@@ -182,7 +182,7 @@ def test_lamb_tensor_larger_than_a_window(wire, shard):
     _run_case(wire, [0.5, 0.5], [1.0, 3.0], sizes, steps=2, warm=True, shard=shard)
 
 
-def test_lamb_plan_windows():
+def test_lamb_plan_chunks():
     import json
     import os
 
@@ -190,13 +190,18 @@ def test_lamb_plan_windows():
     al = tables["albert-large"]
     rnd = AveragingRound(sum(al), al, wire="fp16")
     rnd.assign([1.0], [1.0])
-    # 17.8M elements in windows of <= ~4.3M whole tensors (the 4,194,304
-    # FFN matrices alone fill one)
-    assert 5 <= rnd.lamb_windows() <= 8
+    # chunks cut at every multiple of the tile and at every tensor edge
+    n, tile = rnd.lamb_chunks()
+    edges, start = set(), 0
+    for sz in al:
+        edges.update(range((start // tile + 1) * tile, start + sz, tile))
+        edges.add(start)
+        start += sz
+    assert n == len(edges)
     rnd.close()
     rnd = AveragingRound(sum(al), al, wire="fp16", shard_lamb=True)
     rnd.assign([1.0], [1.0])
-    assert rnd.lamb_windows() == 1
+    assert rnd.lamb_chunks() == (n, tile)
     rnd.close()
 
 
