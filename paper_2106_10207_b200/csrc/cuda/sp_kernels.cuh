@@ -164,7 +164,9 @@ struct alignas(16) Chunk {
   int len;
   int tensor;
   int tchunks;  // chunks of this tensor (in this rank's table)
-  int pad[3];
+  int head;     // unaligned leading elements (split_chunk)
+  int nbody4;   // 16-byte body vectors
+  int tail;     // trailing elements
 };
 
 struct LambArgs {

@@ -72,7 +72,7 @@
 
 namespace sp {
 
-constexpr int kFifo = 32;  // chunks a CTA holds for pass 2 at once (more: overflow)
+constexpr int kFifo = 64;  // chunks a CTA holds for pass 2 at once (more: overflow)
 constexpr int kDrain = 4;  // pass-2 entries per iteration without a pass-1 chunk
 constexpr int kSlots = kLambStages + 1;  // iteration i uses slot i % kSlots
 constexpr int kCtlWarp = kLambDataWarps, kBooksWarp = kLambDataWarps + 1;
@@ -150,15 +150,20 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+// all but the newest group complete
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
-// arrive (count 1) and expect `bytes` of bulk copies on the current phase
-__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
+// expect `bytes` more of bulk copies on the current phase
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// the producer's arrival (count 1): the phase completes once the expected
+// bytes have landed
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
   unsigned ok = 0;
@@ -175,6 +180,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// a bulk copy counted on bar
+__device__ __forceinline__ void bulk_counted(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  mbar_expect_tx(bar, bytes);
+  bulk_g2s(dst, src, bytes, bar);
 }
 
 __device__ __forceinline__ unsigned long long tagged(float x, unsigned tag) {
@@ -419,10 +430,11 @@ __device__ void overflow_pass2(const LambArgs& a, const LambScalars& s, const La
 // ------------------------------------------------------------ the stream
 struct FifoEntry {
   long long start;
+  long long b0;  // first body element
   int len;
-  int off;     // stash offset of element `start` (float index, = start mod 4); -1: recompute
+  int off;       // stash offset of element `start` (float index, = start mod 4); -1: recompute
   int tensor;
-  int pad;
+  int nb;        // body vectors
 };
 
 // Claims lane state, in registers (its step is a chain of dependent
@@ -433,15 +445,12 @@ struct Ctl {
   int ready_t;              // last tensor seen ready (-1: none)
   float ready_neg;          // its -lr * trust
   int probe_t;              // tensor whose ready word is in flight (-1: none)
-  int pdesc;                // chunk whose descriptor is in flight to `desc` (>= nchunks: none)
+  int pdesc[2];             // chunks whose descriptors are in flight to sh.pdesc (>= nchunks: none)
   int claims_done;          // the queue is exhausted for this CTA
 };
 
 // Books lane state, in registers.
 struct Books {
-  int t, n;      // tensor (and its chunk count) of the count in flight
-  int pending;   // a count in flight, to check next step
-  int done;      // the count (an atomic's result, in flight)
   int arrived;   // counted in pl.arrive() (every partial of this CTA out)
   int novf;      // chunks this CTA could not stash (trace builds report it)
 };
@@ -458,7 +467,7 @@ struct StreamShared {
   int n2[kSlots];
   int stop[kSlots];              // 1: nothing left for this CTA
   FifoEntry fifo[kFifo];
-  Chunk pdesc;                   // descriptor prefetched by cp.async
+  Chunk pdesc[2];                // descriptors prefetched by cp.async, two steps ahead
   int nfifo;                     // FIFO entries of the loop (sharded pass 2)
   int k, flag;
   unsigned long long epoch;
@@ -470,46 +479,23 @@ __device__ __forceinline__ int p2_area(bool p1, int j) {
   return p1 ? kLambStageP2 : (j == 0 ? 0 : kLambStageG + (j - 1) * kLambDataThreads * 16);
 }
 
-// Claims lane: chunk c (descriptor ch; >= nchunks: none) into slot q with
-// its pass 2 queued.
-__device__ __forceinline__ void stream_fill(const LambPlan& pl, Ctl& k, int q, int c, const Chunk& ch,
+// Claims lane: chunk c (descriptor ch; >= nchunks: none) into slot q,
+// its body g, p, m, v copied into stage stg (counted on bar) and its pass 2
+// queued. Wire formats narrower than 16 B per vector are fetched as an
+// aligned superset; sh.goff[q] is the offset of the chunk's first body
+// gradient in the g area.
+template <int W, bool FP>
+__device__ __forceinline__ void stream_fill(const LambArgs& a, const LambPlan& pl, Ctl& k, int q, int c,
+                                            const Chunk& ch, unsigned char* stg, unsigned long long* bar,
                                             StreamShared& sh) {
   sh.idx[q] = c;
   if (c >= pl.nchunks) return;
   sh.desc[q] = ch;
-  int off = -2;
-  if (k.ftail - k.fhead < kFifo) {
-    off = ring_alloc(k.ring, pl.cap, ch.start, ch.len);
-    if (off >= 0) ++k.ring.live;
-    FifoEntry& e = sh.fifo[k.ftail % kFifo];
-    e.start = ch.start;
-    e.len = ch.len;
-    e.off = off;
-    e.tensor = ch.tensor;
-    ++k.ftail;
-  }
-  sh.off[q] = off;
-}
-
-// Claims lane: the bulk copies of slot q into stage `stage` (an empty slot
-// only arrives, keeping the stage's phases in step with the iterations):
-// the pass-1 chunk's body g, p, m, v, and the p of the slot's pass-2
-// entries. Wire formats narrower than 16 B per vector are fetched as an
-// aligned superset; sh.goff[q] is the offset of the chunk's first body
-// gradient in the g area.
-template <int W, bool FP>
-__device__ __forceinline__ void stage_issue(const LambArgs& a, const LambPlan& pl, StreamShared& sh, int q,
-                                            int stage, unsigned char* stages) {
-  unsigned char* stg = stages + (size_t)stage * kLambStageBytes;
-  unsigned long long* bar = &sh.full[stage];
-  const bool p1 = sh.idx[q] < pl.nchunks;
-  unsigned total = 0, nb = 0, gbytes = 0;
-  int64_t b0 = 0;
-  const char* gsrc = nullptr;
-  if (p1) {
-    const ChunkSplit sp = split_chunk(sh.desc[q].start, sh.desc[q].len);
-    b0 = sp.start + sp.head;
-    nb = (unsigned)sp.nbody4;
+  const int64_t b0 = ch.start + ch.head;
+  const unsigned nb = (unsigned)ch.nbody4;
+  if (nb) {
+    const char* gsrc;
+    unsigned gbytes;
     int goff = 0;
     if constexpr (FP) {
       gsrc = reinterpret_cast<const char*>(a.g32 + b0);
@@ -521,40 +507,64 @@ __device__ __forceinline__ void stage_issue(const LambArgs& a, const LambPlan& p
       constexpr int wb = W == SP_WIRE_FP16 ? 2 : 1;  // wire bytes per element
       const int64_t lo = (wb * b0) & ~(int64_t)15, hi = (wb * (b0 + 4 * (int64_t)nb) + 15) & ~(int64_t)15;
       gsrc = static_cast<const char*>(a.avg) + lo;
-      gbytes = nb ? (unsigned)(hi - lo) : 0;
+      gbytes = (unsigned)(hi - lo);
       goff = (int)(wb * b0 - lo);
     }
     sh.goff[q] = goff;
-    if (nb) total += gbytes + 48 * nb;
-  }
-  const int n2 = sh.n2[q];
-  for (int j = 0; j < n2; ++j) total += 16 * (unsigned)split_chunk(sh.e2[q][j].start, sh.e2[q][j].len).nbody4;
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  mbar_arrive_tx(bar, total);
-  if (nb) {
+    mbar_expect_tx(bar, gbytes + 48 * nb);
     bulk_g2s(stg, gsrc, gbytes, bar);
     bulk_g2s(stg + kLambStageG, a.p + b0, 16 * nb, bar);
     bulk_g2s(stg + kLambStageG + kLambDataThreads * 16, a.m + b0, 16 * nb, bar);
     bulk_g2s(stg + kLambStageG + 2 * kLambDataThreads * 16, a.v + b0, 16 * nb, bar);
   }
-  for (int j = 0; j < n2; ++j) {
-    const ChunkSplit sp = split_chunk(sh.e2[q][j].start, sh.e2[q][j].len);
-    if (sp.nbody4)
-      bulk_g2s(stg + p2_area(p1, j), a.p + sp.start + sp.head, 16 * (unsigned)sp.nbody4, bar);
+  int off = -2;
+  if (k.ftail - k.fhead < kFifo) {
+    off = ring_alloc(k.ring, pl.cap, ch.start, ch.len);
+    if (off >= 0) ++k.ring.live;
+    FifoEntry& e = sh.fifo[k.ftail % kFifo];
+    e.start = ch.start;
+    e.b0 = b0;
+    e.len = ch.len;
+    e.off = off;
+    e.tensor = ch.tensor;
+    e.nb = (int)nb;
+    ++k.ftail;
   }
+  sh.off[q] = off;
 }
 
-// Books warp, one step: check last step's count (every chunk of its tensor
-// counted: sum the partials, publish trust and the ready word), then
-// publish this iteration's partial and count it (the count is checked next
-// step). With no chunk: every count of this CTA is resolved, so it arrives.
+// Books warp, one step: publish this iteration's partial and count it for
+// its tensor; the CTA that counts a tensor's last chunk sums the partials
+// and publishes trust and the ready word. With no chunk: every count of
+// this CTA is done, so it arrives.
 __device__ __forceinline__ void books_step(const LambPlan& pl, const LambScalars& s, StreamShared& sh,
                                            unsigned tag, int slot, bool have1, int item, Books& k) {
   const int lane = threadIdx.x & 31;
   int last = -1;
-  if (lane == 0 && k.pending) {
-    if (k.done == k.n - 1) last = k.t;
-    k.pending = 0;
+  if (lane == 0) {
+    if (have1) {
+      const Chunk& c = sh.desc[slot];
+      float x = 0.0f, y = 0.0f;
+#pragma unroll
+      for (int w = 0; w < kLambDataWarps; ++w) {
+        x += sh.red_p[slot][w];
+        y += sh.red_u[slot][w];
+      }
+      publish_partial(pl, item, x, y, tag);
+      if (sh.off[slot] < 0) ++k.novf;
+      if (sh.off[slot] == -2) pl.ovf[atomicAdd(pl.ovf_n(), 1)] = item;
+      if (!pl.shard && atomicAdd(pl.done(c.tensor), 1) == c.tchunks - 1) last = c.tensor;
+    } else if (!k.arrived && !pl.shard) {  // every write of this CTA's pass 1 is out
+      __threadfence();
+      atomicAdd(pl.arrive(), 1);
+      k.arrived = 1;
+#ifdef SP_LAMB_TRACE
+      if (pl.trace) {
+        pl.trace[(size_t)blockIdx.x * kLambTraceStride + 1] = globaltimer();
+        pl.trace[(size_t)blockIdx.x * kLambTraceStride + 4] = k.novf;
+      }
+#endif
+    }
   }
   last = __shfl_sync(0xffffffffu, last, 0);
   if (last >= 0) {
@@ -566,35 +576,6 @@ __device__ __forceinline__ void books_step(const LambPlan& pl, const LambScalars
       pl.step_scale[last] = sc;
       *pl.ready(last) = tagged(sc, tag);
     }
-  }
-  if (lane != 0) return;
-  if (have1) {
-    const Chunk& c = sh.desc[slot];
-    float x = 0.0f, y = 0.0f;
-#pragma unroll
-    for (int w = 0; w < kLambDataWarps; ++w) {
-      x += sh.red_p[slot][w];
-      y += sh.red_u[slot][w];
-    }
-    publish_partial(pl, item, x, y, tag);
-    if (sh.off[slot] < 0) ++k.novf;
-    if (sh.off[slot] == -2) pl.ovf[atomicAdd(pl.ovf_n(), 1)] = item;
-    if (!pl.shard) {
-      k.done = atomicAdd(pl.done(c.tensor), 1);
-      k.t = c.tensor;
-      k.n = c.tchunks;
-      k.pending = 1;
-    }
-  } else if (!k.arrived && !pl.shard) {  // every write of this CTA's pass 1 is out
-    __threadfence();
-    atomicAdd(pl.arrive(), 1);
-    k.arrived = 1;
-#ifdef SP_LAMB_TRACE
-    if (pl.trace) {
-      pl.trace[(size_t)blockIdx.x * kLambTraceStride + 1] = globaltimer();
-      pl.trace[(size_t)blockIdx.x * kLambTraceStride + 4] = k.novf;
-    }
-#endif
   }
 }
 
@@ -613,17 +594,27 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
   int pend = pl.nchunks;             // claims: the claim issued one step earlier (in flight)
   unsigned long long probe = 0;      // claims: ready word of k.probe_t (in flight)
   auto claim = [&]() { return atomicAdd(pl.head(), 1); };
-  auto fetch_desc = [&](int c) {
-    cp_async16(&sh.pdesc, pl.chunks + c);
-    cp_async16(reinterpret_cast<char*>(&sh.pdesc) + 16, reinterpret_cast<const char*>(pl.chunks + c) + 16);
+  // the descriptor of chunk c into buffer b (one commit group per call,
+  // empty for no chunk, so that wait_group counts steps)
+  auto fetch_desc = [&](int b, int c) {
+    k.pdesc[b] = c;
+    if (c < pl.nchunks) {
+      cp_async16(&sh.pdesc[b], pl.chunks + c);
+      cp_async16(reinterpret_cast<char*>(&sh.pdesc[b]) + 16, reinterpret_cast<const char*>(pl.chunks + c) + 16);
+    }
     cp_async_commit();
   };
-  // up to maxn FIFO entries of the tensor known ready, in FIFO order
-  auto pick2 = [&](int q, int maxn) {
+  // up to maxn FIFO entries of the tensor known ready, in FIFO order, their
+  // body p copied into the stage (beside a pass-1 chunk: its p2 area; else
+  // the g, p, m, v areas)
+  auto pick2 = [&](int q, int maxn, bool p1, unsigned char* stg, unsigned long long* bar) {
     int n = 0;
-    while (n < maxn && k.fnext < k.ftail && sh.fifo[k.fnext % kFifo].tensor == k.ready_t) {
-      sh.e2[q][n] = sh.fifo[k.fnext % kFifo];
+    while (n < maxn && k.fnext < k.ftail) {
+      const FifoEntry& e = sh.fifo[k.fnext % kFifo];
+      if (e.tensor != k.ready_t) break;
+      sh.e2[q][n] = e;
       sh.neg2[q][n] = k.ready_neg;
+      if (e.nb) bulk_counted(stg + p2_area(p1, n), a.p + e.b0, 16 * (unsigned)e.nb, bar);
       ++n;
       ++k.fnext;
     }
@@ -642,12 +633,15 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
     for (int q = 0; q < kLambStages; ++q) {
       const int c = claim();
       if (c >= pl.nchunks) k.claims_done = 1;
-      stream_fill(pl, k, q, c, c < pl.nchunks ? pl.chunks[c] : Chunk{}, sh);
-      stage_issue<W, FP>(a, pl, sh, q, q, stages);
+      stream_fill<W, FP>(a, pl, k, q, c, c < pl.nchunks ? pl.chunks[c] : Chunk{},
+                         stages + (size_t)q * kLambStageBytes, &sh.full[q], sh);
+      mbar_arrive(&sh.full[q]);
     }
-    k.pdesc = k.claims_done ? pl.nchunks : claim();
-    if (k.pdesc >= pl.nchunks) k.claims_done = 1;
-    else fetch_desc(k.pdesc);
+    for (int b = 0; b < 2; ++b) {
+      const int c = k.claims_done ? pl.nchunks : claim();
+      if (c >= pl.nchunks) k.claims_done = 1;
+      fetch_desc(b, c);
+    }
     pend = claim();
   }
   __syncthreads();
@@ -704,38 +698,40 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
         // iteration it + stages: the chunk whose descriptor was prefetched
         // last step, staged into the stage iteration `it` freed
         const int sq = (it + kLambStages) % kSlots;
-        const int c = k.pdesc;
-        cp_async_wait_all();
+        // the ready word of the FIFO head's tensor, unless known: in flight
+        // while the slot is filled
+        k.probe_t = -1;
+        if (k.fnext < k.ftail && sh.fifo[k.fnext % kFifo].tensor != k.ready_t)
+          k.probe_t = sh.fifo[k.fnext % kFifo].tensor;
+        probe = ld_relaxed_u64(pl.ready(k.probe_t >= 0 ? k.probe_t : 0));
+        const int b = it & 1;  // the buffer fetched two steps ago
+        const int c = k.pdesc[b];
+        cp_async_wait_1();
         LAMB_ITER(it, 5);
-        stream_fill(pl, k, sq, c, sh.pdesc, sh);
+        unsigned char* stg = stages + (size_t)stage * kLambStageBytes;
+        stream_fill<W, FP>(a, pl, k, sq, c, sh.pdesc[b], stg, &sh.full[stage], sh);
         // the descriptor of the claim issued last step; claim again
-        k.pdesc = k.claims_done ? pl.nchunks : pend;
-        if (k.pdesc >= pl.nchunks) k.claims_done = 1;
-        else fetch_desc(k.pdesc);
+        const int cn = k.claims_done ? pl.nchunks : pend;
+        if (cn >= pl.nchunks) k.claims_done = 1;
+        fetch_desc(b, cn);
         pend = claim();  // past the end once the queue is exhausted: harmless, reset at exit
         const bool p1 = c < pl.nchunks;
         if (pl.shard) {
           sh.n2[sq] = 0;
           sh.stop[sq] = p1 ? 0 : 1;
         } else {
-          // readiness learned from last step's probe
           if (k.probe_t >= 0 && (unsigned)(probe >> 32) == tag) {
             k.ready_t = k.probe_t;
             k.ready_neg = -__uint_as_float((unsigned)probe);
           }
-          pick2(sq, p1 ? 1 : kDrain);
-          // the ready word of the FIFO head's tensor, unless known (used next step)
-          k.probe_t = -1;
-          if (k.fnext < k.ftail && sh.fifo[k.fnext % kFifo].tensor != k.ready_t)
-            k.probe_t = sh.fifo[k.fnext % kFifo].tensor;
-          probe = ld_relaxed_u64(pl.ready(k.probe_t >= 0 ? k.probe_t : 0));
+          pick2(sq, p1 ? 1 : kDrain, p1, stg, &sh.full[stage]);
           // nothing left: no chunk, no entry now or later; else (an entry's
           // tensor not ready yet) an empty iteration that polls again
           sh.stop[sq] = (!p1 && sh.n2[sq] == 0 && k.fnext >= k.ftail) ? 1 : 0;
-          if (!p1 && sh.n2[sq] == 0 && !sh.stop[sq]) __nanosleep(200);
+          if (!p1 && sh.n2[sq] == 0 && !sh.stop[sq]) __nanosleep(100);
         }
         LAMB_ITER(it, 6);
-        stage_issue<W, FP>(a, pl, sh, sq, stage, stages);
+        mbar_arrive(&sh.full[stage]);  // the stage of iteration it + stages is armed
         LAMB_ITER(it, 7);
       }
     } else if (wid == kBooksWarp) {
@@ -743,7 +739,7 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
     }
   }
   if (wid == kCtlWarp && lane == 0) sh.nfifo = k.ftail;
-  if (wid == kBooksWarp && !pl.shard) {  // a count still in flight, then the arrive
+  if (wid == kBooksWarp && !pl.shard) {  // the arrive, if no empty iteration made it
     books_step(pl, s, sh, tag, 0, false, pl.nchunks, bk);
   }
 }

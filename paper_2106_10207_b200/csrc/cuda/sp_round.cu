@@ -210,6 +210,9 @@ int build_lamb_plan(sp_round* r) {
       ch.start = s;
       ch.len = (int)(e - s);
       ch.tensor = t;
+      ch.head = std::min(ch.len, (int)((4 - (s & 3)) & 3));  // split_chunk (sp_kernels.cuh)
+      ch.nbody4 = (ch.len - ch.head) >> 2;
+      ch.tail = ch.len - ch.head - 4 * ch.nbody4;
       chunks.push_back(ch);
       s = e;
     }
