@@ -317,10 +317,21 @@ __device__ __forceinline__ float4 dir4(const LambArgs& a, const LambScalars& s, 
                      lamb_dir(a, s, p.z, m.z, v.z), lamb_dir(a, s, p.w, m.w, v.w));
 }
 
-// m', v' of a pass-2 chunk without stash, issued ahead of their use.
+// Loads of a pass-2 chunk's body issued ahead of their use: m', v' (no
+// stash), or p (p not staged).
 struct P2Regs {
   float4 m, v;
 };
+__device__ __forceinline__ const P2Regs& r0_dummy() {
+  static __device__ P2Regs z;
+  return z;
+}
+
+__device__ __forceinline__ void p2_load_p(const LambArgs& a, long long start, int len, P2Regs& r) {
+  const ChunkSplit sp = split_chunk(start, len);
+  const int t = threadIdx.x;
+  if (t < sp.nbody4) r.m = *reinterpret_cast<const float4*>(a.p + sp.start + sp.head + 4 * (int64_t)t);
+}
 
 __device__ __forceinline__ void p2_load_mv(const LambArgs& a, long long start, int len, P2Regs& r) {
   const ChunkSplit sp = split_chunk(start, len);
@@ -332,10 +343,12 @@ __device__ __forceinline__ void p2_load_mv(const LambArgs& a, long long start, i
   }
 }
 
-// Pass 2 of a chunk whose body p is staged at ps (replicated: p' overwrites
-// p). u from the stash, or recomputed from m', v' (mv: already loaded).
+// Pass 2 of a chunk whose body p is staged at ps, or (ps null, stashed)
+// already loaded into mv.m (replicated: p' overwrites p). u from the stash,
+// or recomputed from m', v' (already loaded into mv when have_mv).
 __device__ __forceinline__ void p2_staged(const LambArgs& a, const LambScalars& s, long long start, int len,
-                                          const float4* ps, const float* st, float neg, const P2Regs* mv) {
+                                          const float4* ps, const float* st, float neg, bool have_mv,
+                                          const P2Regs& mv) {
   const ChunkSplit sp = split_chunk(start, len);
   const int t = threadIdx.x;
   const int64_t b0 = sp.start + sp.head;
@@ -349,10 +362,10 @@ __device__ __forceinline__ void p2_staged(const LambArgs& a, const LambScalars& 
   }
   if (t < sp.nbody4) {
     const int64_t i = b0 + 4 * (int64_t)t;
-    const float4 p = ps[t];
+    const float4 p = ps ? ps[t] : mv.m;
     float4 u;
     if (st) u = *reinterpret_cast<const float4*>(st + (i - start));
-    else if (mv) u = dir4(a, s, p, mv->m, mv->v);
+    else if (have_mv) u = dir4(a, s, p, mv.m, mv.v);
     else u = dir4(a, s, p, *reinterpret_cast<const float4*>(a.m + i), *reinterpret_cast<const float4*>(a.v + i));
     *reinterpret_cast<float4*>(a.p + i) = p2_vec(neg, p, u);
   }
@@ -462,7 +475,7 @@ struct StreamShared {
   int idx[kSlots];               // its index (>= nchunks: none)
   int off[kSlots];               // its stash offset (-1: recompute, -2: global overflow)
   int goff[kSlots];              // its first body gradient in the stage's g area
-  FifoEntry e2[kSlots][kDrain];  // pass-2 entries of the iteration
+  FifoEntry e2[kSlots][kDrain];  // pass-2 entries of the iteration (kDrain >= 2)
   float neg2[kSlots][kDrain];    // their -lr * trust
   int n2[kSlots];
   int stop[kSlots];              // 1: nothing left for this CTA
@@ -612,9 +625,10 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
     while (n < maxn && k.fnext < k.ftail) {
       const FifoEntry& e = sh.fifo[k.fnext % kFifo];
       if (e.tensor != k.ready_t) break;
+      if (p1 && n == 1 && e.off < 0) break;  // the second beside a pass-1 chunk: stashed only
       sh.e2[q][n] = e;
       sh.neg2[q][n] = k.ready_neg;
-      if (e.nb) bulk_counted(stg + p2_area(p1, n), a.p + e.b0, 16 * (unsigned)e.nb, bar);
+      if (e.nb && !(p1 && n == 1)) bulk_counted(stg + p2_area(p1, n), a.p + e.b0, 16 * (unsigned)e.nb, bar);
       ++n;
       ++k.fnext;
     }
@@ -654,23 +668,44 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
     if (wid < kLambDataWarps) {
       float pp = 0.0f, uu = 0.0f;
       const unsigned char* stg = stages + (size_t)stage * kLambStageBytes;
-      // m', v' of a pass-2 entry without stash beside a pass-1 chunk: in
-      // flight during the pass-1 math
-      P2Regs r2;
-      const bool mv = have1 && n2 == 1 && sh.e2[q][0].off < 0;
+#ifdef SP_LAMB_TRACE
+      if (tid == 0 && pl.trace && !have1) {  // iterations without a pass-1 chunk: empty, drain
+        unsigned long long* tw = pl.trace + (size_t)blockIdx.x * kLambTraceStride;
+        if (tw[7] == 0) tw[7] = globaltimer();
+        ++tw[n2 ? 6 : 5];
+      }
+#endif
       if (tid == 0) LAMB_ITER(it, 0);
-      if (mv) p2_load_mv(a, sh.e2[q][0].start, sh.e2[q][0].len, r2);
-      if (have1 || n2 > 0) mbar_wait(&sh.full[stage], (unsigned)(it / kLambStages) & 1u);
-      if (tid == 0) LAMB_ITER(it, 1);
       if (have1) {
+        // Beside the pass-1 chunk up to two pass-2 entries: the first with
+        // its p staged (and m', v' loaded here if it has no stash), the
+        // second (stashed) with its p loaded here; these loads are in
+        // flight during the pass-1 math, which reads only shared memory.
+        P2Regs r0, r1;
+        const bool mv0 = n2 >= 1 && sh.e2[q][0].off < 0;
+        if (mv0) p2_load_mv(a, sh.e2[q][0].start, sh.e2[q][0].len, r0);
+        if (n2 == 2) p2_load_p(a, sh.e2[q][1].start, sh.e2[q][1].len, r1);
+        mbar_wait(&sh.full[stage], (unsigned)(it / kLambStages) & 1u);
+        if (tid == 0) LAMB_ITER(it, 1);
         const int off = sh.off[q];
         p1_staged<W, FP>(a, s, sh.desc[q], stg, sh.goff[q], off >= 0 ? stash + off : nullptr, pp, uu);
-      }
-      if (tid == 0) LAMB_ITER(it, 2);
-      for (int j = 0; j < n2; ++j) {  // chunks of completed tensors
-        const FifoEntry e = sh.e2[q][j];
-        p2_staged(a, s, e.start, e.len, reinterpret_cast<const float4*>(stg + p2_area(have1, j)),
-                  e.off >= 0 ? stash + e.off : nullptr, sh.neg2[q][j], mv ? &r2 : nullptr);
+        if (tid == 0) LAMB_ITER(it, 2);
+        if (n2 >= 1) {
+          const FifoEntry& e = sh.e2[q][0];
+          p2_staged(a, s, e.start, e.len, reinterpret_cast<const float4*>(stg + p2_area(true, 0)),
+                    e.off >= 0 ? stash + e.off : nullptr, sh.neg2[q][0], mv0, r0);
+        }
+        if (n2 == 2) {
+          const FifoEntry& e = sh.e2[q][1];
+          p2_staged(a, s, e.start, e.len, nullptr, stash + e.off, sh.neg2[q][1], true, r1);
+        }
+      } else if (n2 > 0) {
+        mbar_wait(&sh.full[stage], (unsigned)(it / kLambStages) & 1u);
+        for (int j = 0; j < n2; ++j) {  // pass 2 only
+          const FifoEntry& e = sh.e2[q][j];
+          p2_staged(a, s, e.start, e.len, reinterpret_cast<const float4*>(stg + p2_area(false, j)),
+                    e.off >= 0 ? stash + e.off : nullptr, sh.neg2[q][j], false, r0_dummy());
+        }
       }
       if (tid == 0) LAMB_ITER(it, 3);
       pp = warp_sum(pp);
@@ -724,7 +759,7 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
             k.ready_t = k.probe_t;
             k.ready_neg = -__uint_as_float((unsigned)probe);
           }
-          pick2(sq, p1 ? 1 : kDrain, p1, stg, &sh.full[stage]);
+          pick2(sq, p1 ? 2 : kDrain, p1, stg, &sh.full[stage]);
           // nothing left: no chunk, no entry now or later; else (an entry's
           // tensor not ready yet) an empty iteration that polls again
           sh.stop[sq] = (!p1 && sh.n2[sq] == 0 && k.fnext >= k.ftail) ? 1 : 0;
@@ -835,6 +870,10 @@ __global__ void __launch_bounds__(kLambThreads, kLambCtasPerSm) k_lamb(LambArgs 
   float* stash = reinterpret_cast<float*>(dyn_smem + (size_t)kLambStages * kLambStageBytes);
   const LambScalars s{a.hp[0], a.hp[1], a.hp[2]};
   const unsigned tag = __ldcg(pl.tag_word()) + 1u;  // this launch's tag
+#ifdef SP_LAMB_TRACE
+  if (threadIdx.x == 0 && pl.trace)
+    for (int k = 5; k < 8; ++k) pl.trace[(size_t)blockIdx.x * kLambTraceStride + k] = 0;
+#endif
   LAMB_STAMP(0);
   if (!pl.shard) stream_replicated<W, FP>(a, s, pl, stages, stash, sh, tag);
   else shard_lamb<W, FP>(a, s, pl, stages, stash, sh, tag);

@@ -53,6 +53,10 @@ def main():
         print(f"{name:20s} min/med/max {x.min():7.1f} {np.median(x):7.1f} {x.max():7.1f}")
     print(f"chunks not stashed: {int(t[:, 4].sum())} (max per CTA {int(t[:, 4].max())})")
     print(f"tail after the last pass-1 count: {span - rel[:, 1].max():.1f} us")
+    drain0 = (t[:, 7] - t0) / 1e3
+    print(f"first iteration without a pass-1 chunk: min/med/max {drain0.min():.1f} {np.median(drain0):.1f} "
+          f"{drain0.max():.1f} us; per CTA: empty iterations median {np.median(t[:, 5]):.0f} "
+          f"(max {t[:, 5].max()}), pass-2-only iterations median {np.median(t[:, 6]):.0f} (max {t[:, 6].max()})")
     # per-iteration phases (SM clocks): 0 top, 1 stage landed, 2 pass 1 done,
     # 3 pass 2 done, 4 after the barrier (thread 0), 5 descriptor landed,
     # 6 slot filled and pass-2 entries picked, 7 copies issued
