@@ -26,7 +26,7 @@ namespace sp {
 // so one CTA of 16 data warps per SM streams at HBM speed); the rest of the
 // SM's shared memory is the u stash.
 #ifndef SP_LAMB_WARPS
-#define SP_LAMB_WARPS 16
+#define SP_LAMB_WARPS 12
 #endif
 #ifndef SP_LAMB_CTAS
 #define SP_LAMB_CTAS 1
@@ -34,19 +34,24 @@ namespace sp {
 #ifndef SP_LAMB_STAGES
 #define SP_LAMB_STAGES 2
 #endif
+#ifndef SP_LAMB_VEC
+#define SP_LAMB_VEC 2
+#endif
 constexpr int kLambDataWarps = SP_LAMB_WARPS;
 constexpr int kLambDataThreads = kLambDataWarps * 32;
 constexpr int kLambThreads = kLambDataThreads + 64;
 constexpr int kLambCtasPerSm = SP_LAMB_CTAS;
 constexpr int kLambStages = SP_LAMB_STAGES;
-constexpr int kLambTile = kLambDataThreads * 4;  // max chunk length: one float4 per data thread
+constexpr int kLambVec = SP_LAMB_VEC;                    // float4 per data thread per array
+constexpr int kLambTile = kLambDataThreads * 4 * kLambVec;  // max chunk length
 // one stage: g (wire bytes or fp32, plus 16 bytes of slack for an aligned
 // superset of a wire range), p, m, v of the pass-1 chunk, and p of the
 // iteration's pass-2 chunk (an iteration without a pass-1 chunk puts the p
 // of up to four pass-2 chunks into the g, p, m, v areas instead)
-constexpr int kLambStageG = kLambDataThreads * 16 + 16;
-constexpr int kLambStageP2 = kLambStageG + 3 * kLambDataThreads * 16;
-constexpr int kLambStageBytes = kLambStageP2 + kLambDataThreads * 16;
+constexpr int kLambArea = kLambTile * 4;  // one fp32 array of a chunk
+constexpr int kLambStageG = kLambArea + 16;
+constexpr int kLambStageP2 = kLambStageG + 3 * kLambArea;
+constexpr int kLambStageBytes = kLambStageP2 + kLambArea;
 constexpr int kPad = 16384;         // wire/avg buffers padded to this multiple
 
 struct BarrierArgs {

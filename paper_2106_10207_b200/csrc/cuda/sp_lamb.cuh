@@ -74,7 +74,7 @@ namespace sp {
 
 constexpr int kFifo = 64;  // chunks a CTA holds for pass 2 at once (more: overflow)
 constexpr int kDrain = 4;  // pass-2 entries per iteration without a pass-1 chunk
-constexpr int kSlots = kLambStages + 1;  // iteration i uses slot i % kSlots
+constexpr int kSlots = kLambStages + 2;  // iteration i uses slot i % kSlots
 constexpr int kCtlWarp = kLambDataWarps, kBooksWarp = kLambDataWarps + 1;
 
 struct LambPlan {
@@ -288,20 +288,24 @@ __device__ __forceinline__ void p1_staged(const LambArgs& a, const LambScalars& 
     pp = __fmaf_rn(ps, ps, pp);
     uu = __fmaf_rn(us, us, uu);
   }
-  if (t < sp.nbody4) {
-    const int64_t i = b0 + 4 * (int64_t)t;
-    GradRaw g;
-    if constexpr (FP || W == SP_WIRE_FP32) {
-      g.f = reinterpret_cast<const float4*>(stg)[t];
-    } else if constexpr (W == SP_WIRE_FP16) {
-      g.h = *reinterpret_cast<const uint2*>(stg + goff + 8 * t);
-    } else {
-      g.q = *reinterpret_cast<const uint32_t*>(stg + goff + 4 * t);
-      g.s = a.avg_scale[i >> a.qshift];
+#pragma unroll
+  for (int j = 0; j < kLambVec; ++j) {
+    const int v = t + j * kLambDataThreads;  // body vector
+    if (v < sp.nbody4) {
+      const int64_t i = b0 + 4 * (int64_t)v;
+      GradRaw g;
+      if constexpr (FP || W == SP_WIRE_FP32) {
+        g.f = reinterpret_cast<const float4*>(stg)[v];
+      } else if constexpr (W == SP_WIRE_FP16) {
+        g.h = *reinterpret_cast<const uint2*>(stg + goff + 8 * v);
+      } else {
+        g.q = *reinterpret_cast<const uint32_t*>(stg + goff + 4 * v);
+        g.s = a.avg_scale[i >> a.qshift];
+      }
+      const float4* pmv = reinterpret_cast<const float4*>(stg + kLambStageG);
+      p1_vec<W, FP>(a, s, i, grad_finish<W, FP>(a, i, g), pmv[v], pmv[kLambTile / 4 + v],
+                    pmv[2 * (kLambTile / 4) + v], st ? st + (i - c.start) : nullptr, pp, uu);
     }
-    const float4* pmv = reinterpret_cast<const float4*>(stg + kLambStageG);
-    p1_vec<W, FP>(a, s, i, grad_finish<W, FP>(a, i, g), pmv[t], pmv[kLambDataThreads + t],
-                  pmv[2 * kLambDataThreads + t], st ? st + (i - c.start) : nullptr, pp, uu);
   }
 }
 
@@ -320,7 +324,7 @@ __device__ __forceinline__ float4 dir4(const LambArgs& a, const LambScalars& s, 
 // Loads of a pass-2 chunk's body issued ahead of their use: m', v' (no
 // stash), or p (p not staged).
 struct P2Regs {
-  float4 m, v;
+  float4 m[kLambVec], v[kLambVec];
 };
 __device__ __forceinline__ const P2Regs& r0_dummy() {
   static __device__ P2Regs z;
@@ -329,17 +333,23 @@ __device__ __forceinline__ const P2Regs& r0_dummy() {
 
 __device__ __forceinline__ void p2_load_p(const LambArgs& a, long long start, int len, P2Regs& r) {
   const ChunkSplit sp = split_chunk(start, len);
-  const int t = threadIdx.x;
-  if (t < sp.nbody4) r.m = *reinterpret_cast<const float4*>(a.p + sp.start + sp.head + 4 * (int64_t)t);
+#pragma unroll
+  for (int j = 0; j < kLambVec; ++j) {
+    const int v = threadIdx.x + j * kLambDataThreads;
+    if (v < sp.nbody4) r.m[j] = *reinterpret_cast<const float4*>(a.p + sp.start + sp.head + 4 * (int64_t)v);
+  }
 }
 
 __device__ __forceinline__ void p2_load_mv(const LambArgs& a, long long start, int len, P2Regs& r) {
   const ChunkSplit sp = split_chunk(start, len);
-  const int t = threadIdx.x;
-  if (t < sp.nbody4) {
-    const int64_t i = sp.start + sp.head + 4 * (int64_t)t;
-    r.m = *reinterpret_cast<const float4*>(a.m + i);
-    r.v = *reinterpret_cast<const float4*>(a.v + i);
+#pragma unroll
+  for (int j = 0; j < kLambVec; ++j) {
+    const int v = threadIdx.x + j * kLambDataThreads;
+    if (v < sp.nbody4) {
+      const int64_t i = sp.start + sp.head + 4 * (int64_t)v;
+      r.m[j] = *reinterpret_cast<const float4*>(a.m + i);
+      r.v[j] = *reinterpret_cast<const float4*>(a.v + i);
+    }
   }
 }
 
@@ -360,14 +370,18 @@ __device__ __forceinline__ void p2_staged(const LambArgs& a, const LambScalars& 
     const float u = st ? st[si - start] : lamb_dir(a, s, p, a.m[si], a.v[si]);
     a.p[si] = __fmaf_rn(neg, u, p);
   }
-  if (t < sp.nbody4) {
-    const int64_t i = b0 + 4 * (int64_t)t;
-    const float4 p = ps ? ps[t] : mv.m;
-    float4 u;
-    if (st) u = *reinterpret_cast<const float4*>(st + (i - start));
-    else if (have_mv) u = dir4(a, s, p, mv.m, mv.v);
-    else u = dir4(a, s, p, *reinterpret_cast<const float4*>(a.m + i), *reinterpret_cast<const float4*>(a.v + i));
-    *reinterpret_cast<float4*>(a.p + i) = p2_vec(neg, p, u);
+#pragma unroll
+  for (int j = 0; j < kLambVec; ++j) {
+    const int v = t + j * kLambDataThreads;
+    if (v < sp.nbody4) {
+      const int64_t i = b0 + 4 * (int64_t)v;
+      const float4 p = ps ? ps[v] : mv.m[j];
+      float4 u;
+      if (st) u = *reinterpret_cast<const float4*>(st + (i - start));
+      else if (have_mv) u = dir4(a, s, p, mv.m[j], mv.v[j]);
+      else u = dir4(a, s, p, *reinterpret_cast<const float4*>(a.m + i), *reinterpret_cast<const float4*>(a.v + i));
+      *reinterpret_cast<float4*>(a.p + i) = p2_vec(neg, p, u);
+    }
   }
 }
 
@@ -392,19 +406,23 @@ __device__ __forceinline__ void p2_chunk(const LambArgs& a, const LambScalars& s
     else
       a.p[si] = q;
   }
-  if (t < sp.nbody4) {
-    const int64_t i = b0 + 4 * (int64_t)t;
-    const float4 p = *reinterpret_cast<const float4*>(a.p + i);
-    const float4 u = st ? *reinterpret_cast<const float4*>(st + (i - start))
-                        : dir4(a, s, p, *reinterpret_cast<const float4*>(a.m + i),
-                               *reinterpret_cast<const float4*>(a.v + i));
-    const float4 q = p2_vec(neg, p, u);
-    if (push) {
-      const int4 o = make_int4(__float_as_int(q.x), __float_as_int(q.y), __float_as_int(q.z),
-                               __float_as_int(q.w));
-      for (int j = 0; j < push->ndst; ++j) st_v4(push->dst[j] + i, o);
-    } else {
-      *reinterpret_cast<float4*>(a.p + i) = q;
+#pragma unroll
+  for (int jv = 0; jv < kLambVec; ++jv) {
+    const int v = t + jv * kLambDataThreads;
+    if (v < sp.nbody4) {
+      const int64_t i = b0 + 4 * (int64_t)v;
+      const float4 p = *reinterpret_cast<const float4*>(a.p + i);
+      const float4 u = st ? *reinterpret_cast<const float4*>(st + (i - start))
+                          : dir4(a, s, p, *reinterpret_cast<const float4*>(a.m + i),
+                                 *reinterpret_cast<const float4*>(a.v + i));
+      const float4 q = p2_vec(neg, p, u);
+      if (push) {
+        const int4 o = make_int4(__float_as_int(q.x), __float_as_int(q.y), __float_as_int(q.z),
+                                 __float_as_int(q.w));
+        for (int j = 0; j < push->ndst; ++j) st_v4(push->dst[j] + i, o);
+      } else {
+        *reinterpret_cast<float4*>(a.p + i) = q;
+      }
     }
   }
 }
@@ -469,7 +487,8 @@ struct Books {
 };
 
 struct StreamShared {
-  unsigned long long full[kLambStages];  // stage mbarriers: bulk copies landed
+  unsigned long long full[kLambStages];   // stage mbarriers: slot filled and its bulk copies landed
+  unsigned long long empty[kLambStages];  // stage mbarriers: every data warp done with the iteration
   float red_p[kSlots][kLambDataWarps], red_u[kSlots][kLambDataWarps];
   Chunk desc[kSlots];            // pass-1 chunk of the iteration
   int idx[kSlots];               // its index (>= nchunks: none)
@@ -482,6 +501,8 @@ struct StreamShared {
   FifoEntry fifo[kFifo];
   Chunk pdesc[2];                // descriptors prefetched by cp.async, two steps ahead
   int nfifo;                     // FIFO entries of the loop (sharded pass 2)
+  volatile int books_done;       // iterations the books lane has finished
+  volatile int iters_done;       // iterations every data warp has finished (claims lane)
   int k, flag;
   unsigned long long epoch;
 };
@@ -489,7 +510,7 @@ struct StreamShared {
 // Stage offset of pass-2 entry j's p: beside a pass-1 chunk the p2 area;
 // else the g, p, m, v areas.
 __device__ __forceinline__ int p2_area(bool p1, int j) {
-  return p1 ? kLambStageP2 : (j == 0 ? 0 : kLambStageG + (j - 1) * kLambDataThreads * 16);
+  return p1 ? kLambStageP2 : (j == 0 ? 0 : kLambStageG + (j - 1) * kLambArea);
 }
 
 // Claims lane: chunk c (descriptor ch; >= nchunks: none) into slot q,
@@ -527,8 +548,8 @@ __device__ __forceinline__ void stream_fill(const LambArgs& a, const LambPlan& p
     mbar_expect_tx(bar, gbytes + 48 * nb);
     bulk_g2s(stg, gsrc, gbytes, bar);
     bulk_g2s(stg + kLambStageG, a.p + b0, 16 * nb, bar);
-    bulk_g2s(stg + kLambStageG + kLambDataThreads * 16, a.m + b0, 16 * nb, bar);
-    bulk_g2s(stg + kLambStageG + 2 * kLambDataThreads * 16, a.v + b0, 16 * nb, bar);
+    bulk_g2s(stg + kLambStageG + kLambArea, a.m + b0, 16 * nb, bar);
+    bulk_g2s(stg + kLambStageG + 2 * kLambArea, a.v + b0, 16 * nb, bar);
   }
   int off = -2;
   if (k.ftail - k.fhead < kFifo) {
@@ -637,12 +658,17 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
   if (wid == kCtlWarp && lane == 0) {
     k.ready_t = -1;
     k.probe_t = -1;
+    sh.books_done = 0;
+    sh.iters_done = 0;
     for (int q = 0; q < kSlots; ++q) {
       sh.stop[q] = 0;
       sh.n2[q] = 0;
       sh.idx[q] = pl.nchunks;
     }
-    for (int st = 0; st < kLambStages; ++st) mbar_init(&sh.full[st], 1);
+    for (int st = 0; st < kLambStages; ++st) {
+      mbar_init(&sh.full[st], 1);
+      mbar_init(&sh.empty[st], kLambDataWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int q = 0; q < kLambStages; ++q) {
       const int c = claim();
@@ -659,118 +685,164 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
     pend = claim();
   }
   __syncthreads();
-  for (int it = 0;; ++it) {
-    const int q = it % kSlots, stage = it % kLambStages;
-    if (sh.stop[q]) break;
-    const int item = sh.idx[q];
-    const bool have1 = item < pl.nchunks;
-    const int n2 = sh.n2[q];
-    if (wid < kLambDataWarps) {
-      float pp = 0.0f, uu = 0.0f;
-      const unsigned char* stg = stages + (size_t)stage * kLambStageBytes;
-#ifdef SP_LAMB_TRACE
-      if (tid == 0 && pl.trace && !have1) {  // iterations without a pass-1 chunk: empty, drain
-        unsigned long long* tw = pl.trace + (size_t)blockIdx.x * kLambTraceStride;
-        if (tw[7] == 0) tw[7] = globaltimer();
-        ++tw[n2 ? 6 : 5];
-      }
-#endif
+  if (wid < kLambDataWarps) {
+    // Data warps: each runs the iterations on its own, waiting only for the
+    // slot and stage of the next one (full) and reporting each one done
+    // (empty).
+    for (int it = 0;; ++it) {
+      const int q = it % kSlots, stage = it % kLambStages;
+      const unsigned ph = (unsigned)(it / kLambStages) & 1u;
       if (tid == 0) LAMB_ITER(it, 0);
-      if (have1) {
-        // Beside the pass-1 chunk up to two pass-2 entries: the first with
-        // its p staged (and m', v' loaded here if it has no stash), the
-        // second (stashed) with its p loaded here; these loads are in
-        // flight during the pass-1 math, which reads only shared memory.
-        P2Regs r0, r1;
-        const bool mv0 = n2 >= 1 && sh.e2[q][0].off < 0;
-        if (mv0) p2_load_mv(a, sh.e2[q][0].start, sh.e2[q][0].len, r0);
-        if (n2 == 2) p2_load_p(a, sh.e2[q][1].start, sh.e2[q][1].len, r1);
-        mbar_wait(&sh.full[stage], (unsigned)(it / kLambStages) & 1u);
-        if (tid == 0) LAMB_ITER(it, 1);
-        const int off = sh.off[q];
-        p1_staged<W, FP>(a, s, sh.desc[q], stg, sh.goff[q], off >= 0 ? stash + off : nullptr, pp, uu);
-        if (tid == 0) LAMB_ITER(it, 2);
-        if (n2 >= 1) {
-          const FifoEntry& e = sh.e2[q][0];
-          p2_staged(a, s, e.start, e.len, reinterpret_cast<const float4*>(stg + p2_area(true, 0)),
-                    e.off >= 0 ? stash + e.off : nullptr, sh.neg2[q][0], mv0, r0);
+      mbar_wait(&sh.full[stage], ph);
+      if (tid == 0) LAMB_ITER(it, 1);
+      const bool stop = sh.stop[q] != 0;
+      if (!stop) {
+        const int item = sh.idx[q];
+        const bool have1 = item < pl.nchunks;
+        const int n2 = sh.n2[q];
+        float pp = 0.0f, uu = 0.0f;
+        const unsigned char* stg = stages + (size_t)stage * kLambStageBytes;
+#ifdef SP_LAMB_TRACE
+        if (tid == 0 && pl.trace && !have1) {  // iterations without a pass-1 chunk: empty, drain
+          unsigned long long* tw = pl.trace + (size_t)blockIdx.x * kLambTraceStride;
+          if (tw[7] == 0) tw[7] = globaltimer();
+          ++tw[n2 ? 6 : 5];
         }
-        if (n2 == 2) {
-          const FifoEntry& e = sh.e2[q][1];
-          p2_staged(a, s, e.start, e.len, nullptr, stash + e.off, sh.neg2[q][1], true, r1);
+#endif
+        if (have1) {
+          // Beside the pass-1 chunk up to two pass-2 entries: the first with
+          // its p staged (and m', v' loaded here if it has no stash), the
+          // second (stashed) with its p loaded here; these loads are in
+          // flight during the pass-1 math, which reads only shared memory.
+          P2Regs r0, r1;
+          const bool mv0 = n2 >= 1 && sh.e2[q][0].off < 0;
+          if (mv0) p2_load_mv(a, sh.e2[q][0].start, sh.e2[q][0].len, r0);
+          if (n2 == 2) p2_load_p(a, sh.e2[q][1].start, sh.e2[q][1].len, r1);
+          const int off = sh.off[q];
+          p1_staged<W, FP>(a, s, sh.desc[q], stg, sh.goff[q], off >= 0 ? stash + off : nullptr, pp, uu);
+          if (tid == 0) LAMB_ITER(it, 2);
+          if (n2 >= 1) {
+            const FifoEntry& e = sh.e2[q][0];
+            p2_staged(a, s, e.start, e.len, reinterpret_cast<const float4*>(stg + p2_area(true, 0)),
+                      e.off >= 0 ? stash + e.off : nullptr, sh.neg2[q][0], mv0, r0);
+          }
+          if (n2 == 2) {
+            const FifoEntry& e = sh.e2[q][1];
+            p2_staged(a, s, e.start, e.len, nullptr, stash + e.off, sh.neg2[q][1], true, r1);
+          }
+        } else {
+          for (int j = 0; j < n2; ++j) {  // pass 2 only
+            const FifoEntry& e = sh.e2[q][j];
+            p2_staged(a, s, e.start, e.len, reinterpret_cast<const float4*>(stg + p2_area(false, j)),
+                      e.off >= 0 ? stash + e.off : nullptr, sh.neg2[q][j], false, r0_dummy());
+          }
         }
-      } else if (n2 > 0) {
-        mbar_wait(&sh.full[stage], (unsigned)(it / kLambStages) & 1u);
-        for (int j = 0; j < n2; ++j) {  // pass 2 only
-          const FifoEntry& e = sh.e2[q][j];
-          p2_staged(a, s, e.start, e.len, reinterpret_cast<const float4*>(stg + p2_area(false, j)),
-                    e.off >= 0 ? stash + e.off : nullptr, sh.neg2[q][j], false, r0_dummy());
+        if (tid == 0) LAMB_ITER(it, 3);
+        pp = warp_sum(pp);
+        uu = warp_sum(uu);
+        if (lane == 0) {
+          sh.red_p[q][wid] = pp;
+          sh.red_u[q][wid] = uu;
         }
       }
-      if (tid == 0) LAMB_ITER(it, 3);
-      pp = warp_sum(pp);
-      uu = warp_sum(uu);
-      if (lane == 0) {
-        sh.red_p[q][wid] = pp;
-        sh.red_u[q][wid] = uu;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.empty[stage]);
+      if (tid == 0) LAMB_ITER(it, 4);
+      if (stop) break;
+    }
+  } else if (wid == kCtlWarp) {
+    // Claims lane: once every data warp is done with iteration it, the slot
+    // and stage of iteration it + stages. The whole warp loops (a barrier
+    // after the loop needs it converged); lane 0 does the work and returns
+    // 1 once it has produced the stop.
+    auto claims_step = [&](int it) -> int {
+      const int q = it % kSlots, stage = it % kLambStages;
+      mbar_wait(&sh.empty[stage], (unsigned)(it / kLambStages) & 1u);
+      sh.iters_done = it + 1;  // for the books lane (a counter: it may lag several phases)
+      LAMB_ITER(it, 5);
+      const int n2 = sh.n2[q];
+      if (n2 > 0) {  // free the entries pass 2 just finished and their ring regions
+        for (int j = 0; j < n2; ++j) {
+          if (sh.fifo[k.fhead % kFifo].off >= 0) --k.ring.live;
+          ++k.fhead;
+        }
+        for (int f = k.fhead; f < k.ftail; ++f)  // the oldest live region
+          if (sh.fifo[f % kFifo].off >= 0) {
+            k.ring.head = sh.fifo[f % kFifo].off;
+            break;
+          }
+      }
+      const int sq = (it + kLambStages) % kSlots;
+      // the slot was last used by iteration it + stages - kSlots: the books
+      // lane must be done with it
+      while (sh.books_done < it + kLambStages - kSlots + 1) {
+      }
+      // the ready word of the FIFO head's tensor, unless known: in flight
+      // while the slot is filled
+      k.probe_t = -1;
+      if (k.fnext < k.ftail && sh.fifo[k.fnext % kFifo].tensor != k.ready_t)
+        k.probe_t = sh.fifo[k.fnext % kFifo].tensor;
+      probe = ld_relaxed_u64(pl.ready(k.probe_t >= 0 ? k.probe_t : 0));
+      const int b = it & 1;  // the buffer fetched two steps ago
+      const int c = k.pdesc[b];
+      cp_async_wait_1();
+      unsigned char* stg = stages + (size_t)stage * kLambStageBytes;
+      stream_fill<W, FP>(a, pl, k, sq, c, sh.pdesc[b], stg, &sh.full[stage], sh);
+      // the descriptor of the claim issued last step; claim again
+      const int cn = k.claims_done ? pl.nchunks : pend;
+      if (cn >= pl.nchunks) k.claims_done = 1;
+      fetch_desc(b, cn);
+      pend = claim();  // past the end once the queue is exhausted: harmless, reset at exit
+      const bool p1 = c < pl.nchunks;
+      int stop;
+      if (pl.shard) {
+        sh.n2[sq] = 0;
+        stop = p1 ? 0 : 1;
+      } else {
+        if (k.probe_t >= 0 && (unsigned)(probe >> 32) == tag) {
+          k.ready_t = k.probe_t;
+          k.ready_neg = -__uint_as_float((unsigned)probe);
+        }
+        pick2(sq, p1 ? 2 : kDrain, p1, stg, &sh.full[stage]);
+        // nothing left: no chunk, no entry now or later; else (an entry's
+        // tensor not ready yet) an empty iteration that polls again
+        stop = (!p1 && sh.n2[sq] == 0 && k.fnext >= k.ftail) ? 1 : 0;
+        if (!p1 && sh.n2[sq] == 0 && !stop) __nanosleep(100);
+      }
+      sh.stop[sq] = stop;
+      LAMB_ITER(it, 6);
+      mbar_arrive(&sh.full[stage]);  // iteration it + stages is ready
+      LAMB_ITER(it, 7);
+      return stop;
+    };
+    for (int it = 0;; ++it) {
+      int brk = 0;
+      if (lane == 0) brk = claims_step(it);
+      if (__shfl_sync(0xffffffffu, brk, 0)) {
+        // the stop is iteration it + stages: keep counting the ones before
+        // it for the books lane
+        for (int j = it + 1; lane == 0 && j < it + kLambStages; ++j) {
+          mbar_wait(&sh.empty[j % kLambStages], (unsigned)(j / kLambStages) & 1u);
+          sh.iters_done = j + 1;
+        }
+        __syncwarp();
+        break;
       }
     }
-    __syncthreads();  // iteration `it` done; its stage is free
-    if (tid == 0) LAMB_ITER(it, 4);
-    if (wid == kCtlWarp) {
-      if (lane == 0) {
-        if (n2 > 0) {  // free the entries pass 2 just finished and their ring regions
-          for (int j = 0; j < n2; ++j) {
-            if (sh.fifo[k.fhead % kFifo].off >= 0) --k.ring.live;
-            ++k.fhead;
-          }
-          for (int f = k.fhead; f < k.ftail; ++f)  // the oldest live region
-            if (sh.fifo[f % kFifo].off >= 0) {
-              k.ring.head = sh.fifo[f % kFifo].off;
-              break;
-            }
-        }
-        // iteration it + stages: the chunk whose descriptor was prefetched
-        // last step, staged into the stage iteration `it` freed
-        const int sq = (it + kLambStages) % kSlots;
-        // the ready word of the FIFO head's tensor, unless known: in flight
-        // while the slot is filled
-        k.probe_t = -1;
-        if (k.fnext < k.ftail && sh.fifo[k.fnext % kFifo].tensor != k.ready_t)
-          k.probe_t = sh.fifo[k.fnext % kFifo].tensor;
-        probe = ld_relaxed_u64(pl.ready(k.probe_t >= 0 ? k.probe_t : 0));
-        const int b = it & 1;  // the buffer fetched two steps ago
-        const int c = k.pdesc[b];
-        cp_async_wait_1();
-        LAMB_ITER(it, 5);
-        unsigned char* stg = stages + (size_t)stage * kLambStageBytes;
-        stream_fill<W, FP>(a, pl, k, sq, c, sh.pdesc[b], stg, &sh.full[stage], sh);
-        // the descriptor of the claim issued last step; claim again
-        const int cn = k.claims_done ? pl.nchunks : pend;
-        if (cn >= pl.nchunks) k.claims_done = 1;
-        fetch_desc(b, cn);
-        pend = claim();  // past the end once the queue is exhausted: harmless, reset at exit
-        const bool p1 = c < pl.nchunks;
-        if (pl.shard) {
-          sh.n2[sq] = 0;
-          sh.stop[sq] = p1 ? 0 : 1;
-        } else {
-          if (k.probe_t >= 0 && (unsigned)(probe >> 32) == tag) {
-            k.ready_t = k.probe_t;
-            k.ready_neg = -__uint_as_float((unsigned)probe);
-          }
-          pick2(sq, p1 ? 2 : kDrain, p1, stg, &sh.full[stage]);
-          // nothing left: no chunk, no entry now or later; else (an entry's
-          // tensor not ready yet) an empty iteration that polls again
-          sh.stop[sq] = (!p1 && sh.n2[sq] == 0 && k.fnext >= k.ftail) ? 1 : 0;
-          if (!p1 && sh.n2[sq] == 0 && !sh.stop[sq]) __nanosleep(100);
-        }
-        LAMB_ITER(it, 6);
-        mbar_arrive(&sh.full[stage]);  // the stage of iteration it + stages is armed
-        LAMB_ITER(it, 7);
+  } else if (wid == kBooksWarp) {
+    // Books lane: once iteration it is done, its partial and count.
+    for (int it = 0;; ++it) {
+      const int q = it % kSlots;
+      // wait until every data warp is done with iteration it, or it is the
+      // stop (the claims lane sets that flag and stops counting)
+      const volatile int* stopq = &sh.stop[q];
+      while (!*stopq && sh.iters_done <= it) {
       }
-    } else if (wid == kBooksWarp) {
-      books_step(pl, s, sh, tag, q, have1, item, bk);
+      if (*stopq) break;
+      const int item = sh.idx[q];
+      books_step(pl, s, sh, tag, q, item < pl.nchunks, item, bk);
+      __syncwarp();
+      if (lane == 0) sh.books_done = it + 1;
     }
   }
   if (wid == kCtlWarp && lane == 0) sh.nfifo = k.ftail;

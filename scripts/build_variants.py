@@ -3,7 +3,7 @@
 
     python scripts/build_variants.py w16c1s3 w8c2s3 trace
 
-<name> = w<warps>c<CTAs per SM>s<stages>, or "trace" (the default
+<name> = w<warps>c<CTAs per SM>s<stages>[v<float4 per thread>], or "trace" (the default
 configuration with SP_LAMB_TRACE, for scripts/micro/lamb_trace.py).
 """
 import os
@@ -22,10 +22,12 @@ def flags(name):
     if "_" in name:  # <config>_<DIAG>: a diagnostic build (SP_DIAG_<DIAG>)
         base, diag = name.split("_", 1)
         return flags(base) + [f"-DSP_DIAG_{diag}"]
-    m = re.fullmatch(r"w(\d+)c(\d+)s(\d+)", name)
+    m = re.fullmatch(r"w(\d+)c(\d+)s(\d+)(?:v(\d+))?", name)
     if not m:
         raise SystemExit(f"bad variant {name}")
     out = [f"-DSP_LAMB_WARPS={m.group(1)}", f"-DSP_LAMB_CTAS={m.group(2)}", f"-DSP_LAMB_STAGES={m.group(3)}"]
+    if m.group(4):
+        out.append(f"-DSP_LAMB_VEC={m.group(4)}")
     return out
 
 

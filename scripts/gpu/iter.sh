@@ -2,7 +2,7 @@
 # timeline, the k_lamb configuration variants
 mkdir -p gpurun_out
 export SP_SKIP_BUILD=1
-timeout 1200 python -m pytest tests/test_round_gpu.py tests/test_pybind_round.py -q --timeout 300 -x > gpurun_out/it_test.log 2>&1
+timeout 400 python -m pytest tests/test_round_gpu.py tests/test_pybind_round.py -q --timeout 60 -x > gpurun_out/it_test.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/it_test.log
 timeout 300 python scripts/micro/lamb_trace.py build/variants/trace/libsp_round.so albert-large fp16 > gpurun_out/it_trace_fp16.txt 2>&1
 bash scripts/gpu/variants.sh

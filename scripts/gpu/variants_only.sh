@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+export SP_SKIP_BUILD=1
+bash scripts/gpu/variants.sh

@@ -57,22 +57,20 @@ def main():
     print(f"first iteration without a pass-1 chunk: min/med/max {drain0.min():.1f} {np.median(drain0):.1f} "
           f"{drain0.max():.1f} us; per CTA: empty iterations median {np.median(t[:, 5]):.0f} "
           f"(max {t[:, 5].max()}), pass-2-only iterations median {np.median(t[:, 6]):.0f} (max {t[:, 6].max()})")
-    # per-iteration phases (SM clocks): 0 top, 1 stage landed, 2 pass 1 done,
-    # 3 pass 2 done, 4 after the barrier (thread 0), 5 descriptor landed,
-    # 6 slot filled and pass-2 entries picked, 7 copies issued
+    # per-iteration phases (SM clocks): data warp 0: 0 top, 1 slot and stage
+    # ready, 2 pass 1 done, 3 pass 2 done, 4 reported done; claims lane: 5
+    # iteration reported done by every data warp, 6 next slot filled, 7 armed
     it = tr[:, 64:].reshape(grid, 128, 8).astype(np.float64)
     ok = (it[:, :-1, 0] > 0) & (it[:, 1:, 0] > 0)
     d = lambda a, b: (it[:, :-1, b] - it[:, :-1, a])[ok]
     per = (it[:, 1:, 0] - it[:, :-1, 0])[ok]
-    print(f"iterations traced: {int(ok.sum())}; cycles per iteration median {np.median(per):.0f} "
-          f"(mean {per.mean():.0f})")
-    for (a, b, name) in ((0, 1, "wait for the stage"), (1, 2, "pass 1"), (2, 3, "pass 2"),
-                         (3, 4, "barrier (thread 0)"), (4, 5, "claims: desc wait"), (5, 6, "claims: fill+pick"),
-                         (6, 7, "claims: stage copies"), (4, 7, "claims step")):
+    print(f"iterations traced: {int(ok.sum())}; cycles per iteration median {np.median(per):.0f}")
+    for (a, b, name) in ((0, 1, "wait for slot+stage"), (1, 2, "pass 1"), (2, 3, "pass 2"),
+                         (3, 4, "reduce + report"), (4, 5, "last warp -> claims"), (5, 6, "claims: fill+pick"),
+                         (6, 7, "claims: arm")):
         x = d(a, b)
         print(f"  {name:22s} median {np.median(x):8.0f}  mean {x.mean():8.0f}  p90 {np.percentile(x, 90):8.0f}")
-    nxt = (it[:, 1:, 0] - it[:, :-1, 4])[ok]
-    print(f"  {'barrier -> next top':22s} median {np.median(nxt):8.0f}  mean {nxt.mean():8.0f}")
+
     r.close()
 
 
