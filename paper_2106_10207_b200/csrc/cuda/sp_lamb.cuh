@@ -427,6 +427,56 @@ __device__ __forceinline__ void p2_chunk(const LambArgs& a, const LambScalars& s
   }
 }
 
+// Sharded pass 2 of a FIFO entry in two halves: the body loads (p, and m',
+// v' without stash), then the update stored to every rank's copy.
+struct P2Full {
+  float4 p[kLambVec], m[kLambVec], v[kLambVec];
+};
+
+template <typename E>
+__device__ __forceinline__ void p2_load_full(const LambArgs& a, const E& e, P2Full& r) {
+#pragma unroll
+  for (int j = 0; j < kLambVec; ++j) {
+    const int v = threadIdx.x + j * kLambDataThreads;
+    if (v < e.nb) {
+      const int64_t i = e.b0 + 4 * (int64_t)v;
+      r.p[j] = *reinterpret_cast<const float4*>(a.p + i);
+      if (e.off < 0) {
+        r.m[j] = *reinterpret_cast<const float4*>(a.m + i);
+        r.v[j] = *reinterpret_cast<const float4*>(a.v + i);
+      }
+    }
+  }
+}
+
+template <typename E>
+__device__ __forceinline__ void p2_finish_full(const LambArgs& a, const LambScalars& s, const E& e,
+                                               const float* st, float neg, const ParamPush* push, const P2Full& r) {
+  const int t = threadIdx.x;
+  const int head = (int)(e.b0 - e.start), tail = e.len - head - 4 * e.nb;
+  int64_t si = -1;
+  if (t < head) si = e.start + t;
+  else if (t >= 32 && t - 32 < tail) si = e.b0 + 4 * (int64_t)e.nb + (t - 32);
+  if (si >= 0) {
+    const float ps = a.p[si];
+    const float us = st ? st[si - e.start] : lamb_dir(a, s, ps, a.m[si], a.v[si]);
+    const float q = __fmaf_rn(neg, us, ps);
+    for (int k = 0; k < push->ndst; ++k) push->dst[k][si] = q;
+  }
+#pragma unroll
+  for (int j = 0; j < kLambVec; ++j) {
+    const int v = t + j * kLambDataThreads;
+    if (v < e.nb) {
+      const int64_t i = e.b0 + 4 * (int64_t)v;
+      const float4 u = st ? *reinterpret_cast<const float4*>(st + (i - e.start)) : dir4(a, s, r.p[j], r.m[j], r.v[j]);
+      const float4 q = p2_vec(neg, r.p[j], u);
+      const int4 o = make_int4(__float_as_int(q.x), __float_as_int(q.y), __float_as_int(q.z),
+                               __float_as_int(q.w));
+      for (int k = 0; k < push->ndst; ++k) st_v4(push->dst[k] + i, o);
+    }
+  }
+}
+
 // -lr * trust of tensor t for the overflow and sharded pass 2 (the same bits
 // everywhere: replicated, the published lr * trust; sharded, the world's
 // pairs summed in rank order).
@@ -925,10 +975,19 @@ __device__ void shard_lamb(const LambArgs& a, const LambScalars& s, const LambPl
     while (ld_acquire_gpu(reinterpret_cast<const unsigned*>(pl.release_flag())) == 0u) __nanosleep(32);
   __syncthreads();
   LAMB_STAMP(2);
-  const int nf = sh.nfifo;  // every FIFO entry of this CTA (nothing was picked)
-  for (int f = 0; f < nf && tid < kLambDataThreads; ++f) {
-    const FifoEntry e = sh.fifo[f];
-    p2_chunk(a, s, e.start, e.len, e.off >= 0 ? stash + e.off : nullptr, neg_of(pl, s, e.tensor), &pl.push);
+  // pass 2 of every FIFO entry of this CTA (nothing was picked), the loads
+  // of the next entry in flight while the current one is finished
+  const int nf = sh.nfifo;
+  if (tid < kLambDataThreads && nf > 0) {
+    P2Full cur, nxt;
+    p2_load_full(a, sh.fifo[0], cur);
+    for (int f = 0; f < nf; ++f) {
+      const FifoEntry e = sh.fifo[f];
+      if (f + 1 < nf) p2_load_full(a, sh.fifo[f + 1], nxt);
+      p2_finish_full(a, s, e, e.off >= 0 ? stash + e.off : nullptr, -__ldcg(pl.step_scale + e.tensor), &pl.push,
+                     cur);
+      cur = nxt;
+    }
   }
   overflow_pass2(a, s, pl, &sh.k);
 }
