@@ -19,9 +19,6 @@ SRC = os.path.join(ROOT, "paper_2106_10207_b200", "csrc", "cuda", "sp_round.cu")
 def flags(name):
     if name == "trace":
         return ["-DSP_LAMB_TRACE"]
-    if "_" in name:  # <config>_<DIAG>: a diagnostic build (SP_DIAG_<DIAG>)
-        base, diag = name.split("_", 1)
-        return flags(base) + [f"-DSP_DIAG_{diag}"]
     m = re.fullmatch(r"w(\d+)c(\d+)s(\d+)(?:v(\d+))?", name)
     if not m:
         raise SystemExit(f"bad variant {name}")
