@@ -427,6 +427,33 @@ __device__ __forceinline__ void p2_chunk(const LambArgs& a, const LambScalars& s
   }
 }
 
+// Pass 2 of a FIFO entry with p (and, without stash, m' and v') staged
+// (replicated: p' overwrites p).
+template <typename E>
+__device__ __forceinline__ void p2_drain(const LambArgs& a, const LambScalars& s, const E& e, const float4* ps,
+                                         const float4* ms, const float4* vs, const float* st, float neg) {
+  const int t = threadIdx.x;
+  const int head = (int)(e.b0 - e.start), tail = e.len - head - 4 * e.nb;
+  int64_t si = -1;
+  if (t < head) si = e.start + t;
+  else if (t >= 32 && t - 32 < tail) si = e.b0 + 4 * (int64_t)e.nb + (t - 32);
+  if (si >= 0) {
+    const float p = a.p[si];
+    const float u = st ? st[si - e.start] : lamb_dir(a, s, p, a.m[si], a.v[si]);
+    a.p[si] = __fmaf_rn(neg, u, p);
+  }
+#pragma unroll
+  for (int j = 0; j < kLambVec; ++j) {
+    const int v = t + j * kLambDataThreads;
+    if (v < e.nb) {
+      const int64_t i = e.b0 + 4 * (int64_t)v;
+      const float4 p = ps[v];
+      const float4 u = st ? *reinterpret_cast<const float4*>(st + (i - e.start)) : dir4(a, s, p, ms[v], vs[v]);
+      *reinterpret_cast<float4*>(a.p + i) = p2_vec(neg, p, u);
+    }
+  }
+}
+
 // Sharded pass 2 of a FIFO entry in two halves: the body loads (p, and m',
 // v' without stash), then the update stored to every rank's copy.
 struct P2Full {
@@ -545,6 +572,7 @@ struct StreamShared {
   int off[kSlots];               // its stash offset (-1: recompute, -2: global overflow)
   int goff[kSlots];              // its first body gradient in the stage's g area
   FifoEntry e2[kSlots][kDrain];  // pass-2 entries of the iteration (kDrain >= 2)
+  int area2[kSlots][kDrain];     // without a pass-1 chunk: each entry's first stage area
   float neg2[kSlots][kDrain];    // their -lr * trust
   int n2[kSlots];
   int stop[kSlots];              // 1: nothing left for this CTA
@@ -562,6 +590,9 @@ struct StreamShared {
 __device__ __forceinline__ int p2_area(bool p1, int j) {
   return p1 ? kLambStageP2 : (j == 0 ? 0 : kLambStageG + (j - 1) * kLambArea);
 }
+// The five fp32 areas of a stage (g, p, m, v, p2), for iterations without a
+// pass-1 chunk.
+__device__ __forceinline__ int stage_area(int k) { return k == 0 ? 0 : kLambStageG + (k - 1) * kLambArea; }
 
 // Claims lane: chunk c (descriptor ch; >= nchunks: none) into slot q,
 // its body g, p, m, v copied into stage stg (counted on bar) and its pass 2
@@ -691,15 +722,35 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
   // up to maxn FIFO entries of the tensor known ready, in FIFO order, their
   // body p copied into the stage (beside a pass-1 chunk: its p2 area; else
   // the g, p, m, v areas)
+  // In an iteration without a pass-1 chunk the five areas of the stage are
+  // shared out: p of a stashed entry takes one, p, m', v' of an entry
+  // without stash three (m', v' were written by this CTA's threads in pass
+  // 1: a proxy fence orders those stores before the bulk copies read them).
   auto pick2 = [&](int q, int maxn, bool p1, unsigned char* stg, unsigned long long* bar) {
-    int n = 0;
+    int n = 0, areas = 0;
+    bool fenced = false;
     while (n < maxn && k.fnext < k.ftail) {
       const FifoEntry& e = sh.fifo[k.fnext % kFifo];
       if (e.tensor != k.ready_t) break;
       if (p1 && n == 1 && e.off < 0) break;  // the second beside a pass-1 chunk: stashed only
+      const int need = (p1 || e.off >= 0) ? 1 : 3;
+      if (!p1 && areas + need > 5) break;
       sh.e2[q][n] = e;
       sh.neg2[q][n] = k.ready_neg;
-      if (e.nb && !(p1 && n == 1)) bulk_counted(stg + p2_area(p1, n), a.p + e.b0, 16 * (unsigned)e.nb, bar);
+      sh.area2[q][n] = areas;
+      if (e.nb && !(p1 && n == 1)) {
+        const unsigned bytes = 16 * (unsigned)e.nb;
+        bulk_counted(stg + (p1 ? kLambStageP2 : stage_area(areas)), a.p + e.b0, bytes, bar);
+        if (need == 3) {
+          if (!fenced) {
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            fenced = true;
+          }
+          bulk_counted(stg + stage_area(areas + 1), a.m + e.b0, bytes, bar);
+          bulk_counted(stg + stage_area(areas + 2), a.v + e.b0, bytes, bar);
+        }
+      }
+      areas += need;
       ++n;
       ++k.fnext;
     }
@@ -781,10 +832,13 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
             p2_staged(a, s, e.start, e.len, nullptr, stash + e.off, sh.neg2[q][1], true, r1);
           }
         } else {
-          for (int j = 0; j < n2; ++j) {  // pass 2 only
+          for (int j = 0; j < n2; ++j) {  // pass 2 only: p (and m', v') staged
             const FifoEntry& e = sh.e2[q][j];
-            p2_staged(a, s, e.start, e.len, reinterpret_cast<const float4*>(stg + p2_area(false, j)),
-                      e.off >= 0 ? stash + e.off : nullptr, sh.neg2[q][j], false, r0_dummy());
+            const int ar = sh.area2[q][j];
+            p2_drain(a, s, e, reinterpret_cast<const float4*>(stg + stage_area(ar)),
+                     e.off >= 0 ? nullptr : reinterpret_cast<const float4*>(stg + stage_area(ar + 1)),
+                     e.off >= 0 ? nullptr : reinterpret_cast<const float4*>(stg + stage_area(ar + 2)),
+                     e.off >= 0 ? stash + e.off : nullptr, sh.neg2[q][j]);
           }
         }
         if (tid == 0) LAMB_ITER(it, 3);
