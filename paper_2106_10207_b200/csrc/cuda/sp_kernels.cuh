@@ -45,13 +45,12 @@ constexpr int kLambStages = SP_LAMB_STAGES;
 constexpr int kLambVec = SP_LAMB_VEC;                    // float4 per data thread per array
 constexpr int kLambTile = kLambDataThreads * 4 * kLambVec;  // max chunk length
 // one stage: g (wire bytes or fp32, plus 16 bytes of slack for an aligned
-// superset of a wire range), p, m, v of the pass-1 chunk, and p of the
-// iteration's pass-2 chunk (an iteration without a pass-1 chunk puts the p
-// of up to four pass-2 chunks into the g, p, m, v areas instead)
+// superset of a wire range), p, m, v of the pass-1 chunk (an iteration
+// without a pass-1 chunk puts pass-2 entries into these four areas instead)
 constexpr int kLambArea = kLambTile * 4;  // one fp32 array of a chunk
 constexpr int kLambStageG = kLambArea + 16;
-constexpr int kLambStageP2 = kLambStageG + 3 * kLambArea;
-constexpr int kLambStageBytes = kLambStageP2 + kLambArea;
+constexpr int kLambStageAreas = 4;
+constexpr int kLambStageBytes = kLambStageG + 3 * kLambArea;
 constexpr int kPad = 16384;         // wire/avg buffers padded to this multiple
 
 struct BarrierArgs {

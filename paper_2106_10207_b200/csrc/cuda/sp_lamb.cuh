@@ -488,7 +488,10 @@ __device__ __forceinline__ void p2_finish_full(const LambArgs& a, const LambScal
     const float ps = a.p[si];
     const float us = st ? st[si - e.start] : lamb_dir(a, s, ps, a.m[si], a.v[si]);
     const float q = __fmaf_rn(neg, us, ps);
-    for (int k = 0; k < push->ndst; ++k) push->dst[k][si] = q;
+    if (push)
+      for (int k = 0; k < push->ndst; ++k) push->dst[k][si] = q;
+    else
+      a.p[si] = q;
   }
 #pragma unroll
   for (int j = 0; j < kLambVec; ++j) {
@@ -497,9 +500,13 @@ __device__ __forceinline__ void p2_finish_full(const LambArgs& a, const LambScal
       const int64_t i = e.b0 + 4 * (int64_t)v;
       const float4 u = st ? *reinterpret_cast<const float4*>(st + (i - e.start)) : dir4(a, s, r.p[j], r.m[j], r.v[j]);
       const float4 q = p2_vec(neg, r.p[j], u);
-      const int4 o = make_int4(__float_as_int(q.x), __float_as_int(q.y), __float_as_int(q.z),
-                               __float_as_int(q.w));
-      for (int k = 0; k < push->ndst; ++k) st_v4(push->dst[k] + i, o);
+      if (push) {
+        const int4 o = make_int4(__float_as_int(q.x), __float_as_int(q.y), __float_as_int(q.z),
+                                 __float_as_int(q.w));
+        for (int k = 0; k < push->ndst; ++k) st_v4(push->dst[k] + i, o);
+      } else {
+        *reinterpret_cast<float4*>(a.p + i) = q;
+      }
     }
   }
 }
@@ -585,13 +592,8 @@ struct StreamShared {
   unsigned long long epoch;
 };
 
-// Stage offset of pass-2 entry j's p: beside a pass-1 chunk the p2 area;
-// else the g, p, m, v areas.
-__device__ __forceinline__ int p2_area(bool p1, int j) {
-  return p1 ? kLambStageP2 : (j == 0 ? 0 : kLambStageG + (j - 1) * kLambArea);
-}
-// The five fp32 areas of a stage (g, p, m, v, p2), for iterations without a
-// pass-1 chunk.
+// The four fp32 areas of a stage (g, p, m, v): in iterations without a
+// pass-1 chunk they hold pass-2 entries.
 __device__ __forceinline__ int stage_area(int k) { return k == 0 ? 0 : kLambStageG + (k - 1) * kLambArea; }
 
 // Claims lane: chunk c (descriptor ch; >= nchunks: none) into slot q,
@@ -734,13 +736,13 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
       if (e.tensor != k.ready_t) break;
       if (p1 && n == 1 && e.off < 0) break;  // the second beside a pass-1 chunk: stashed only
       const int need = (p1 || e.off >= 0) ? 1 : 3;
-      if (!p1 && areas + need > 5) break;
+      if (!p1 && areas + need > kLambStageAreas) break;
       sh.e2[q][n] = e;
       sh.neg2[q][n] = k.ready_neg;
       sh.area2[q][n] = areas;
-      if (e.nb && !(p1 && n == 1)) {
+      if (e.nb && !p1) {
         const unsigned bytes = 16 * (unsigned)e.nb;
-        bulk_counted(stg + (p1 ? kLambStageP2 : stage_area(areas)), a.p + e.b0, bytes, bar);
+        bulk_counted(stg + stage_area(areas), a.p + e.b0, bytes, bar);
         if (need == 3) {
           if (!fenced) {
             asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -815,17 +817,16 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
           // its p staged (and m', v' loaded here if it has no stash), the
           // second (stashed) with its p loaded here; these loads are in
           // flight during the pass-1 math, which reads only shared memory.
-          P2Regs r0, r1;
-          const bool mv0 = n2 >= 1 && sh.e2[q][0].off < 0;
-          if (mv0) p2_load_mv(a, sh.e2[q][0].start, sh.e2[q][0].len, r0);
+          P2Full r0;
+          P2Regs r1;
+          if (n2 >= 1) p2_load_full(a, sh.e2[q][0], r0);
           if (n2 == 2) p2_load_p(a, sh.e2[q][1].start, sh.e2[q][1].len, r1);
           const int off = sh.off[q];
           p1_staged<W, FP>(a, s, sh.desc[q], stg, sh.goff[q], off >= 0 ? stash + off : nullptr, pp, uu);
           if (tid == 0) LAMB_ITER(it, 2);
           if (n2 >= 1) {
             const FifoEntry& e = sh.e2[q][0];
-            p2_staged(a, s, e.start, e.len, reinterpret_cast<const float4*>(stg + p2_area(true, 0)),
-                      e.off >= 0 ? stash + e.off : nullptr, sh.neg2[q][0], mv0, r0);
+            p2_finish_full(a, s, e, e.off >= 0 ? stash + e.off : nullptr, sh.neg2[q][0], nullptr, r0);
           }
           if (n2 == 2) {
             const FifoEntry& e = sh.e2[q][1];
