@@ -544,8 +544,9 @@ def main():
         dk = dominant_kernel(phc, mc, world, L, n, b, shard, peak)
         dom = dk["kernel"]
         widx = {"fp32": 0, "fp16": 1, "q8": 2}[wire]
+        fused = world == 1 and L == 1 and wire != "q8"  # the pack runs inside k_lamb<W, true>
         kname = {"pack_ms": f"k_pack_{wire}", "reduce_ms": f"k_reduce_{wire}",
-                 "lamb_ms": f"k_lamb<{widx}>"}[dom]
+                 "lamb_ms": f"k_lamb<{widx}, {int(fused)}>"}[dom]
         traffic = (ncu_traffic(kname) if table == "albert-large" and world == 1 and L == 1 else None)
         # whole-round roofline (per phase on the slowest rank)
         hbm_round = max(x["hbm"] for x in models)
