@@ -74,6 +74,7 @@ namespace sp {
 
 constexpr int kFifo = 64;  // chunks a CTA holds for pass 2 at once (more: overflow)
 constexpr int kDrain = 4;  // pass-2 entries per iteration without a pass-1 chunk
+constexpr int kP2Beside = 2;  // pass-2 entries beside a pass-1 chunk (3 and 4 measured no faster)
 constexpr int kSlots = kLambStages + 2;  // iteration i uses slot i % kSlots
 constexpr int kCtlWarp = kLambDataWarps, kBooksWarp = kLambDataWarps + 1;
 
@@ -734,7 +735,7 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
     while (n < maxn && k.fnext < k.ftail) {
       const FifoEntry& e = sh.fifo[k.fnext % kFifo];
       if (e.tensor != k.ready_t) break;
-      if (p1 && n == 1 && e.off < 0) break;  // the second beside a pass-1 chunk: stashed only
+      if (p1 && n >= 1 && e.off < 0) break;  // beside a pass-1 chunk, after the first: stashed only
       const int need = (p1 || e.off >= 0) ? 1 : 3;
       if (!p1 && areas + need > kLambStageAreas) break;
       sh.e2[q][n] = e;
@@ -818,9 +819,11 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
           // second (stashed) with its p loaded here; these loads are in
           // flight during the pass-1 math, which reads only shared memory.
           P2Full r0;
-          P2Regs r1;
+          P2Regs r1[kP2Beside > 1 ? kP2Beside - 1 : 1];
           if (n2 >= 1) p2_load_full(a, sh.e2[q][0], r0);
-          if (n2 == 2) p2_load_p(a, sh.e2[q][1].start, sh.e2[q][1].len, r1);
+#pragma unroll
+          for (int j = 1; j < kP2Beside; ++j)
+            if (j < n2) p2_load_p(a, sh.e2[q][j].start, sh.e2[q][j].len, r1[j - 1]);
           const int off = sh.off[q];
           p1_staged<W, FP>(a, s, sh.desc[q], stg, sh.goff[q], off >= 0 ? stash + off : nullptr, pp, uu);
           if (tid == 0) LAMB_ITER(it, 2);
@@ -828,10 +831,12 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
             const FifoEntry& e = sh.e2[q][0];
             p2_finish_full(a, s, e, e.off >= 0 ? stash + e.off : nullptr, sh.neg2[q][0], nullptr, r0);
           }
-          if (n2 == 2) {
-            const FifoEntry& e = sh.e2[q][1];
-            p2_staged(a, s, e.start, e.len, nullptr, stash + e.off, sh.neg2[q][1], true, r1);
-          }
+#pragma unroll
+          for (int j = 1; j < kP2Beside; ++j)
+            if (j < n2) {
+              const FifoEntry& e = sh.e2[q][j];
+              p2_staged(a, s, e.start, e.len, nullptr, stash + e.off, sh.neg2[q][j], true, r1[j - 1]);
+            }
         } else {
           for (int j = 0; j < n2; ++j) {  // pass 2 only: p (and m', v') staged
             const FifoEntry& e = sh.e2[q][j];
@@ -908,7 +913,7 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
           k.ready_t = k.probe_t;
           k.ready_neg = -__uint_as_float((unsigned)probe);
         }
-        pick2(sq, p1 ? 2 : kDrain, p1, stg, &sh.full[stage]);
+        pick2(sq, p1 ? kP2Beside : kDrain, p1, stg, &sh.full[stage]);
         // nothing left: no chunk, no entry now or later; else (an entry's
         // tensor not ready yet) an empty iteration that polls again
         stop = (!p1 && sh.n2[sq] == 0 && k.fnext >= k.ftail) ? 1 : 0;
