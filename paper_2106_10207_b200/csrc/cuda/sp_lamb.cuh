@@ -74,7 +74,7 @@ namespace sp {
 
 constexpr int kFifo = 64;  // chunks a CTA holds for pass 2 at once (more: overflow)
 constexpr int kDrain = 4;  // pass-2 entries per iteration without a pass-1 chunk
-constexpr int kP2Beside = 2;  // pass-2 entries beside a pass-1 chunk (3 and 4 measured no faster)
+constexpr int kP2Beside = 2;  // pass-2 entries beside a pass-1 chunk (3 and 4 measured slower)
 constexpr int kSlots = kLambStages + 2;  // iteration i uses slot i % kSlots
 constexpr int kCtlWarp = kLambDataWarps, kBooksWarp = kLambDataWarps + 1;
 
