@@ -267,45 +267,11 @@ __device__ __forceinline__ void p1_vec(const LambArgs& a, const LambScalars& s, 
   uu = __fmaf_rn(u.z, u.z, uu); uu = __fmaf_rn(u.w, u.w, uu);
 }
 
-// Pass 1 of a staged chunk in two halves: p1_take copies this thread's
-// staged g, p, m, v into registers (after which the stage may be refilled),
-// p1_compute does the math. st: the chunk's stash (indexed by element -
+// Pass 1 of a staged chunk. st: the chunk's stash (indexed by element -
 // c.start), or nullptr.
 template <int W, bool FP>
-struct P1Regs {
-  GradRaw g[kLambVec];
-  float4 p[kLambVec], m[kLambVec], v[kLambVec];
-};
-
-template <int W, bool FP>
-__device__ __forceinline__ void p1_take(const LambArgs& a, const Chunk& c, const unsigned char* stg, int goff,
-                                        P1Regs<W, FP>& r) {
-  const ChunkSplit sp = split_chunk(c.start, c.len);
-  const int t = threadIdx.x;
-  const int64_t b0 = sp.start + sp.head;
-  const float4* pmv = reinterpret_cast<const float4*>(stg + kLambStageG);
-#pragma unroll
-  for (int j = 0; j < kLambVec; ++j) {
-    const int v = t + j * kLambDataThreads;  // body vector
-    if (v < sp.nbody4) {
-      if constexpr (FP || W == SP_WIRE_FP32) {
-        r.g[j].f = reinterpret_cast<const float4*>(stg)[v];
-      } else if constexpr (W == SP_WIRE_FP16) {
-        r.g[j].h = *reinterpret_cast<const uint2*>(stg + goff + 8 * v);
-      } else {
-        r.g[j].q = *reinterpret_cast<const uint32_t*>(stg + goff + 4 * v);
-        r.g[j].s = a.avg_scale[(b0 + 4 * (int64_t)v) >> a.qshift];
-      }
-      r.p[j] = pmv[v];
-      r.m[j] = pmv[kLambTile / 4 + v];
-      r.v[j] = pmv[2 * (kLambTile / 4) + v];
-    }
-  }
-}
-
-template <int W, bool FP>
-__device__ __forceinline__ void p1_compute(const LambArgs& a, const LambScalars& s, const Chunk& c,
-                                           const P1Regs<W, FP>& r, float* st, float& pp, float& uu) {
+__device__ __forceinline__ void p1_staged(const LambArgs& a, const LambScalars& s, const Chunk& c,
+                                          const unsigned char* stg, int goff, float* st, float& pp, float& uu) {
   const ChunkSplit sp = split_chunk(c.start, c.len);
   const int t = threadIdx.x;
   const int64_t b0 = sp.start + sp.head;
@@ -325,11 +291,21 @@ __device__ __forceinline__ void p1_compute(const LambArgs& a, const LambScalars&
   }
 #pragma unroll
   for (int j = 0; j < kLambVec; ++j) {
-    const int v = t + j * kLambDataThreads;
+    const int v = t + j * kLambDataThreads;  // body vector
     if (v < sp.nbody4) {
       const int64_t i = b0 + 4 * (int64_t)v;
-      p1_vec<W, FP>(a, s, i, grad_finish<W, FP>(a, i, r.g[j]), r.p[j], r.m[j], r.v[j],
-                    st ? st + (i - c.start) : nullptr, pp, uu);
+      GradRaw g;
+      if constexpr (FP || W == SP_WIRE_FP32) {
+        g.f = reinterpret_cast<const float4*>(stg)[v];
+      } else if constexpr (W == SP_WIRE_FP16) {
+        g.h = *reinterpret_cast<const uint2*>(stg + goff + 8 * v);
+      } else {
+        g.q = *reinterpret_cast<const uint32_t*>(stg + goff + 4 * v);
+        g.s = a.avg_scale[i >> a.qshift];
+      }
+      const float4* pmv = reinterpret_cast<const float4*>(stg + kLambStageG);
+      p1_vec<W, FP>(a, s, i, grad_finish<W, FP>(a, i, g), pmv[v], pmv[kLambTile / 4 + v],
+                    pmv[2 * (kLambTile / 4) + v], st ? st + (i - c.start) : nullptr, pp, uu);
     }
   }
 }
@@ -597,7 +573,7 @@ struct Books {
 
 struct StreamShared {
   unsigned long long full[kLambStages];   // stage mbarriers: slot filled and its bulk copies landed
-  unsigned long long empty[kLambStages];  // stage mbarriers: every data warp has read the stage
+  unsigned long long empty[kLambStages];  // stage mbarriers: every data warp done with the iteration
   float red_p[kSlots][kLambDataWarps], red_u[kSlots][kLambDataWarps];
   Chunk desc[kSlots];            // pass-1 chunk of the iteration
   int idx[kSlots];               // its index (>= nchunks: none)
@@ -613,7 +589,6 @@ struct StreamShared {
   int nfifo;                     // FIFO entries of the loop (sharded pass 2)
   volatile int books_done;       // iterations the books lane has finished
   volatile int iters_done;       // iterations every data warp has finished (claims lane)
-  int done_cnt[kSlots];          // per slot: data warps done with its iteration (shared atomics)
   int k, flag;
   unsigned long long epoch;
 };
@@ -789,7 +764,6 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
     k.probe_t = -1;
     sh.books_done = 0;
     sh.iters_done = 0;
-    for (int q = 0; q < kSlots; ++q) sh.done_cnt[q] = 0;
     for (int q = 0; q < kSlots; ++q) {
       sh.stop[q] = 0;
       sh.n2[q] = 0;
@@ -851,11 +825,7 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
           for (int j = 1; j < kP2Beside; ++j)
             if (j < n2) p2_load_p(a, sh.e2[q][j].start, sh.e2[q][j].len, r1[j - 1]);
           const int off = sh.off[q];
-          P1Regs<W, FP> r;
-          p1_take<W, FP>(a, sh.desc[q], stg, sh.goff[q], r);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&sh.empty[stage]);  // the stage may be refilled now
-          p1_compute<W, FP>(a, s, sh.desc[q], r, off >= 0 ? stash + off : nullptr, pp, uu);
+          p1_staged<W, FP>(a, s, sh.desc[q], stg, sh.goff[q], off >= 0 ? stash + off : nullptr, pp, uu);
           if (tid == 0) LAMB_ITER(it, 2);
           if (n2 >= 1) {
             const FifoEntry& e = sh.e2[q][0];
@@ -868,7 +838,7 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
               p2_staged(a, s, e.start, e.len, nullptr, stash + e.off, sh.neg2[q][j], true, r1[j - 1]);
             }
         } else {
-          for (int j = 0; j < n2; ++j) {  // pass 2 only (or nothing): p (and m', v') staged
+          for (int j = 0; j < n2; ++j) {  // pass 2 only: p (and m', v') staged
             const FifoEntry& e = sh.e2[q][j];
             const int ar = sh.area2[q][j];
             p2_drain(a, s, e, reinterpret_cast<const float4*>(stg + stage_area(ar)),
@@ -876,8 +846,6 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
                      e.off >= 0 ? nullptr : reinterpret_cast<const float4*>(stg + stage_area(ar + 2)),
                      e.off >= 0 ? stash + e.off : nullptr, sh.neg2[q][j]);
           }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&sh.empty[stage]);
         }
         if (tid == 0) LAMB_ITER(it, 3);
         pp = warp_sum(pp);
@@ -888,11 +856,7 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
         }
       }
       __syncwarp();
-      if (lane == 0) {
-        if (stop) mbar_arrive(&sh.empty[stage]);  // (a pass-1 or pass-2 iteration arrived above)
-        __threadfence_block();  // the partials above before the count
-        atomicAdd(&sh.done_cnt[q], 1);
-      }
+      if (lane == 0) mbar_arrive(&sh.empty[stage]);
       if (tid == 0) LAMB_ITER(it, 4);
       if (stop) break;
     }
@@ -902,23 +866,12 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
     // after the loop needs it converged); lane 0 does the work and returns
     // 1 once it has produced the stop.
     auto claims_step = [&](int it) -> int {
-      const int stage = it % kLambStages;
-      // every data warp has read iteration it's stage: refill it
+      const int q = it % kSlots, stage = it % kLambStages;
       mbar_wait(&sh.empty[stage], (unsigned)(it / kLambStages) & 1u);
-      // iteration it - 1 finished by every data warp (warps may run ahead of
-      // each other, so the count is per slot; reset for the slot's next use,
-      // iteration it + 3, which needs this lane's step it + 1): its partial
-      // for the books lane, its pass-2 entries done
-      if (it > 0) {
-        volatile int* dc = &sh.done_cnt[(it - 1) % kSlots];
-        while (*dc < kLambDataWarps) {
-        }
-        *dc = 0;
-      }
-      sh.iters_done = it;
+      sh.iters_done = it + 1;  // for the books lane (a counter: it may lag several phases)
       LAMB_ITER(it, 5);
-      const int n2 = it > 0 ? sh.n2[(it - 1) % kSlots] : 0;
-      if (n2 > 0) {  // free those entries and their ring regions
+      const int n2 = sh.n2[q];
+      if (n2 > 0) {  // free the entries pass 2 just finished and their ring regions
         for (int j = 0; j < n2; ++j) {
           if (sh.fifo[k.fhead % kFifo].off >= 0) --k.ring.live;
           ++k.fhead;
@@ -978,10 +931,8 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
       if (__shfl_sync(0xffffffffu, brk, 0)) {
         // the stop is iteration it + stages: keep counting the ones before
         // it for the books lane
-        for (int j = it; lane == 0 && j < it + kLambStages; ++j) {
-          const volatile int* dc = &sh.done_cnt[j % kSlots];
-          while (*dc < kLambDataWarps) {
-          }
+        for (int j = it + 1; lane == 0 && j < it + kLambStages; ++j) {
+          mbar_wait(&sh.empty[j % kLambStages], (unsigned)(j / kLambStages) & 1u);
           sh.iters_done = j + 1;
         }
         __syncwarp();
