@@ -240,6 +240,42 @@ def test_phased_equals_graph():
         assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("wire,shard", [("fp16", False), ("q8", False), ("fp32", True)])
+def test_lamb_bits_do_not_depend_on_the_claim_order(wire, shard):
+    # k_lamb hands chunks out at run time and runs pass 2 whenever a tensor
+    # completes, so the chunk -> CTA map, the stash/recompute split and the
+    # order of completions differ from launch to launch: the results must
+    # not (norm partials per chunk, tensor sums in chunk order)
+    import json
+    import os
+
+    sizes = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "tensor_tables.json")))["albert-base"]
+    n = sum(sizes)
+    g = torch.empty(n, device="cuda")
+    fill_synthetic(g, 9, 0, SIGMA)
+    p0 = torch.empty(n, device="cuda")
+    fill_synthetic(p0, 10, 0, 0.02, 0)
+    rnd = AveragingRound(n, sizes, wire=wire, lr=HP["lr"], shard_lamb=shard)
+    rnd.assign([1.0], [1.0])
+    outs = []
+    for _ in range(4):
+        if shard:
+            p = rnd.param_buffer()
+            p.copy_(p0)
+        else:
+            p = p0.clone()
+        m = torch.zeros(n, device="cuda")
+        v = torch.zeros(n, device="cuda")
+        for step in (1, 2, 3):
+            rnd.run([g], p, m, v, step)
+        torch.cuda.synchronize()
+        outs.append((p.cpu().clone(), m.cpu(), v.cpu(), torch.tensor(rnd.read_trust())))
+    rnd.close()
+    for o in outs[1:]:
+        for x, y in zip(outs[0], o):
+            assert torch.equal(x, y)
+
+
 def test_bad_arguments_raise():
     rnd = AveragingRound(1000, [1000], wire="fp16", peers_per_rank=2)
     with pytest.raises(ValueError):
