@@ -77,6 +77,7 @@ constexpr int kDrain = 4;  // pass-2 entries per iteration without a pass-1 chun
 constexpr int kP2Beside = 2;  // pass-2 entries beside a pass-1 chunk (3 and 4 measured slower)
 constexpr int kSlots = kLambStages + 2;  // iteration i uses slot i % kSlots
 constexpr int kCtlWarp = kLambDataWarps, kBooksWarp = kLambDataWarps + 1;
+static_assert(kLambTile <= 6144, "a chunk's q8 scales (block >= 512) fit the 16-float staging window");
 
 struct LambPlan {
   const Chunk* chunks;            // claim order: tensor by tensor, largest first
@@ -271,7 +272,8 @@ __device__ __forceinline__ void p1_vec(const LambArgs& a, const LambScalars& s, 
 // c.start), or nullptr.
 template <int W, bool FP>
 __device__ __forceinline__ void p1_staged(const LambArgs& a, const LambScalars& s, const Chunk& c,
-                                          const unsigned char* stg, int goff, float* st, float& pp, float& uu) {
+                                          const unsigned char* stg, int goff, const float* qs, long long qs0,
+                                          float* st, float& pp, float& uu) {
   const ChunkSplit sp = split_chunk(c.start, c.len);
   const int t = threadIdx.x;
   const int64_t b0 = sp.start + sp.head;
@@ -301,7 +303,7 @@ __device__ __forceinline__ void p1_staged(const LambArgs& a, const LambScalars& 
         g.h = *reinterpret_cast<const uint2*>(stg + goff + 8 * v);
       } else {
         g.q = *reinterpret_cast<const uint32_t*>(stg + goff + 4 * v);
-        g.s = a.avg_scale[i >> a.qshift];
+        g.s = qs[(i >> a.qshift) - qs0];  // the chunk's q8 scales, staged
       }
       const float4* pmv = reinterpret_cast<const float4*>(stg + kLambStageG);
       p1_vec<W, FP>(a, s, i, grad_finish<W, FP>(a, i, g), pmv[v], pmv[kLambTile / 4 + v],
@@ -579,6 +581,8 @@ struct StreamShared {
   int idx[kSlots];               // its index (>= nchunks: none)
   int off[kSlots];               // its stash offset (-1: recompute, -2: global overflow)
   int goff[kSlots];              // its first body gradient in the stage's g area
+  alignas(16) float qs[kSlots][16];  // q8: the chunk's block scales (an aligned window)
+  long long qs0[kSlots];         // q8: block index of qs[.][0]
   FifoEntry e2[kSlots][kDrain];  // pass-2 entries of the iteration (kDrain >= 2)
   int area2[kSlots][kDrain];     // without a pass-1 chunk: each entry's first stage area
   float neg2[kSlots][kDrain];    // their -lr * trust
@@ -629,6 +633,13 @@ __device__ __forceinline__ void stream_fill(const LambArgs& a, const LambPlan& p
       goff = (int)(wb * b0 - lo);
     }
     sh.goff[q] = goff;
+    if constexpr (W == SP_WIRE_Q8 && !FP) {  // the block scales the body needs, 16-byte window
+      const int64_t s0 = b0 >> a.qshift, s1 = (b0 + 4 * (int64_t)nb - 1) >> a.qshift;
+      const int64_t lo = s0 & ~(int64_t)3;
+      const unsigned cnt = (unsigned)((s1 + 1 - lo + 3) & ~(int64_t)3);  // <= 16 (chunk <= 4096, block >= 512)
+      sh.qs0[q] = lo;
+      bulk_counted(sh.qs[q], a.avg_scale + lo, 4 * cnt, bar);
+    }
     mbar_expect_tx(bar, gbytes + 48 * nb);
     bulk_g2s(stg, gsrc, gbytes, bar);
     bulk_g2s(stg + kLambStageG, a.p + b0, 16 * nb, bar);
@@ -825,7 +836,8 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
           for (int j = 1; j < kP2Beside; ++j)
             if (j < n2) p2_load_p(a, sh.e2[q][j].start, sh.e2[q][j].len, r1[j - 1]);
           const int off = sh.off[q];
-          p1_staged<W, FP>(a, s, sh.desc[q], stg, sh.goff[q], off >= 0 ? stash + off : nullptr, pp, uu);
+          p1_staged<W, FP>(a, s, sh.desc[q], stg, sh.goff[q], sh.qs[q], sh.qs0[q], off >= 0 ? stash + off : nullptr,
+                           pp, uu);
           if (tid == 0) LAMB_ITER(it, 2);
           if (n2 >= 1) {
             const FifoEntry& e = sh.e2[q][0];

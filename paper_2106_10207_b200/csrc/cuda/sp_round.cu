@@ -655,7 +655,8 @@ int sp_round_create(const sp_round_cfg* cfg, sp_round** out) {
   r->npad = round_up(cfg->n, std::max<int64_t>(kPad, cfg->wire == SP_WIRE_Q8 ? cfg->q8_block : 1));
   r->align = cfg->wire == SP_WIRE_Q8 ? cfg->q8_block : 8;
   r->buf_bytes = (size_t)r->npad * wire_bits(cfg->wire) / 8;
-  if (cfg->wire == SP_WIRE_Q8) r->buf_bytes += round_up(r->npad / cfg->q8_block * 4, 256);
+  // q8 scales, with slack: k_lamb stages them in 16-byte windows
+  if (cfg->wire == SP_WIRE_Q8) r->buf_bytes += round_up(r->npad / cfg->q8_block * 4 + 64, 256);
   r->buf_bytes = round_up(r->buf_bytes, 256);
   r->flags_bytes = 256 + round_up((int64_t)2 * r->G * 8, 256);
   r->shared_bytes = r->flags_bytes + (size_t)(r->G + 1) * r->buf_bytes;
