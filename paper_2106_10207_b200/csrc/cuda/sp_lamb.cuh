@@ -9,43 +9,44 @@
 // element of L2 traffic on top of pass 1's 24 + b; the round-1 kernel moved
 // 44 B/element through L2 at 6.35 TB/s.
 //
-// Loads. Pass 1's g, p, m, v of a chunk are fetched by bulk async copies
-// (cp.async.bulk, completion on an mbarrier) into one of kLambStages stages
-// in shared memory, issued kLambStages - 1 iterations ahead by one thread.
-// The bytes in flight then hold no registers and do not depend on the warp
-// count: one CTA of 16 warps per SM streams pass 1 at ~6 TB/s
-// (scripts/micro/tma_stream.cu, profiles/r02/tma_stream.txt), where
+// Loads. Pass 1's g, p, m, v of a chunk (and, with the q8 wire, its block
+// scales) are fetched by bulk async copies (cp.async.bulk, completion on the
+// stage's `full` mbarrier) into one of kLambStages stages in shared memory,
+// one iteration ahead. The bytes in flight hold no registers and do not
+// depend on the warp count (scripts/micro/tma_stream.cu,
+// profiles/r02/tma_stream.txt: ~6 TB/s with 128-1024 threads per SM), where
 // register-held loads need 32 warps per SM and every register of them.
 //
 // Stash. Pass 1 keeps u in a ring buffer in the rest of the CTA's shared
-// memory, so pass 2 re-reads only p (mostly an L2 hit: it was read in pass 1
-// shortly before) and writes p': 24 + b + 8 B per element.
+// memory (sp_ring.h), so pass 2 re-reads only p (mostly an L2 hit: it was
+// read in pass 1 shortly before) and writes p': 24 + b + 8 B per element.
 //
 // Replicated mode (every rank steps the whole vector) streams: CTAs claim
 // chunks tensor by tensor (largest first) from one queue; a CTA puts u of
 // each chunk it claims into its ring and the chunk into a FIFO; a tensor's
 // norms are complete as soon as its last chunk is counted (the CTA that
 // counts it sums the chunk partials and publishes lr * trust), and from then
-// on the CTAs holding chunks of that tensor run their pass 2, one FIFO entry
-// per pass-1 chunk, interleaved with the pass-1 chunks of later tensors (the
-// entry's p loads are issued before the pass-1 math, which reads only shared
-// memory, and consumed after it). No grid-wide barrier: a chunk waits only
-// for its own tensor. A chunk for which the ring has no room is queued
-// without stash (u recomputed from p, m', v', which the same thread stored
-// in pass 1); only with the FIFO full does a chunk go to a global overflow
-// list, processed at the end by any CTA.
+// on the CTAs holding chunks of that tensor run their pass 2: up to two
+// FIFO entries beside every pass-1 chunk (their loads issued before the
+// pass-1 math, which reads only shared memory), and in iterations without
+// a pass-1 chunk as many as the stage's four areas hold (p, and m', v' of
+// entries without stash, bulk-copied after a proxy fence). No grid-wide
+// barrier: a chunk waits only for its own tensor. A chunk for which the
+// ring has no room is queued without stash (u recomputed from p, m', v',
+// which the same thread stored in pass 1); only with the FIFO full does a
+// chunk go to a global overflow list, processed at the end by any CTA.
 //
-// Control never stalls the streaming warps on a global round trip. After the
-// one CTA barrier of an iteration, lane 0 of warp 0 ("claims") and of warp 1
-// ("books") do the bookkeeping, then join the next iteration:
-//   claims  fills the slot of iteration i + kLambStages and issues its bulk
-//           copies into the stage iteration i freed, for a chunk claimed two
-//           steps earlier whose descriptor it fetched with cp.async one step
-//           earlier; probes the ready word of the FIFO head's tensor (the
-//           result is used one step later);
-//   books   stores the chunk's norm partial and counts it for its tensor
-//           (the count is checked one step later, or at once for the CTA's
-//           last chunk), and completes a tensor whose count is full.
+// Warps. kLambDataWarps data warps run the iterations on their own, waiting
+// only on the stage's `full` mbarrier and reporting each iteration on its
+// `empty` mbarrier; two control warps keep every global round trip off
+// them:
+//   claims  once iteration i is done, fills the slot of iteration
+//           i + kLambStages and issues its bulk copies into the stage i
+//           freed, for a chunk claimed two steps earlier whose descriptor
+//           it fetched with cp.async; probes the ready word of the FIFO
+//           head's tensor while it fills;
+//   books   publishes each iteration's norm partial, counts it for its
+//           tensor and completes a tensor whose count is full.
 // No fences on this path: partials and ready words carry the launch's tag
 // in the same 64-bit word as the value (single-copy atomic), so a reader
 // that sees the tag sees the value; readers of a partial spin on the tag.
