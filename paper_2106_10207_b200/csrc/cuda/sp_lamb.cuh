@@ -602,18 +602,13 @@ struct StreamShared {
 // pass-1 chunk they hold pass-2 entries.
 __device__ __forceinline__ int stage_area(int k) { return k == 0 ? 0 : kLambStageG + (k - 1) * kLambArea; }
 
-// Claims lane: chunk c (descriptor ch; >= nchunks: none) into slot q,
-// its body g, p, m, v copied into stage stg (counted on bar) and its pass 2
-// queued. Wire formats narrower than 16 B per vector are fetched as an
-// aligned superset; sh.goff[q] is the offset of the chunk's first body
-// gradient in the g area.
+// Claims lane: the bulk copies of chunk ch's body (g, p, m, v, and the
+// q8 block scales) into stage stg, counted on bar, for slot q. Wire formats
+// narrower than 16 B per vector are fetched as an aligned superset;
+// sh.goff[q] is the offset of the chunk's first body gradient in the g area.
 template <int W, bool FP>
-__device__ __forceinline__ void stream_fill(const LambArgs& a, const LambPlan& pl, Ctl& k, int q, int c,
-                                            const Chunk& ch, unsigned char* stg, unsigned long long* bar,
-                                            StreamShared& sh) {
-  sh.idx[q] = c;
-  if (c >= pl.nchunks) return;
-  sh.desc[q] = ch;
+__device__ __forceinline__ void stage_copies(const LambArgs& a, const Chunk& ch, unsigned char* stg,
+                                             unsigned long long* bar, StreamShared& sh, int q) {
   const int64_t b0 = ch.start + ch.head;
   const unsigned nb = (unsigned)ch.nbody4;
   if (nb) {
@@ -647,6 +642,20 @@ __device__ __forceinline__ void stream_fill(const LambArgs& a, const LambPlan& p
     bulk_g2s(stg + kLambStageG + kLambArea, a.m + b0, 16 * nb, bar);
     bulk_g2s(stg + kLambStageG + 2 * kLambArea, a.v + b0, 16 * nb, bar);
   }
+}
+
+// Claims lane: chunk c (descriptor ch; >= nchunks: none) into slot q with
+// its pass 2 queued; its copies issued here too unless the caller did.
+template <int W, bool FP>
+__device__ __forceinline__ void stream_fill(const LambArgs& a, const LambPlan& pl, Ctl& k, int q, int c,
+                                            const Chunk& ch, unsigned char* stg, unsigned long long* bar,
+                                            StreamShared& sh, bool copy = true) {
+  sh.idx[q] = c;
+  if (c >= pl.nchunks) return;
+  sh.desc[q] = ch;
+  if (copy) stage_copies<W, FP>(a, ch, stg, bar, sh, q);
+  const int64_t b0 = ch.start + ch.head;
+  const unsigned nb = (unsigned)ch.nbody4;
   int off = -2;
   if (k.ftail - k.fhead < kFifo) {
     off = ring_alloc(k.ring, pl.cap, ch.start, ch.len);
@@ -883,6 +892,14 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
       mbar_wait(&sh.empty[stage], (unsigned)(it / kLambStages) & 1u);
       sh.iters_done = it + 1;  // for the books lane (a counter: it may lag several phases)
       LAMB_ITER(it, 5);
+      // the copies of iteration it + stages first: the stage is free, the
+      // descriptor was fetched two steps ago
+      const int sq = (it + kLambStages) % kSlots;
+      const int b = it & 1;
+      const int c = k.pdesc[b];
+      cp_async_wait_1();
+      unsigned char* stg = stages + (size_t)stage * kLambStageBytes;
+      if (c < pl.nchunks) stage_copies<W, FP>(a, sh.pdesc[b], stg, &sh.full[stage], sh, sq);
       const int n2 = sh.n2[q];
       if (n2 > 0) {  // free the entries pass 2 just finished and their ring regions
         for (int j = 0; j < n2; ++j) {
@@ -895,7 +912,6 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
             break;
           }
       }
-      const int sq = (it + kLambStages) % kSlots;
       // the slot was last used by iteration it + stages - kSlots: the books
       // lane must be done with it
       while (sh.books_done < it + kLambStages - kSlots + 1) {
@@ -906,11 +922,7 @@ __device__ void stream_loop(const LambArgs& a, const LambScalars& s, const LambP
       if (k.fnext < k.ftail && sh.fifo[k.fnext % kFifo].tensor != k.ready_t)
         k.probe_t = sh.fifo[k.fnext % kFifo].tensor;
       probe = ld_relaxed_u64(pl.ready(k.probe_t >= 0 ? k.probe_t : 0));
-      const int b = it & 1;  // the buffer fetched two steps ago
-      const int c = k.pdesc[b];
-      cp_async_wait_1();
-      unsigned char* stg = stages + (size_t)stage * kLambStageBytes;
-      stream_fill<W, FP>(a, pl, k, sq, c, sh.pdesc[b], stg, &sh.full[stage], sh);
+      stream_fill<W, FP>(a, pl, k, sq, c, sh.pdesc[b], stg, &sh.full[stage], sh, false);
       // the descriptor of the claim issued last step; claim again
       const int cn = k.claims_done ? pl.nchunks : pend;
       if (cn >= pl.nchunks) k.claims_done = 1;
