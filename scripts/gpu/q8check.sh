@@ -1,3 +1,4 @@
+# q8 parity tests and N=1 q8/fp16 bench lines
 mkdir -p gpurun_out/q8
 export SP_SKIP_BUILD=1
 timeout 600 python -m pytest tests/test_round_gpu.py -q --timeout 120 -k "q8" > gpurun_out/q8/test.log 2>&1; echo "pytest rc=$?" >> gpurun_out/q8/test.log
